@@ -1,0 +1,173 @@
+"""ctypes declarations of include/pba_gpu.h and a loader for the in-tree libraries.
+
+Both the product library (``lib/libpba_gpu.so``) and the CPU oracle
+(``oracle/_build/liboracle.so``, TEST INFRASTRUCTURE ONLY) export the same call
+set (prefixes ``pba_gpu_`` / ``pba_oracle_``), so ``Backend`` binds either one.
+The product path never falls back to the oracle: loading the GPU library fails
+loudly when it has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+REPO = _PKG.parent
+GPU_LIB = _PKG / "lib" / "libpba_gpu.so"
+ORACLE_LIB = REPO / "oracle" / "_build" / "liboracle.so"
+
+# status codes (pba_gpu.h)
+PBA_OK = 0
+PBA_E_EMPTY_PROBLEM = 1
+PBA_E_OUT_OF_BOUNDS = 2
+PBA_E_INVALID_DEPTH = 3
+PBA_E_DEGENERATE_DEPTH = 4
+PBA_E_SINGULAR_HESSIAN = 5
+PBA_E_CUDA = 6
+PBA_E_ARG = 7
+PBA_E_STATE = 8
+PBA_E_SPEC_INFEASIBLE = 9
+
+PBA_K_NAMES = ["obs_pass", "schur", "cholesky", "trisolve", "ic_build", "reduce"]
+
+i32, i64, f64, u8, u64 = C.c_int32, C.c_int64, C.c_double, C.c_uint8, C.c_uint64
+P = C.POINTER
+
+
+class pba_image(C.Structure):
+    _fields_ = [("width", i32), ("height", i32), ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64),
+                ("data", P(C.c_float))]
+
+
+class pba_problem(C.Structure):
+    _fields_ = [("ref", pba_image), ("num_frames", i32), ("targets", P(pba_image)), ("pose_R", P(f64)),
+                ("pose_t", P(f64)), ("num_points", i32), ("anchors_px", P(f64)), ("inv_depths", P(f64)),
+                ("pattern_size", i32), ("pattern", P(i32)), ("obs_ptr", P(i64)), ("obs_frame", P(i32))]
+
+
+class pba_config(C.Structure):
+    _fields_ = [("gamma", f64), ("threshold_px", f64), ("max_iters", i32), ("lambda0", f64),
+                ("max_bad_steps", i32), ("normalize_depth_gauge", i32), ("refresh_ic_hessian", i32),
+                ("record_snapshots", i32)]
+
+
+class pba_iter_stats(C.Structure):
+    _fields_ = [("iter", i32), ("energy", f64), ("max_update_px", f64), ("wall_ms", f64),
+                ("hessian_builds", i32), ("hessian_factorizations", i32), ("num_active", i64),
+                ("accepted", i32)]
+
+
+class pba_report(C.Structure):
+    _fields_ = [("converged", i32), ("diverged", i32), ("iterations", i32), ("hessian_builds", i32),
+                ("hessian_factorizations", i32), ("rejected_steps", i32), ("final_energy", f64),
+                ("total_wall_ms", f64), ("masked_residuals", i64), ("final_R", P(f64)), ("final_t", P(f64)),
+                ("final_inv_depths", P(f64)), ("iters", P(pba_iter_stats)), ("iters_capacity", i32),
+                ("num_iters", i32), ("snap_R", P(f64)), ("snap_t", P(f64)), ("snap_d", P(f64)),
+                ("message", C.c_char * 256)]
+
+
+class pba_energy_result(C.Structure):
+    _fields_ = [("energy", f64), ("num_active", i64), ("num_out_of_bounds", i64)]
+
+
+class pba_oracle_scene_spec(C.Structure):
+    _fields_ = [("width", i32), ("height", i32), ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64),
+                ("octaves", i32), ("base_wavelength_px", f64), ("lo", f64), ("hi", f64),
+                ("geometry_kind", i32), ("base_depth", f64), ("amplitude", f64), ("wavelength_px", f64),
+                ("trajectory_kind", i32), ("frames", i32), ("span_deg", f64), ("extent", f64 * 3),
+                ("num_points", i32), ("patch_radius", i32), ("seed", u64), ("supersample", i32)]
+
+
+VP = C.c_void_p
+_COMMON = {
+    # name: (restype, argtypes)
+    "create": (C.c_int, [P(pba_problem), P(VP)]),
+    "destroy": (None, [VP]),
+    "last_error": (C.c_char_p, [VP]),
+    "num_observations": (i64, [VP]),
+    "set_params": (C.c_int, [VP, P(f64), P(f64), P(f64)]),
+    "get_params": (C.c_int, [VP, P(f64), P(f64), P(f64)]),
+    "energy": (C.c_int, [VP, f64, P(u8), P(pba_energy_result), P(f64), P(u8)]),
+    "ic_build": (C.c_int, [VP, P(pba_config)]),
+    "ic_gradient": (C.c_int, [VP, P(f64)]),
+    "ic_compute_step": (C.c_int, [VP, P(f64)]),
+    "ic_solve_step": (C.c_int, [VP, P(f64), P(f64)]),
+    "ic_factorize": (C.c_int, [VP, f64]),
+    "ic_hessian": (C.c_int, [VP, P(f64), P(f64), P(f64), P(f64)]),
+    "warning_count": (C.c_int, [VP]),
+    "warning": (C.c_int, [VP, C.c_int, C.c_char_p, C.c_int]),
+    "ic_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),
+    "fc_build": (C.c_int, [VP, f64, P(f64), P(f64), P(f64), P(f64)]),
+    "fc_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),
+    "solve_normal_equations_schur": (C.c_int, [i32, i32, P(i64), P(i32), P(f64), P(f64), P(f64), P(f64), f64,
+                                                P(f64)]),
+    "apply_update": (C.c_int, [VP, C.c_int, P(f64), P(f64), P(f64), P(f64), P(C.c_int)]),
+    "max_reproj_update": (C.c_int, [VP, P(f64), P(f64), P(f64), P(f64)]),
+    "normalize_gauge": (C.c_int, [VP]),
+}
+_GPU_ONLY = {
+    "ic_begin": (C.c_int, [VP, P(pba_config)]),
+    "fc_begin": (C.c_int, [VP, P(pba_config)]),
+    "iterate": (C.c_int, [VP, P(pba_iter_stats), P(C.c_int)]),
+    "end": (C.c_int, [VP, P(pba_report)]),
+    "stream": (VP, [VP]),
+    "set_profiling": (C.c_int, [VP, C.c_int]),
+    "kernel_times": (C.c_int, [VP, P(i64), P(f64)]),
+    "device_bytes": (i64, [VP]),
+}
+_ORACLE_ONLY = {
+    "solve_normal_equations_dense": _COMMON["solve_normal_equations_schur"],
+    "scene_spec_default": (None, [P(pba_oracle_scene_spec)]),
+    "render_sequence": (C.c_int, [P(pba_oracle_scene_spec), P(f64), P(f64), P(f64), P(f64), P(f64), P(f64),
+                                  C.c_char_p, C.c_int]),
+    "perturb_parameters": (C.c_int, [i32, P(f64), P(f64), i32, P(f64), f64, u64]),
+}
+
+_cache: dict = {}
+
+
+class Backend:
+    """A loaded library with uniformly named functions (``self.create`` ...)."""
+
+    def __init__(self, kind: str):
+        self.kind = kind
+        if kind == "gpu":
+            path, prefix, extra = GPU_LIB, "pba_gpu_", _GPU_ONLY
+        elif kind == "oracle":
+            path, prefix, extra = ORACLE_LIB, "pba_oracle_", _ORACLE_ONLY
+        else:
+            raise ValueError(kind)
+        if not path.exists():
+            raise RuntimeError(
+                f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                f"(the {kind} path has no fallback)")
+        self.lib = C.CDLL(str(path))
+        self.path = path
+        for name, (res, args) in {**_COMMON, **extra}.items():
+            fn = getattr(self.lib, prefix + name)
+            fn.restype = res
+            fn.argtypes = args
+            setattr(self, name, fn)
+        if kind == "gpu":
+            self.status_string = self.lib.pba_status_string
+            self.status_string.restype = C.c_char_p
+            self.status_string.argtypes = [C.c_int]
+        self.config_default = self.lib.pba_config_default if kind == "gpu" else None
+
+
+def backend(kind: str) -> Backend:
+    if kind not in _cache:
+        _cache[kind] = Backend(kind)
+    return _cache[kind]
+
+
+def default_config() -> pba_config:
+    """SolverConfig{} (solver.hpp:45-54)."""
+    return pba_config(gamma=0.03, threshold_px=5e-3, max_iters=200, lambda0=1e-6, max_bad_steps=8,
+                      normalize_depth_gauge=1, refresh_ic_hessian=0, record_snapshots=0)
+
+
+def lib_paths() -> dict:
+    return {"gpu": str(GPU_LIB), "oracle": str(ORACLE_LIB), "exists_gpu": GPU_LIB.exists(),
+            "exists_oracle": ORACLE_LIB.exists(), "pid": os.getpid()}

@@ -1,0 +1,643 @@
+// Host engine: device state of one PBA problem + the reference's LM control flow.
+// Control flow mirrors /root/reference/proj/src/solver.cpp line by line (cited);
+// every per-pixel / per-point / per-frame computation is a kernel in kernels.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "engine.hpp"
+
+namespace pba_b200 {
+
+namespace {
+
+uint32_t morton_key(double u, double v) {
+  auto part = [](uint32_t x) {
+    x &= 0xffff;
+    x = (x | (x << 8)) & 0x00FF00FF;
+    x = (x | (x << 4)) & 0x0F0F0F0F;
+    x = (x | (x << 2)) & 0x33333333;
+    x = (x | (x << 1)) & 0x55555555;
+    return x;
+  };
+  const double cu = std::min(std::max(std::floor(u), 0.0), 65535.0);
+  const double cv = std::min(std::max(std::floor(v), 0.0), 65535.0);
+  return part(static_cast<uint32_t>(cu)) | (part(static_cast<uint32_t>(cv)) << 1);
+}
+
+int next_pow2(int p) {
+  int g = 1;
+  while (g < p) g <<= 1;
+  return g;
+}
+
+}  // namespace
+
+template <typename T>
+void DBuf<T>::alloc(size_t count) {
+  if (count == n && p) return;
+  release();
+  if (count == 0) return;
+  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  n = count;
+}
+template <typename T>
+void DBuf<T>::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  n = 0;
+}
+
+// =====================================================================================
+// construction: upload the ProblemState (solver.hpp:33-43) into the device layout
+// =====================================================================================
+Engine::Engine(const pba_problem* p) {
+  if (!p) throw PbaError(PBA_E_ARG, "null problem");
+  if (p->num_frames < 0 || p->num_points < 0) throw PbaError(PBA_E_ARG, "negative sizes");
+  if (p->pattern_size < 1 || p->pattern_size > 32 || !p->pattern)
+    throw PbaError(PBA_E_ARG, "pattern_size must be in [1, 32]");
+  N_ = p->num_points;
+  F_ = p->num_frames;
+  P_ = p->pattern_size;
+  pat_.P = P_;
+  for (int k = 0; k < P_; ++k) {
+    pat_.dx[k] = p->pattern[2 * k];
+    pat_.dy[k] = p->pattern[2 * k + 1];
+  }
+  if (!p->ref.data || p->ref.width < 4 || p->ref.height < 4) throw PbaError(PBA_E_ARG, "bad reference image");
+  if (F_ > 0 && (!p->targets || !p->pose_R || !p->pose_t)) throw PbaError(PBA_E_ARG, "missing frames");
+  if (N_ > 0 && (!p->anchors_px || !p->inv_depths)) throw PbaError(PBA_E_ARG, "missing points");
+  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+
+  // ---- images: one fp32 buffer, reference first ----
+  std::vector<int64_t> off(F_ + 2, 0);
+  off[1] = static_cast<int64_t>(p->ref.width) * p->ref.height;
+  for (int f = 0; f < F_; ++f) {
+    const pba_image& im = p->targets[f];
+    if (!im.data || im.width < 4 || im.height < 4) throw PbaError(PBA_E_ARG, "bad target image");
+    off[f + 2] = off[f + 1] + static_cast<int64_t>(im.width) * im.height;
+  }
+  images_.alloc(off[F_ + 1]);
+  ck(cudaMemcpyAsync(images_.p, p->ref.data, off[1] * sizeof(float), cudaMemcpyHostToDevice, stream_), "upload ref");
+  for (int f = 0; f < F_; ++f)
+    ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
+                       cudaMemcpyHostToDevice, stream_),
+       "upload target");
+  ref_ = FrameD{images_.p, p->ref.width, p->ref.height, p->ref.fx, p->ref.fy, p->ref.cx, p->ref.cy};
+  frames_h_.resize(F_);
+  for (int f = 0; f < F_; ++f) {
+    const pba_image& im = p->targets[f];
+    frames_h_[f] = FrameD{images_.p + off[f + 1], im.width, im.height, im.fx, im.fy, im.cx, im.cy};
+  }
+  frames_.alloc(std::max(F_, 1));
+  if (F_ > 0)
+    ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, stream_), "frames");
+
+  // ---- user observation list ----
+  uo_ptr_.assign(N_ + 1, 0);
+  if (p->obs_ptr) {
+    if (p->obs_ptr[0] != 0) throw PbaError(PBA_E_ARG, "obs_ptr[0] must be 0");
+    for (int n = 0; n <= N_; ++n) uo_ptr_[n] = p->obs_ptr[n];
+    uo_frame_.assign(p->obs_frame, p->obs_frame + uo_ptr_[N_]);
+    for (int n = 0; n < N_; ++n) {
+      if (uo_ptr_[n + 1] < uo_ptr_[n]) throw PbaError(PBA_E_ARG, "obs_ptr must be non-decreasing");
+      for (int64_t o = uo_ptr_[n]; o < uo_ptr_[n + 1]; ++o) {
+        if (uo_frame_[o] < 0 || uo_frame_[o] >= F_) throw PbaError(PBA_E_ARG, "obs_frame out of range");
+        if (o > uo_ptr_[n] && uo_frame_[o] <= uo_frame_[o - 1])
+          throw PbaError(PBA_E_ARG, "obs_frame must be strictly increasing per point");
+      }
+    }
+  } else {
+    for (int n = 0; n <= N_; ++n) uo_ptr_[n] = static_cast<int64_t>(n) * F_;
+    uo_frame_.resize(static_cast<size_t>(N_) * F_);
+    for (int n = 0; n < N_; ++n)
+      for (int f = 0; f < F_; ++f) uo_frame_[static_cast<size_t>(n) * F_ + f] = f;
+  }
+  NO_ = uo_ptr_[N_];
+  if (NO_ >= (int64_t(1) << 31) - 1) throw PbaError(PBA_E_ARG, "more than 2^31 observations");
+
+  // ---- internal point order: Morton order of the anchor pixel (texture locality) ----
+  perm_.resize(N_);
+  std::iota(perm_.begin(), perm_.end(), 0);
+  {
+    std::vector<uint32_t> key(N_);
+    for (int n = 0; n < N_; ++n) key[n] = morton_key(p->anchors_px[2 * n], p->anchors_px[2 * n + 1]);
+    std::stable_sort(perm_.begin(), perm_.end(), [&](int a, int b) { return key[a] < key[b]; });
+  }
+  iperm_.resize(N_);
+  for (int i = 0; i < N_; ++i) iperm_[perm_[i]] = i;
+
+  std::vector<int64_t> pm_ptr(N_ + 1, 0);
+  std::vector<int32_t> pm_frame(NO_);
+  for (int i = 0; i < N_; ++i) {
+    const int u = perm_[i];
+    const int64_t k = uo_ptr_[u + 1] - uo_ptr_[u];
+    pm_ptr[i + 1] = pm_ptr[i] + k;
+    std::copy(uo_frame_.begin() + uo_ptr_[u], uo_frame_.begin() + uo_ptr_[u + 1], pm_frame.begin() + pm_ptr[i]);
+  }
+  std::vector<int64_t> fm_ptr(F_ + 1, 0);
+  for (int64_t o = 0; o < NO_; ++o) ++fm_ptr[pm_frame[o] + 1];
+  for (int f = 0; f < F_; ++f) fm_ptr[f + 1] += fm_ptr[f];
+  std::vector<int64_t> cursor(fm_ptr.begin(), fm_ptr.end() - (F_ >= 0 ? 1 : 0));
+  std::vector<int32_t> fm_point(NO_), pm2fm(NO_);
+  for (int i = 0; i < N_; ++i)
+    for (int64_t o = pm_ptr[i]; o < pm_ptr[i + 1]; ++o) {
+      const int64_t q = cursor[pm_frame[o]]++;
+      fm_point[q] = i;
+      pm2fm[o] = static_cast<int32_t>(q);
+    }
+  uo2q_.resize(NO_);
+  for (int u = 0; u < N_; ++u) {
+    const int i = iperm_[u];
+    for (int64_t j = 0; j < uo_ptr_[u + 1] - uo_ptr_[u]; ++j) uo2q_[uo_ptr_[u] + j] = pm2fm[pm_ptr[i] + j];
+  }
+
+  // ---- frame-major tiles ----
+  const int G = next_pow2(P_);
+  const int ops = 256 / G;
+  const int64_t steps = std::min<int64_t>(64, std::max<int64_t>(1, (NO_ + 148 * 8 * ops - 1) / (148 * 8 * ops)));
+  const int64_t T = ops * steps;
+  std::vector<int32_t> tile_frame, ftile_ptr(F_ + 1, 0);
+  std::vector<int64_t> tq0, tq1;
+  for (int f = 0; f < F_; ++f) {
+    for (int64_t q = fm_ptr[f]; q < fm_ptr[f + 1]; q += T) {
+      tile_frame.push_back(f);
+      tq0.push_back(q);
+      tq1.push_back(std::min(q + T, fm_ptr[f + 1]));
+    }
+    ftile_ptr[f + 1] = static_cast<int32_t>(tile_frame.size());
+  }
+  const int ntiles = static_cast<int>(tile_frame.size());
+
+  auto up = [&](auto& buf, const auto& vec) {
+    using T2 = std::remove_reference_t<decltype(*buf.p)>;
+    buf.alloc(std::max<size_t>(vec.size(), 1));
+    if (!vec.empty())
+      ck(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T2), cudaMemcpyHostToDevice, stream_), "upload");
+  };
+  up(pm_ptr_, pm_ptr);
+  up(pm_frame_, pm_frame);
+  up(pm2fm_, pm2fm);
+  up(fm_ptr_, fm_ptr);
+  up(fm_point_, fm_point);
+  up(tile_frame_, tile_frame);
+  up(tile_q0_, tq0);
+  up(tile_q1_, tq1);
+  up(ftile_ptr_, ftile_ptr);
+  // pinned staging vectors must outlive the async copies
+  ck(cudaStreamSynchronize(stream_), "sync upload");
+
+  ov_.N = N_;
+  ov_.F = F_;
+  ov_.P = P_;
+  ov_.NO = NO_;
+  ov_.pm_ptr = pm_ptr_.p;
+  ov_.pm_frame = pm_frame_.p;
+  ov_.pm2fm = pm2fm_.p;
+  ov_.fm_ptr = fm_ptr_.p;
+  ov_.fm_point = fm_point_.p;
+  ov_.ntiles = ntiles;
+  ov_.tile_frame = tile_frame_.p;
+  ov_.tile_q0 = tile_q0_.p;
+  ov_.tile_q1 = tile_q1_.p;
+  ov_.ftile_ptr = ftile_ptr_.p;
+
+  // ---- points ----
+  std::vector<double2> anc(N_);
+  for (int i = 0; i < N_; ++i) anc[i] = make_double2(p->anchors_px[2 * perm_[i]], p->anchors_px[2 * perm_[i] + 1]);
+  up(anchor_, anc);
+  // template feasibility (solver.cpp:40-45): every template pixel inside [1, W-3] x [1, H-3]
+  template_ok_ = true;
+  for (int n = 0; n < N_ && template_ok_; ++n)
+    for (int k = 0; k < P_; ++k) {
+      const double u = p->anchors_px[2 * n] + static_cast<double>(pat_.dx[k]);
+      const double v = p->anchors_px[2 * n + 1] + static_cast<double>(pat_.dy[k]);
+      if (!(u >= 1.0 && u <= p->ref.width - 3 && v >= 1.0 && v <= p->ref.height - 3)) {
+        template_ok_ = false;
+        break;
+      }
+    }
+  ck(cudaStreamSynchronize(stream_), "sync upload");
+
+  const size_t nN = std::max(N_, 1), nF = std::max(F_, 1), nO = std::max<int64_t>(NO_, 1);
+  pose_state_.alloc(nF);
+  pose_cur_.alloc(nF);
+  pose_cand_.alloc(nF);
+  pose0_.alloc(nF);
+  d_state_.alloc(nN);
+  d_cur_.alloc(nN);
+  d_cand_.alloc(nN);
+  d0_.alloc(nN);
+  mask_[0].alloc(nO);
+  mask_[1].alloc(nO);
+  scratch_bits_.alloc(nO);
+  rec_.alloc(nO);
+  s_n_.alloc(nN);
+  dx_n_.alloc(nN);
+  xp_.alloc(6 * nF);
+  g_tmp_.alloc(6 * nF + nN);
+  for (int b = 0; b < 2; ++b) {
+    gn_[b].alloc(nN);
+    gf_[b].alloc(6 * nF);
+    rhs_[b].alloc(6 * nF);
+  }
+  partial_.alloc(static_cast<size_t>(std::max(ntiles, 1)) * PT_STRIDE);
+  partial_cf_.alloc(static_cast<size_t>(std::max(ntiles, 1)) * 8);
+  partial_bs_.alloc(static_cast<size_t>(std::max(backsub_blocks(N_), 1)) * 4);
+  partial_pt_.alloc(static_cast<size_t>(std::max(point_blocks(N_), 1)) * 2);
+  partial_mr_.alloc(1024);
+  S_.alloc(static_cast<size_t>(36) * nF * nF);
+  status_.alloc(1);
+  flags_.alloc(4);
+  ck(cudaMallocHost(&status_h_, sizeof(Status)), "pinned");
+  ck(cudaMallocHost(&flags_h_, 4 * sizeof(int)), "pinned");
+
+  R_state_.assign(p->pose_R, p->pose_R + 9 * F_);
+  t_state_.assign(p->pose_t, p->pose_t + 3 * F_);
+  set_params(p->pose_R, p->pose_t, p->inv_depths);
+}
+
+Engine::~Engine() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto& pd : pending_) {
+    cudaEventDestroy(pd.a);
+    cudaEventDestroy(pd.b);
+  }
+  if (status_h_) cudaFreeHost(status_h_);
+  if (flags_h_) cudaFreeHost(flags_h_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+int64_t Engine::device_bytes() const {
+  int64_t b = images_.bytes() + J_.bytes() + S_.bytes() + rec_.bytes() + partial_.bytes();
+  for (int i = 0; i < 2; ++i) b += B_[i].bytes() + D_[i].bytes() + mask_[i].bytes();
+  return b + pm2fm_.bytes() + fm_point_.bytes() + pm_frame_.bytes();
+}
+
+// =====================================================================================
+// parameters
+// =====================================================================================
+void Engine::upload_poses(DBuf<PoseD>& dst, const double* R, const double* t) {
+  std::vector<PoseD> h(F_);
+  for (int f = 0; f < F_; ++f) {
+    std::memcpy(h[f].R, R + 9 * f, 9 * sizeof(double));
+    std::memcpy(h[f].t, t + 3 * f, 3 * sizeof(double));
+  }
+  if (F_ > 0) ck(cudaMemcpyAsync(dst.p, h.data(), F_ * sizeof(PoseD), cudaMemcpyHostToDevice, stream_), "poses");
+  ck(cudaStreamSynchronize(stream_), "sync");
+}
+void Engine::upload_depths_user(DBuf<double>& dst, const double* d_user) {
+  std::vector<double> h(N_);
+  for (int i = 0; i < N_; ++i) h[i] = d_user[perm_[i]];
+  if (N_ > 0) ck(cudaMemcpyAsync(dst.p, h.data(), N_ * sizeof(double), cudaMemcpyHostToDevice, stream_), "depths");
+  ck(cudaStreamSynchronize(stream_), "sync");
+}
+void Engine::download_poses(const DBuf<PoseD>& src, double* R, double* t) {
+  std::vector<PoseD> h(F_);
+  if (F_ > 0) ck(cudaMemcpyAsync(h.data(), src.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToHost, stream_), "poses");
+  ck(cudaStreamSynchronize(stream_), "sync");
+  for (int f = 0; f < F_; ++f) {
+    if (R) std::memcpy(R + 9 * f, h[f].R, 9 * sizeof(double));
+    if (t) std::memcpy(t + 3 * f, h[f].t, 3 * sizeof(double));
+  }
+}
+void Engine::download_depths_user(const DBuf<double>& src, double* d_user) {
+  std::vector<double> h(N_);
+  if (N_ > 0) ck(cudaMemcpyAsync(h.data(), src.p, N_ * sizeof(double), cudaMemcpyDeviceToHost, stream_), "depths");
+  ck(cudaStreamSynchronize(stream_), "sync");
+  for (int i = 0; i < N_; ++i) d_user[perm_[i]] = h[i];
+}
+
+void Engine::set_params(const double* R, const double* t, const double* d) {
+  R_state_.assign(R, R + 9 * F_);
+  t_state_.assign(t, t + 3 * F_);
+  d_state_.alloc(std::max(N_, 1));
+  upload_poses(pose_state_, R, t);
+  upload_depths_user(d_state_, d);
+}
+
+void Engine::get_params(double* R, double* t, double* d) const {
+  auto* self = const_cast<Engine*>(this);
+  self->download_poses(pose_state_, R, t);
+  self->download_depths_user(d_state_, d);
+}
+
+// =====================================================================================
+// small helpers
+// =====================================================================================
+cudaEvent_t Engine::ev_begin(int kid) {
+  (void)kid;
+  if (!prof_) return nullptr;
+  cudaEvent_t a;
+  if (!ev_pool_.empty()) {
+    a = ev_pool_.back();
+    ev_pool_.pop_back();
+  } else {
+    ck(cudaEventCreate(&a), "event");
+  }
+  ck(cudaEventRecord(a, stream_), "event record");
+  return a;
+}
+void Engine::ev_end(int kid, cudaEvent_t a) {
+  if (!prof_ || !a) return;
+  cudaEvent_t b;
+  if (!ev_pool_.empty()) {
+    b = ev_pool_.back();
+    ev_pool_.pop_back();
+  } else {
+    ck(cudaEventCreate(&b), "event");
+  }
+  ck(cudaEventRecord(b, stream_), "event record");
+  pending_.push_back({kid, a, b});
+}
+void Engine::drain_profile() {
+  for (auto& pd : pending_) {
+    float ms = 0.f;
+    ck(cudaEventSynchronize(pd.b), "event sync");
+    ck(cudaEventElapsedTime(&ms, pd.a, pd.b), "elapsed");
+    kms_[pd.kid] += ms;
+    kcount_[pd.kid] += 1;
+    ev_pool_.push_back(pd.a);
+    ev_pool_.push_back(pd.b);
+  }
+  pending_.clear();
+}
+void Engine::set_profiling(bool on) {
+  drain_profile();
+  prof_ = on;
+  for (int i = 0; i < PBA_K_COUNT; ++i) {
+    kcount_[i] = 0;
+    kms_[i] = 0.0;
+  }
+}
+void Engine::kernel_times(int64_t* counts, double* total_ms) {
+  ck(cudaStreamSynchronize(stream_), "sync");
+  drain_profile();
+  for (int i = 0; i < PBA_K_COUNT; ++i) {
+    if (counts) counts[i] = kcount_[i];
+    if (total_ms) total_ms[i] = kms_[i];
+  }
+}
+
+void Engine::check_template() const {
+  if (!template_ok_) throw PbaError(PBA_E_OUT_OF_BOUNDS, "template patch pixel outside reference image");
+}
+
+Status Engine::read_status() {
+  ck(cudaMemcpyAsync(status_h_, status_.p, sizeof(Status), cudaMemcpyDeviceToHost, stream_), "status");
+  ck(cudaMemcpyAsync(flags_h_, flags_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_), "flags");
+  ck(cudaStreamSynchronize(stream_), "sync status");
+  ck(cudaGetLastError(), "kernel");
+  drain_profile();
+  return *status_h_;
+}
+int Engine::read_flag(int i) {
+  ck(cudaMemcpyAsync(flags_h_, flags_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_), "flags");
+  ck(cudaStreamSynchronize(stream_), "sync flags");
+  ck(cudaGetLastError(), "kernel");
+  drain_profile();
+  return flags_h_[i];
+}
+void Engine::clear_flags() { ck(cudaMemsetAsync(flags_.p, 0, 4 * sizeof(int), stream_), "memset flags"); }
+
+ObsArgs Engine::obs_args(double gamma) const {
+  ObsArgs a{};
+  a.ov = ov_;
+  a.ref = ref_;
+  a.frames = frames_.p;
+  a.pat = pat_;
+  a.anchor = anchor_.p;
+  a.gamma = gamma;
+  a.partial = partial_.p;
+  a.rec = rec_.p;
+  return a;
+}
+
+void Engine::finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
+                      double* rhs, const double* g_f_in, double* H, bool status) {
+  FinalizeArgs f{};
+  f.ov = ov_;
+  f.partial = partial;
+  f.partial_cf = partial_cf;
+  f.partial_bs = bs ? partial_bs_.p : nullptr;
+  f.nbs = backsub_blocks(N_);
+  f.partial_pt = pt ? partial_pt_.p : nullptr;
+  f.npt = point_blocks(N_);
+  f.want_h = want_h ? 1 : 0;
+  f.g_f = g_f;
+  f.rhs = rhs;
+  f.g_f_in = g_f_in;
+  f.H = H;
+  f.status = status ? status_.p : nullptr;
+  const auto e = ev_begin(PBA_K_REDUCE);
+  launch_finalize(f, stream_);
+  ev_end(PBA_K_REDUCE, e);
+}
+
+// =====================================================================================
+// energy_eval (solver.cpp:229-244)
+// =====================================================================================
+void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, double* residuals, uint8_t* active) {
+  check_template();
+  ObsArgs a = obs_args(gamma);
+  a.pose_eval = pose_state_.p;
+  a.d_eval = d_state_.p;
+  a.active_out = scratch_bits_.p;
+  if (mask) {
+    std::vector<uint32_t> bits(NO_, 0);
+    for (int64_t ou = 0; ou < NO_; ++ou) {
+      uint32_t b = 0;
+      for (int k = 0; k < P_; ++k)
+        if (mask[ou * P_ + k]) b |= 1u << k;
+      bits[uo2q_[ou]] = b;
+    }
+    DBuf<uint32_t> mb;
+    mb.alloc(std::max<int64_t>(NO_, 1));
+    if (NO_ > 0) ck(cudaMemcpyAsync(mb.p, bits.data(), NO_ * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_), "mask");
+    a.mask_in = mb.p;
+    if (residuals) {
+      r_out_.alloc(std::max<int64_t>(NO_ * P_, 1));
+      ck(cudaMemsetAsync(r_out_.p, 0, r_out_.bytes(), stream_), "memset r");
+      a.r_out = r_out_.p;
+    }
+    const auto e = ev_begin(PBA_K_OBS_PASS);
+    launch_obs(OBS_ENERGY, a, stream_);
+    ev_end(PBA_K_OBS_PASS, e);
+    finalize(partial_.p, nullptr, false, false, false, nullptr, nullptr, nullptr, nullptr, true);
+    ck(cudaStreamSynchronize(stream_), "sync");
+  } else {
+    if (residuals) {
+      r_out_.alloc(std::max<int64_t>(NO_ * P_, 1));
+      ck(cudaMemsetAsync(r_out_.p, 0, r_out_.bytes(), stream_), "memset r");
+      a.r_out = r_out_.p;
+    }
+    const auto e = ev_begin(PBA_K_OBS_PASS);
+    launch_obs(OBS_ENERGY, a, stream_);
+    ev_end(PBA_K_OBS_PASS, e);
+    finalize(partial_.p, nullptr, false, false, false, nullptr, nullptr, nullptr, nullptr, true);
+  }
+  const Status s = read_status();
+  if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");
+  if (out) {
+    out->energy = s.energy;
+    out->num_active = static_cast<int64_t>(s.num_active);
+    out->num_out_of_bounds = static_cast<int64_t>(s.num_oob);
+  }
+  if (residuals) {
+    std::vector<double> r(NO_ * P_);
+    if (NO_ > 0) ck(cudaMemcpy(r.data(), r_out_.p, r.size() * sizeof(double), cudaMemcpyDeviceToHost), "r");
+    for (int64_t ou = 0; ou < NO_; ++ou)
+      for (int k = 0; k < P_; ++k) residuals[ou * P_ + k] = r[static_cast<int64_t>(uo2q_[ou]) * P_ + k];
+  }
+  if (active) {
+    std::vector<uint32_t> bits(NO_);
+    if (NO_ > 0) ck(cudaMemcpy(bits.data(), scratch_bits_.p, NO_ * sizeof(uint32_t), cudaMemcpyDeviceToHost), "bits");
+    for (int64_t ou = 0; ou < NO_; ++ou)
+      for (int k = 0; k < P_; ++k) active[ou * P_ + k] = (bits[uo2q_[ou]] >> k) & 1u;
+  }
+}
+
+// =====================================================================================
+// IC pieces
+// =====================================================================================
+void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
+                     double lambda, const PoseD* pose_old, const double* d_old) {
+  // eval_residuals + assemble_gradient (solver.cpp:436-468) + solve_step rhs (:407-416)
+  ObsArgs a = obs_args(ic_.cfg.gamma);
+  a.pose_eval = pose;
+  a.d_eval = d;
+  a.pose_old = pose_old;
+  a.d_old = d_old;
+  a.mask_in = mask_in;
+  a.active_out = active_out;
+  a.J = J_.p;
+  auto e = ev_begin(PBA_K_OBS_PASS);
+  launch_obs(OBS_IC, a, stream_);
+  ev_end(PBA_K_OBS_PASS, e);
+  PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
+  e = ev_begin(PBA_K_REDUCE);
+  launch_point(pa, stream_);
+  launch_cf(ov_, Bic_.p, s_n_.p, partial_cf_.p, stream_);
+  ev_end(PBA_K_REDUCE, e);
+  finalize(partial_.p, partial_cf_.p, pose_old != nullptr, true, false, gf_[buf].p, rhs_[buf].p, nullptr, nullptr,
+           true);
+}
+
+void Engine::ic_rescale_rhs(int buf, double lambda) {
+  PointArgs pa{ov_, PT_RESCALE, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
+  const auto e = ev_begin(PBA_K_REDUCE);
+  launch_point(pa, stream_);
+  launch_cf(ov_, Bic_.p, s_n_.p, partial_cf_.p, stream_);
+  ev_end(PBA_K_REDUCE, e);
+  finalize(nullptr, partial_cf_.p, false, false, false, nullptr, rhs_[buf].p, gf_[buf].p, nullptr, false);
+}
+
+bool Engine::factor_reduced(const double* H, const double* B, const double* D, double lambda) {
+  const int n = 6 * F_;
+  clear_flags();
+  auto e = ev_begin(PBA_K_SCHUR);
+  launch_schur(ov_, H, B, D, lambda, S_.p, stream_);
+  ev_end(PBA_K_SCHUR, e);
+  e = ev_begin(PBA_K_CHOLESKY);
+  launch_cholesky(S_.p, n, flags_.p, stream_);
+  ev_end(PBA_K_CHOLESKY, e);
+  return read_flag(0) == 0;
+}
+
+// IcSolver::factorize (solver.cpp:370-402)
+void Engine::ic_factorize_loop(double lambda) {
+  for (int attempt = 0; attempt < 60; ++attempt) {
+    ++ic_.factorizations;
+    if (factor_reduced(Hic_.p, Bic_.p, Dic_.p, lambda)) {
+      ic_.lambda = lambda;
+      return;
+    }
+    lambda *= 10.0;
+  }
+  throw PbaError(PBA_E_SINGULAR_HESSIAN, "SingularHessian: damping retries exhausted");
+}
+
+void Engine::solve_xp(const double* rhs) {
+  const auto e = ev_begin(PBA_K_TRISOLVE);
+  if (F_ > 0) launch_trisolve(S_.p, 6 * F_, rhs, xp_.p, flags_.p + 1, stream_);
+  ev_end(PBA_K_TRISOLVE, e);
+}
+
+// IcSolver::build (solver.cpp:254-368)
+void Engine::ic_build(const pba_config* cfg) {
+  ic_ = SolverState{};
+  if (cfg) {
+    ic_.cfg = *cfg;
+  } else {
+    pba_config_default(&ic_.cfg);
+  }
+  ic_.lambda = ic_.cfg.lambda0;
+  check_template();
+  if (F_ > 0) ck(cudaMemcpyAsync(pose0_.p, pose_state_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p0");
+  if (N_ > 0) ck(cudaMemcpyAsync(d0_.p, d_state_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d0");
+  for (int f = 0; f < F_; ++f) {  // :265-271
+    const double* t = &t_state_[3 * f];
+    if (std::sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]) < 1e-9)
+      ic_.warnings.push_back("frame " + std::to_string(f) +
+                             ": zero initial translation, inverse depth unobservable from this frame");
+  }
+  const size_t nO = std::max<int64_t>(NO_, 1);
+  J_.alloc(static_cast<size_t>(7) * nO * P_);
+  Bic_.alloc(6 * nO);
+  Dic_.alloc(std::max(N_, 1));
+  Hic_.alloc(21 * std::max(F_, 1));
+
+  ObsArgs a = obs_args(ic_.cfg.gamma);
+  a.pose_eval = pose0_.p;
+  a.d_eval = d0_.p;
+  a.pose0 = pose0_.p;
+  a.d0 = d0_.p;
+  a.active_out = mask_[0].p;
+  a.Jw = J_.p;
+  a.B_out = Bic_.p;
+  auto e = ev_begin(PBA_K_IC_BUILD);
+  launch_obs(OBS_BUILD, a, stream_);
+  ev_end(PBA_K_IC_BUILD, e);
+  PointArgs pa{ov_, PT_DONLY, rec_.p, nullptr, Dic_.p, 0.0, nullptr, partial_pt_.p};
+  e = ev_begin(PBA_K_REDUCE);
+  launch_point(pa, stream_);
+  ev_end(PBA_K_REDUCE, e);
+  finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, true);
+  const Status s = read_status();
+  if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
+  ic_.mcur = 0;
+  {  // :359-364 zero depth Hessian warnings, in user point order
+    std::vector<double> D(N_);
+    if (N_ > 0) ck(cudaMemcpy(D.data(), Dic_.p, N_ * sizeof(double), cudaMemcpyDeviceToHost), "D");
+    for (int u = 0; u < N_; ++u)
+      if (D[iperm_[u]] == 0.0)
+        ic_.warnings.push_back("point " + std::to_string(u) + ": zero depth Hessian entry (unobservable depth)");
+  }
+  ic_.builds = 1;
+  ic_factorize_loop(ic_.lambda);
+  ic_.built = true;
+}
+
+// =====================================================================================
+// gradient / compute_step / solve_step mirrors (evaluated at the solver's p0)
+// =====================================================================================
+static void need_built(const SolverState& s) {
+  if (!s.built) throw PbaError(PBA_E_STATE, "IC solver not built (call pba_gpu_ic_build first)");
+}
+
+void Engine::ic_gradient(double* g) {
+  need_built(ic_);
+  ic_eval(pose0_.p, d0_.p, mask_[ic_.mcur].p, scratch_bits_.p, 0, ic_.lambda, nullptr, nullptr);
+  (void)read_status();
+  if (F_ > 0) ck(cudaMemcpy(g, gf_[0].p, 6 * F_ * sizeof(double), cudaMemcpyDeviceToHost), "g_f");
+  download_depths_user(gn_[0], g + 6 * F_);
+}
+
+void Engine::ic_factorize(double lambda) {
+  need_built(ic_);
+  ic_factorize_loop(lambda);
+}
+
+}  // namespace pba_b200

@@ -1,0 +1,211 @@
+// Host engine behind the C ABI: owns the device state of one PBA problem and
+// runs the reference's LM control flow (solver.cpp:481-654, 663-843) with all
+// per-pixel / per-point / per-frame work on the GPU.  One 64-byte status copy
+// crosses to the host per candidate evaluation.
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pba_gpu.h"
+#include "kernels.hpp"
+
+namespace pba_b200 {
+
+struct PbaError : std::runtime_error {
+  int code;
+  PbaError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline double ms_since(std::chrono::steady_clock::time_point t0) {  // solver.cpp:16-18
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw PbaError(PBA_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void alloc(size_t count);
+  void release();
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+struct SolverState {
+  pba_config cfg{};
+  bool built = false;
+  double lambda = 1e-6;
+  int builds = 0;
+  int factorizations = 0;
+  int mcur = 0;  // index of the sticky residual mask in mask_[] (solver.hpp:162)
+  std::vector<std::string> warnings;
+};
+
+class Engine {
+ public:
+  explicit Engine(const pba_problem* p);
+  ~Engine();
+
+  // ---- C ABI operations (see include/pba_gpu.h) ----
+  void set_params(const double* R, const double* t, const double* d);
+  void get_params(double* R, double* t, double* d) const;
+  void energy(double gamma, const uint8_t* mask, pba_energy_result* out, double* residuals, uint8_t* active);
+  void ic_build(const pba_config* cfg);
+  void ic_gradient(double* g);
+  void ic_compute_step(double* dx);
+  void ic_solve_step(const double* g, double* dx);
+  void ic_factorize(double lambda);
+  void ic_hessian(double* pp, double* dd, double* pd, double* lambda);
+  void fc_build(double gamma, double* pp, double* dd, double* pd, double* g);
+  void apply_update(int mode, const double* dx, double* R, double* t, double* d, int* invalid);
+  double max_reproj_update(const double* R, const double* t, const double* d);
+  void normalize_gauge();
+  void begin(bool ic, const pba_config* cfg);
+  bool iterate(pba_iter_stats* stats);  // returns true when the run is done
+  void end(pba_report* rep);
+
+  static void solve_schur_free(int F, int N, const int64_t* obs_ptr, const int32_t* obs_frame,
+                               const double* pp, const double* dd, const double* pd, const double* g,
+                               double lambda, double* dx);
+
+  int64_t num_obs() const { return NO_; }
+  int64_t device_bytes() const;
+  cudaStream_t stream() const { return stream_; }
+  void set_profiling(bool on);
+  void kernel_times(int64_t* counts, double* total_ms);
+  const std::vector<std::string>& warnings() const { return ic_.warnings; }
+
+  std::string last_error;
+
+ private:
+  // problem / layout
+  int N_ = 0, F_ = 0, P_ = 0;
+  int64_t NO_ = 0;
+  PatternD pat_{};
+  FrameD ref_{};
+  std::vector<FrameD> frames_h_;
+  std::vector<int32_t> perm_;    // internal point -> user point
+  std::vector<int32_t> iperm_;   // user point -> internal point
+  std::vector<int64_t> uo_ptr_;  // user CSR
+  std::vector<int32_t> uo_frame_;
+  std::vector<int32_t> uo2q_;    // user obs -> frame-major obs q
+  bool template_ok_ = true;
+  std::vector<double> R_state_, t_state_;  // user order (host copy of the problem poses)
+  ObsView ov_{};
+  cudaStream_t stream_ = nullptr;
+
+  DBuf<float> images_;
+  DBuf<FrameD> frames_;
+  DBuf<double2> anchor_;
+  DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
+  DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
+  DBuf<PoseD> pose_state_, pose_cur_, pose_cand_, pose0_;
+  DBuf<double> d_state_, d_cur_, d_cand_, d0_;
+  DBuf<uint32_t> mask_[2];        // IC sticky mask / candidate active bits
+  DBuf<uint32_t> scratch_bits_;
+  DBuf<double> J_;                // 7 planes, IC frozen rows
+  DBuf<double> Bic_, Dic_, Hic_;  // IC frozen BlockHessian (solver.hpp:163)
+  DBuf<double> B_[2];             // frame-major pose-depth blocks (cur / cand)
+  DBuf<double> D_[2];
+  DBuf<double> H_[2];             // 21F
+  DBuf<double> gn_[2], gf_[2], rhs_[2];
+  DBuf<double2> rec_;
+  DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
+  DBuf<double> r_out_;
+  DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
+  DBuf<double> S_;
+  DBuf<Status> status_;
+  DBuf<int> flags_;
+  Status* status_h_ = nullptr;    // pinned
+  int* flags_h_ = nullptr;        // pinned
+
+  SolverState ic_;
+
+  // run (stepping) state
+  struct Run {
+    bool active = false;
+    bool ic = true;
+    pba_config cfg{};
+    std::chrono::steady_clock::time_point t_start;
+    double wall_ms = 0.0;
+    int iter = 0;
+    int bad = 0;
+    double energy = 0.0;
+    int64_t initial_active = 0;
+    int64_t num_active = 0;
+    double lambda = 0.0;        // FC damping
+    int fc_builds = 0, fc_factorizations = 0;
+    int cur = 0;                // index of the current (accepted) double buffer
+    double rhs_lambda = 0.0;    // damping baked into rhs_[cur]
+    double gnorm2_n = 0.0;      // |g_n|^2 of the current gradient
+    bool done = false;
+    bool converged = false, diverged = false;
+    int rejected = 0;
+    int iterations = 0;
+    std::string message;
+    std::vector<pba_iter_stats> iters;
+    std::vector<double> snapR, snapT, snapD;
+  } run_;
+
+  // profiling
+  bool prof_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  struct Pending { int kid; cudaEvent_t a, b; };
+  std::vector<Pending> pending_;
+  int64_t kcount_[PBA_K_COUNT] = {};
+  double kms_[PBA_K_COUNT] = {};
+  cudaEvent_t ev_begin(int kid);
+  void ev_end(int kid, cudaEvent_t a);
+  void drain_profile();
+
+  // helpers
+  void check_template() const;
+  void upload_poses(DBuf<PoseD>& dst, const double* R, const double* t);
+  void upload_depths_user(DBuf<double>& dst, const double* d_user);
+  void download_poses(const DBuf<PoseD>& src, double* R, double* t);
+  void download_depths_user(const DBuf<double>& src, double* d_user);
+  Status read_status();
+  int read_flag(int i);
+  void clear_flags();
+  ObsArgs obs_args(double gamma) const;
+  void finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
+                double* rhs, const double* g_f_in, double* H, bool status);
+  // IC pieces
+  void ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
+               double lambda, const PoseD* pose_old, const double* d_old);
+  void ic_rescale_rhs(int buf, double lambda);
+  bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
+  void ic_factorize_loop(double lambda);
+  void ic_refresh();
+  void ic_solve_loop_and_download(double* dx);
+  // FC pieces
+  void alloc_fc();
+  void fc_eval(double gamma, const PoseD* pose, const double* d, int buf, double lambda_next, const PoseD* pose_old,
+               const double* d_old);
+  void fc_rescale_rhs(int buf, double lambda);
+  // shared
+  void download_block_hessian(const DBuf<double>& H, const DBuf<double>& D, const DBuf<double>& B, double* pp,
+                              double* dd, double* pd);
+  void solve_block_hessian(const double* pp, const double* dd, const double* pd, const double* g, double lambda,
+                           double* dx);
+  void solve_xp(const double* rhs);  // trisolve with the factor in S_
+  void backsub(bool ic, const double* B, const double* D, const double* g_n, double lambda, const double* d_cur,
+               double* d_cand, double* dx_out);
+  void record_iter(int iter, double energy, double max_upd, int64_t nact, bool accepted, pba_iter_stats* out);
+  bool grad_is_zero(int buf);
+  void commit_candidate(double sum_d);
+  bool iterate_ic(pba_iter_stats* st);
+  bool iterate_fc(pba_iter_stats* st);
+};
+
+}  // namespace pba_b200

@@ -1,0 +1,886 @@
+// B200 (sm_100a) kernels for the per-iteration photometric bundle adjustment step.
+//
+// Work decomposition:
+//   k_obs      frame-major fused pass over observation pixels: warp, bilinear,
+//              Huber residual, Jacobian (frozen IC rows / FC rows / IC build),
+//              per-frame J^T W r and J^T W J as per-lane register sums reduced
+//              once per tile, per-observation records reduced over the G lanes
+//              of the pattern.                         solver.cpp:63-103,306-358,450-468,688-724
+//   k_backsub  point-major depth back-substitution + candidate depth.  solver.cpp:418-428,553-560,747-750
+//   k_point    point-major gather of per-observation records -> g_n, D_n, s_n.
+//   k_cf       frame-major  c_f = sum_n B_nf g_n/(D_n+lambda).           solver.cpp:407-416
+//   k_finalize deterministic fixed-order reduction of tile partials -> status.
+//   k_schur    reduced camera system.                                   solver.cpp:170-189,375-392
+//   k_chol_*   blocked right-looking fp64 Cholesky (stands in for Eigen::LDLT, solver.cpp:190,393).
+//   k_trisolve forward/backward substitution with the cached factor.    solver.cpp:417
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "kernels.hpp"
+
+namespace pba_b200 {
+
+namespace {
+
+constexpr int NT = 256;  // threads per block for the observation / tile kernels
+
+__device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------------------------
+// k_obs: one block per frame-major tile; G lanes per observation (G = next pow2 >= P)
+// ---------------------------------------------------------------------------------
+template <int MODE, int G>
+__global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
+  constexpr int OPS = NT / G;  // observations per block step
+  constexpr bool kHasH = (MODE == OBS_FC || MODE == OBS_BUILD || MODE == OBS_REFRESH);
+  constexpr bool kHasG = (MODE == OBS_IC || MODE == OBS_FC);
+  constexpr bool kHasRec = (MODE != OBS_ENERGY);
+  const int t = blockIdx.x;
+  const int f = a.ov.tile_frame[t];
+  const int64_t q0 = a.ov.tile_q0[t];
+  const int64_t q1 = a.ov.tile_q1[t];
+  const FrameD fr = a.frames[f];
+  const FrameD rf = a.ref;
+  const PoseD pe = a.pose_eval[f];
+  const bool want_upd = a.pose_old != nullptr;
+  PoseD po;
+  if (want_upd) po = a.pose_old[f];
+  PoseD p0;
+  if (MODE == OBS_BUILD) p0 = a.pose0[f];
+  const int P = a.pat.P;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int k = threadIdx.x % G;
+  const int j = threadIdx.x / G;
+  const bool klive = k < P;
+  const int64_t NPX = a.ov.NO * static_cast<int64_t>(P);
+  const double gam = a.gamma;
+
+  double gacc[6] = {0, 0, 0, 0, 0, 0};
+  double hacc[kHasH ? 21 : 1];
+#pragma unroll
+  for (int i = 0; i < (kHasH ? 21 : 1); ++i) hacc[i] = 0.0;
+  double energy = 0.0, nact = 0.0, noob = 0.0, maxupd = 0.0;
+
+  for (int64_t base = q0; base < q1; base += OPS) {
+    const int64_t q = base + j;
+    const bool live = q < q1;
+    bool act = false;     // residual active at the evaluation parameters
+    bool keep = false;    // final mask bit (BUILD)
+    double gnc = 0.0, dc = 0.0;
+    double b6[6] = {0, 0, 0, 0, 0, 0};
+    if (live) {
+      const int n = a.ov.fm_point[q];
+      const double2 an = __ldg(&a.anchor[n]);
+      const double dv = __ldg(&a.d_eval[n]);
+      // anchor reprojection update (solver.cpp:105-131): anchor = pattern offset 0
+      if (want_upd && k == 0) {
+        const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
+        const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
+        double xo, yo, xn2, yn2, t0_, t1_, t2_;
+        const bool oka = warp_point(po, xa, ya, __ldg(&a.d_old[n]), xo, yo, t0_, t1_, t2_);
+        const bool okb = warp_point(pe, xa, ya, dv, xn2, yn2, t0_, t1_, t2_);
+        if (!oka || !okb) {
+          maxupd = INFINITY;
+        } else {
+          const double du = (fr.fx * xo + fr.cx) - (fr.fx * xn2 + fr.cx);
+          const double dvv = (fr.fy * yo + fr.cy) - (fr.fy * yn2 + fr.cy);
+          maxupd = fmax(maxupd, sqrt(du * du + dvv * dvv));
+        }
+      }
+      const uint32_t mbits = (MODE == OBS_BUILD || a.mask_in == nullptr) ? 0xffffffffu : a.mask_in[q];
+      if (klive && ((mbits >> k) & 1u)) {
+        // template pixel (solver.cpp:42-49)
+        const double pu = an.x + static_cast<double>(a.pat.dx[k]);
+        const double pv = an.y + static_cast<double>(a.pat.dy[k]);
+        const double x = (pu - rf.cx) / rf.fx;
+        const double y = (pv - rf.cy) / rf.fy;
+        const double tval = bilinear(rf.img, rf.W, pu, pv);
+        double xn, yn, vx, vy, vz;
+        double r = 0.0;
+        if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
+          noob += 1.0;
+        } else {
+          const double u = fr.fx * xn + fr.cx;
+          const double v = fr.fy * yn + fr.cy;
+          if (!in_margin(u, v, fr.W, fr.H)) {
+            noob += 1.0;
+          } else {
+            r = tval - bilinear(fr.img, fr.W, u, v);
+            act = true;
+            energy += huber_loss(r, gam);
+            nact += 1.0;
+            if (a.r_out) a.r_out[q * P + k] = r;
+            if constexpr (MODE == OBS_FC) {
+              // image_gradient on the target at the warped point (image.cpp:36-49)
+              const double du = bilinear(fr.img, fr.W, u + 0.5, v) - bilinear(fr.img, fr.W, u - 0.5, v);
+              const double dvv = bilinear(fr.img, fr.W, u, v + 0.5) - bilinear(fr.img, fr.W, u, v - 0.5);
+              const double gx = du * fr.fx, gy = dvv * fr.fy;
+              // fc_warp_jacobian (geometry.cpp:129-139); row = -(grad^T J_img)
+              const double Rx0 = pe.R[0] * x + pe.R[1] * y + pe.R[2];
+              const double Rx1 = pe.R[3] * x + pe.R[4] * y + pe.R[5];
+              const double Rx2 = pe.R[6] * x + pe.R[7] * y + pe.R[8];
+              const double iz = 1.0 / vz;
+              const double P02 = -vx * iz * iz, P12 = -vy * iz * iz;
+              // pre columns: c0 = (0,-Rx2,Rx1), c1 = (Rx2,0,-Rx0), c2 = (-Rx1,Rx0,0),
+              // c3..5 = d e_i, c6 = t
+              double row[7];
+              row[0] = -(gx * (P02 * Rx1) + gy * (iz * -Rx2 + P12 * Rx1));
+              row[1] = -(gx * (iz * Rx2 + P02 * -Rx0) + gy * (P12 * -Rx0));
+              row[2] = -(gx * (iz * -Rx1) + gy * (iz * Rx0));
+              row[3] = -(gx * (iz * dv));
+              row[4] = -(gy * (iz * dv));
+              row[5] = -(gx * (P02 * dv) + gy * (P12 * dv));
+              row[6] = -(gx * (iz * pe.t[0] + P02 * pe.t[2]) + gy * (iz * pe.t[1] + P12 * pe.t[2]));
+              const double w = huber_weight(r, gam);
+              const double wr = w * r;
+              int h = 0;
+#pragma unroll
+              for (int i2 = 0; i2 < 6; ++i2) {
+                const double wi = w * row[i2];
+#pragma unroll
+                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+                b6[i2] = wi * row[6];
+                gacc[i2] += row[i2] * wr;
+              }
+              dc = w * row[6] * row[6];
+              gnc = row[6] * wr;
+            } else if constexpr (MODE == OBS_IC || MODE == OBS_REFRESH) {
+              const int64_t px = q * P + k;
+              double J[7];
+#pragma unroll
+              for (int c = 0; c < 7; ++c) J[c] = ldcs(a.J + c * NPX + px);
+              if constexpr (MODE == OBS_IC) {
+                const double wr = huber_weight(r, gam) * r;  // fresh weights (solver.cpp:461)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
+                gnc = J[6] * wr;
+              } else {
+                const double w = huber_weight(r, gam);
+                int h = 0;
+#pragma unroll
+                for (int i2 = 0; i2 < 6; ++i2) {
+                  const double wi = w * J[i2];
+#pragma unroll
+                  for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * J[j2];
+                  b6[i2] = wi * J[6];
+                }
+                dc = w * J[6] * J[6];
+              }
+            }
+          }
+        }
+        if constexpr (MODE == OBS_BUILD) {
+          // IcSolver::build per-pixel rows (solver.cpp:306-356)
+          const int64_t px = q * P + k;
+          double row[7] = {0, 0, 0, 0, 0, 0, 0};
+          const double d0 = __ldg(&a.d0[n]);
+          // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
+          const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
+          const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
+          const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + d0 * p0.t[2];
+          const bool obs_ok = (d0 > 0.0) && !(vza < kDegenerateDepthEps);
+          if (act && obs_ok) {
+            // template gradient image_gradient(ref, x) (image.cpp:36-49)
+            const double gu = rf.fx * x + rf.cx, gv = rf.fy * y + rf.cy;
+            const bool grad_ok = in_bounds_px(gu - 0.5, gv, rf.W, rf.H) && in_bounds_px(gu + 0.5, gv, rf.W, rf.H) &&
+                                 in_bounds_px(gu, gv - 0.5, rf.W, rf.H) && in_bounds_px(gu, gv + 0.5, rf.W, rf.H);
+            const double R0x0 = p0.R[0] * x + p0.R[1] * y + p0.R[2];
+            const double R0x1 = p0.R[3] * x + p0.R[4] * y + p0.R[5];
+            const double R0x2 = p0.R[6] * x + p0.R[7] * y + p0.R[8];
+            const double vz0 = R0x2 + d0 * p0.t[2];
+            if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
+              keep = true;
+              const double gxi = (bilinear(rf.img, rf.W, gu + 0.5, gv) - bilinear(rf.img, rf.W, gu - 0.5, gv)) * rf.fx;
+              const double gyi = (bilinear(rf.img, rf.W, gu, gv + 0.5) - bilinear(rf.img, rf.W, gu, gv - 0.5)) * rf.fy;
+              const double zbar0 = vz0 / d0;
+              const double g30 = gxi / zbar0, g31 = gyi / zbar0, g32 = -(gxi * x + gyi * y) / zbar0;
+              const double a0 = p0.R[0] * g30 + p0.R[1] * g31 + p0.R[2] * g32;
+              const double a1 = p0.R[3] * g30 + p0.R[4] * g31 + p0.R[5] * g32;
+              const double a2 = p0.R[6] * g30 + p0.R[7] * g31 + p0.R[8] * g32;
+              const double adt = a0 * p0.t[0] + a1 * p0.t[1] + a2 * p0.t[2];
+              const double m0 = zbar0 * a0, m1 = zbar0 * a1, m2 = zbar0 * a2 - adt;
+              row[0] = R0x1 * m2 - R0x2 * m1;
+              row[1] = R0x2 * m0 - R0x0 * m2;
+              row[2] = R0x0 * m1 - R0x1 * m0;
+              row[3] = d0 * m0;
+              row[4] = d0 * m1;
+              row[5] = d0 * m2;
+              row[6] = m0 * p0.t[0] + m1 * p0.t[1] + m2 * p0.t[2];
+              const double w = huber_weight(r, gam);  // W0 (solver.cpp:279)
+              int h = 0;
+#pragma unroll
+              for (int i2 = 0; i2 < 6; ++i2) {
+                const double wi = w * row[i2];
+#pragma unroll
+                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+                b6[i2] = wi * row[6];
+              }
+              dc = w * row[6] * row[6];
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 7; ++c) a.Jw[c * NPX + px] = row[c];
+        }
+      }
+    }
+    // per-observation records: reduce over the G lanes of the pattern
+    if constexpr (kHasRec) {
+      gnc = group_sum<G>(gnc);
+      dc = group_sum<G>(dc);
+      if constexpr (kHasH) {
+#pragma unroll
+        for (int i2 = 0; i2 < 6; ++i2) b6[i2] = group_sum<G>(b6[i2]);
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, MODE == OBS_BUILD ? keep : act);
+    if (live && k == 0) {
+      const unsigned bits = (G == 32) ? bal : ((bal >> ((lane / G) * G)) & ((1u << G) - 1u));
+      a.active_out[q] = bits;
+      if (kHasRec) a.rec[q] = make_double2(gnc, dc);
+      if (kHasH) {
+#pragma unroll
+        for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+      }
+    }
+  }
+
+  // ---- deterministic block reduction of the per-lane frame accumulators ----
+  __shared__ double red[NT / 32][PT_STRIDE];
+  auto put = [&](int slot, double v) {
+    v = warp_sum(v);
+    if (lane == 0) red[warp][slot] = v;
+  };
+  if constexpr (kHasG) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) put(PT_G + i, gacc[i]);
+  }
+  if constexpr (kHasH) {
+#pragma unroll
+    for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
+  }
+  put(PT_E, energy);
+  put(PT_NACT, nact);
+  put(PT_NOOB, noob);
+  {
+    const double m = warp_max(maxupd);
+    if (lane == 0) red[warp][PT_MAXUPD] = m;
+  }
+  __syncthreads();
+  if (warp == 0 && lane < PT_STRIDE) {
+    const bool used = (lane >= PT_E && lane <= PT_MAXUPD) || (kHasG && lane < 6) ||
+                      (kHasH && lane >= PT_H && lane < PT_H + 21);
+    double v = 0.0;
+    if (used) {
+      if (lane == PT_MAXUPD) {
+        for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w][lane]);
+      } else {
+        for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
+      }
+    }
+    a.partial[static_cast<int64_t>(t) * PT_STRIDE + lane] = v;
+  }
+}
+
+template <int MODE>
+void launch_obs_mode(const ObsArgs& a, int G, cudaStream_t s) {
+  const dim3 grid(a.ov.ntiles), block(NT);
+  switch (G) {
+    case 1: k_obs<MODE, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: k_obs<MODE, 2><<<grid, block, 0, s>>>(a); break;
+    case 4: k_obs<MODE, 4><<<grid, block, 0, s>>>(a); break;
+    case 8: k_obs<MODE, 8><<<grid, block, 0, s>>>(a); break;
+    case 16: k_obs<MODE, 16><<<grid, block, 0, s>>>(a); break;
+    default: k_obs<MODE, 32><<<grid, block, 0, s>>>(a); break;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_pose_update
+// ---------------------------------------------------------------------------------
+__global__ void k_pose_update(int ic, int F, const PoseD* __restrict__ cur, const PoseD* __restrict__ pose0,
+                              const double* __restrict__ xp, PoseD* __restrict__ cand) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const PoseD pk = cur[f];
+  const double w[3] = {xp[6 * f], xp[6 * f + 1], xp[6 * f + 2]};
+  const double dt[3] = {xp[6 * f + 3], xp[6 * f + 4], xp[6 * f + 5]};
+  double dR[9];
+  so3_exp(w, dR);
+  PoseD out;
+  if (ic) {
+    // apply_ic_update (geometry.cpp:197-209): R = R_k R0^T dR^T R0; t = t_k - R_k R0^T dt
+    const PoseD p0 = pose0[f];
+    double R0T[9], dRT[9], A[9], Bm[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        R0T[3 * r + c] = p0.R[3 * c + r];
+        dRT[3 * r + c] = dR[3 * c + r];
+      }
+    mat3_mul(pk.R, R0T, A);   // R_k R0^T
+    mat3_mul(A, dRT, Bm);     // (R_k R0^T) dR^T
+    mat3_mul(Bm, p0.R, out.R);
+    for (int r = 0; r < 3; ++r) out.t[r] = pk.t[r] - (A[3 * r] * dt[0] + A[3 * r + 1] * dt[1] + A[3 * r + 2] * dt[2]);
+  } else {
+    // pose_boxplus (geometry.cpp:93-98)
+    mat3_mul(dR, pk.R, out.R);
+    for (int r = 0; r < 3; ++r) out.t[r] = pk.t[r] + dt[r];
+  }
+  cand[f] = out;
+}
+
+// ---------------------------------------------------------------------------------
+// k_backsub: warp per point, lanes over the point's observations
+// ---------------------------------------------------------------------------------
+constexpr int kPointsPerWarp = 4;
+
+__global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[NT / 32][3];
+  double sum_d = 0.0, ninv = 0.0, nnf = 0.0;
+  for (int i = 0; i < kPointsPerWarp; ++i) {
+    const int n = (blockIdx.x * (NT / 32) + warp) * kPointsPerWarp + i;
+    if (n >= a.ov.N) break;
+    const int64_t o0 = a.ov.pm_ptr[n], o1 = a.ov.pm_ptr[n + 1];
+    double acc = 0.0;
+    for (int64_t o = o0 + lane; o < o1; o += 32) {
+      const int f = a.ov.pm_frame[o];
+      const int64_t q = a.ov.pm2fm[o];
+      const double* b = a.B + q * 6;
+      const double* x = a.xp + 6 * f;
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) dot += b[c] * x[c];
+      acc += dot;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double D = a.D[n] + a.lambda;
+      const double dx = (-a.g_n[n] - acc) / D;
+      const double dc = a.d_cur[n];
+      double dn;
+      if (a.ic) {
+        const double d0 = a.d0[n];
+        dn = ((d0 - dx) / d0) * dc;
+      } else {
+        dn = dc + dx;
+      }
+      a.d_cand[n] = dn;
+      if (a.dx_out) a.dx_out[n] = dx;
+      sum_d += dn;
+      if (dn <= 0.0) ninv += 1.0;
+      if (!isfinite(dx)) nnf += 1.0;
+    }
+  }
+  if (lane == 0) {
+    red[warp][0] = sum_d;
+    red[warp][1] = ninv;
+    red[warp][2] = nnf;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    a.partial[blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_point: warp per point gather of per-observation records
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_point(const PointArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[NT / 32];
+  double g2 = 0.0;
+  for (int i = 0; i < kPointsPerWarp; ++i) {
+    const int n = (blockIdx.x * (NT / 32) + warp) * kPointsPerWarp + i;
+    if (n >= a.ov.N) break;
+    double gs = 0.0, ds = 0.0;
+    if (a.mode != PT_RESCALE) {
+      const int64_t o0 = a.ov.pm_ptr[n], o1 = a.ov.pm_ptr[n + 1];
+      for (int64_t o = o0 + lane; o < o1; o += 32) {
+        const double2 rc = a.rec[a.ov.pm2fm[o]];
+        gs += rc.x;
+        ds += rc.y;
+      }
+      gs = warp_sum(gs);
+      ds = warp_sum(ds);
+    }
+    if (lane == 0) {
+      double g = gs, D;
+      switch (a.mode) {
+        case PT_GRAD:
+          a.g_n[n] = g;
+          D = a.D[n];
+          break;
+        case PT_FCH:
+          a.g_n[n] = g;
+          a.D[n] = ds;
+          D = ds;
+          break;
+        case PT_DONLY:
+          a.D[n] = ds;
+          D = ds;
+          g = 0.0;
+          break;
+        default:  // PT_RESCALE
+          g = a.g_n[n];
+          D = a.D[n];
+          break;
+      }
+      if (a.s_n && a.mode != PT_DONLY) a.s_n[n] = g / (D + a.lambda);
+      g2 += g * g;
+    }
+  }
+  if (lane == 0) red[warp] = g2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v += red[w];
+    a.partial[blockIdx.x * 2] = v;
+    a.partial[blockIdx.x * 2 + 1] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_cf: c_f partial per tile (solver.cpp:407-416 Schur right-hand-side term)
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_cf(const ObsView ov, const double* __restrict__ B,
+                                           const double* __restrict__ s_n, double* __restrict__ partial) {
+  const int t = blockIdx.x;
+  const int64_t q0 = ov.tile_q0[t], q1 = ov.tile_q1[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double c[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
+    const double s = __ldg(&s_n[ov.fm_point[q]]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) c[i] += B[q * 6 + i] * s;
+  }
+  __shared__ double red[NT / 32][6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double v = warp_sum(c[i]);
+    if (lane == 0) red[warp][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    partial[static_cast<int64_t>(t) * 8 + threadIdx.x] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_finalize: blocks 0..F-1 reduce the tiles of frame f; block F the scalars.
+// Fixed strided order + warp tree: bitwise reproducible for a given tiling.
+// ---------------------------------------------------------------------------------
+__device__ double tile_sum(const double* part, int stride, int slot, int t0, int t1, int lane, bool is_max) {
+  double v = 0.0;
+  for (int t = t0 + lane; t < t1; t += 32) {
+    const double x = part[static_cast<int64_t>(t) * stride + slot];
+    v = is_max ? fmax(v, x) : v + x;
+  }
+  return is_max ? warp_max(v) : warp_sum(v);
+}
+
+__global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int F = a.ov.F;
+  if (blockIdx.x < F) {
+    const int f = blockIdx.x;
+    const int t0 = a.ov.ftile_ptr[f], t1 = a.ov.ftile_ptr[f + 1];
+    __shared__ double vals[6 + 6 + 21];
+    // components: 0..5 g, 6..11 cf, 12..32 H
+    for (int c = warp; c < 33; c += NT / 32) {
+      double v = 0.0;
+      if (c < 6) {
+        v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_G + c, t0, t1, lane, false)
+                      : (a.g_f_in ? a.g_f_in[6 * f + c] : 0.0);
+      } else if (c < 12) {
+        if (a.partial_cf) v = tile_sum(a.partial_cf, 8, c - 6, t0, t1, lane, false);
+      } else if (a.want_h && a.partial) {
+        v = tile_sum(a.partial, PT_STRIDE, PT_H + (c - 12), t0, t1, lane, false);
+      }
+      if (lane == 0) vals[c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      const double g = vals[threadIdx.x];
+      if (a.g_f) a.g_f[6 * f + threadIdx.x] = g;
+      if (a.rhs) a.rhs[6 * f + threadIdx.x] = -g + vals[6 + threadIdx.x];
+    }
+    if (a.want_h && a.H && threadIdx.x < 21) a.H[21 * f + threadIdx.x] = vals[12 + threadIdx.x];
+    return;
+  }
+  // scalar block
+  __shared__ double sc[8];
+  const int nt = a.ov.ntiles;
+  double v = 0.0;
+  switch (warp) {
+    case 0: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_E, 0, nt, lane, false) : 0.0; break;
+    case 1: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NACT, 0, nt, lane, false) : 0.0; break;
+    case 2: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NOOB, 0, nt, lane, false) : 0.0; break;
+    case 3: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_MAXUPD, 0, nt, lane, true) : 0.0; break;
+    case 4: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 0, 0, a.nbs, lane, false) : 0.0; break;
+    case 5: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 1, 0, a.nbs, lane, false) : 0.0; break;
+    case 6: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 2, 0, a.nbs, lane, false) : 0.0; break;
+    default: v = a.partial_pt ? tile_sum(a.partial_pt, 2, 0, 0, a.npt, lane, false) : 0.0; break;
+  }
+  if (lane == 0) sc[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0 && a.status) {
+    Status s;
+    s.energy = sc[0];
+    s.num_active = sc[1];
+    s.num_oob = sc[2];
+    s.max_upd = sc[3];
+    s.sum_d = sc[4];
+    s.invalid = sc[5];
+    s.nonfinite = sc[6];
+    s.gnorm2_n = sc[7];
+    *a.status = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_commit (normalize_depth_gauge, solver.cpp:135-143, applied on accept)
+// ---------------------------------------------------------------------------------
+__global__ void k_commit(int N, int F, const double* __restrict__ d_cand, const PoseD* __restrict__ pose_cand,
+                         double mean, double tscale, double* __restrict__ d_cur, PoseD* __restrict__ pose_cur) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) d_cur[i] = d_cand[i] / mean;
+  if (i < F) {
+    PoseD p = pose_cand[i];
+    for (int r = 0; r < 3; ++r) p.t[r] = p.t[r] * tscale;
+    pose_cur[i] = p;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_max_reproj: standalone max_reprojection_update_px over point-major obs
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_max_reproj(const ObsView ov, const FrameD* __restrict__ frames, const FrameD ref,
+                                                   const double2* __restrict__ anchor, int dx0, int dy0,
+                                                   const PoseD* __restrict__ pa,
+                                                   const double* __restrict__ da, const PoseD* __restrict__ pb,
+                                                   const double* __restrict__ db, double* __restrict__ partial) {
+  double m = 0.0;
+  for (int64_t o = blockIdx.x * static_cast<int64_t>(NT) + threadIdx.x; o < ov.NO;
+       o += static_cast<int64_t>(gridDim.x) * NT) {
+    // point of obs o: binary search in pm_ptr
+    int lo = 0, hi = ov.N - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ov.pm_ptr[mid] <= o) lo = mid; else hi = mid - 1;
+    }
+    const int n = lo;
+    const int f = ov.pm_frame[o];
+    const double2 an = anchor[n];
+    const double x = ((an.x + static_cast<double>(dx0)) - ref.cx) / ref.fx;
+    const double y = ((an.y + static_cast<double>(dy0)) - ref.cy) / ref.fy;
+    double xa, ya, xb, yb, t0, t1, t2;
+    const bool oka = warp_point(pa[f], x, y, da[n], xa, ya, t0, t1, t2);
+    const bool okb = warp_point(pb[f], x, y, db[n], xb, yb, t0, t1, t2);
+    if (!oka || !okb) {
+      m = INFINITY;
+    } else {
+      const FrameD fr = frames[f];
+      const double du = (fr.fx * xa + fr.cx) - (fr.fx * xb + fr.cx);
+      const double dv = (fr.fy * ya + fr.cy) - (fr.fy * yb + fr.cy);
+      m = fmax(m, sqrt(du * du + dv * dv));
+    }
+  }
+  __shared__ double red[NT / 32];
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w]);
+    partial[blockIdx.x] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Schur complement (round-1 form: per-point pair outer products, fp64 RED to S)
+// ---------------------------------------------------------------------------------
+__global__ void k_schur_init(int F, const double* __restrict__ H21, double lambda, double* __restrict__ S) {
+  const int n = 6 * F;
+  const int64_t total = static_cast<int64_t>(n) * n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
+    double v = 0.0;
+    if (r / 6 == c / 6) {
+      const int f = r / 6, i = r % 6, j = c % 6;
+      const int lo = i < j ? i : j, hi = i < j ? j : i;
+      const int idx = lo * 6 - lo * (lo - 1) / 2 + (hi - lo);  // upper-triangle packing
+      v = H21[21 * f + idx] + (i == j ? lambda : 0.0);
+    }
+    S[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double* __restrict__ B,
+                                                  const double* __restrict__ D, double lambda, double* __restrict__ S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = blockIdx.x * (NT / 32) + warp;
+  if (n >= ov.N) return;
+  const int64_t o0 = ov.pm_ptr[n], o1 = ov.pm_ptr[n + 1];
+  const int kn = static_cast<int>(o1 - o0);
+  const double Dn = D[n] + lambda;
+  const int ld = 6 * ov.F;
+  for (int a = 0; a < kn; ++a) {
+    const int fa = ov.pm_frame[o0 + a];
+    const double* Ba = B + static_cast<int64_t>(ov.pm2fm[o0 + a]) * 6;
+    bool za = true;
+    for (int c = 0; c < 6; ++c) za = za && (Ba[c] == 0.0);
+    if (za) continue;  // Bf.isZero(0.0) (solver.cpp:181,384)
+    const int items = (kn - a) * 36;
+    for (int it = lane; it < items; it += 32) {
+      const int b = a + it / 36, ij = it % 36, i = ij / 6, jj = ij % 6;
+      const int fb = ov.pm_frame[o0 + b];
+      const double* Bb = B + static_cast<int64_t>(ov.pm2fm[o0 + b]) * 6;
+      bool zb = true;
+      for (int c = 0; c < 6; ++c) zb = zb && (Bb[c] == 0.0);
+      if (zb) continue;
+      const double v = Ba[i] * Bb[jj] / Dn;
+      atomicAdd(&S[static_cast<int64_t>(6 * fa + i) * ld + 6 * fb + jj], -v);
+      if (b != a) atomicAdd(&S[static_cast<int64_t>(6 * fb + jj) * ld + 6 * fa + i], -v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Blocked right-looking Cholesky, NB = 32, lower factor in place.
+// ---------------------------------------------------------------------------------
+constexpr int NB = 32;
+
+__global__ void __launch_bounds__(1024) k_chol_diag(double* __restrict__ A, int n, int j0, int nb, int* fail) {
+  __shared__ double a[NB][NB + 1];
+  const int r = threadIdx.y, c = threadIdx.x;
+  if (r < nb && c < nb && c <= r) a[r][c] = A[static_cast<int64_t>(j0 + r) * n + j0 + c];
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (r == 0 && c == 0) {
+      const double d = a[j][j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        *fail = 1;
+        a[j][j] = 1.0;
+      } else {
+        a[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (c == j && r > j && r < nb) a[r][j] = a[r][j] / a[j][j];
+    __syncthreads();
+    if (r > j && r < nb && c > j && c <= r) a[r][c] -= a[r][j] * a[c][j];
+    __syncthreads();
+  }
+  if (r < nb && c < nb && c <= r) A[static_cast<int64_t>(j0 + r) * n + j0 + c] = a[r][c];
+}
+
+__global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ A, int n, int j0, int nb) {
+  __shared__ double l11[NB][NB + 1];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    l11[r][c] = (r < nb && c <= r) ? A[static_cast<int64_t>(j0 + r) * n + j0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int i = j0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* row = A + static_cast<int64_t>(i) * n + j0;
+  double l[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    if (c < nb) {
+      double v = row[c];
+      for (int p = 0; p < c; ++p) v -= l[p] * l11[c][p];
+      l[c] = v / l11[c][c];
+      row[c] = l[c];
+    }
+  }
+}
+
+// trailing update of the lower triangle: A[i][c] -= sum_p L[i][p] L[c][p], 32x32 tiles
+__global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ A, int n, int j0, int nb) {
+  const int base = j0 + nb;
+  const int m = (n - base + NB - 1) / NB;
+  // map blockIdx.x -> (ti, tj) with tj <= ti
+  int tid = blockIdx.x, ti = 0;
+  while (tid > ti) {
+    tid -= ti + 1;
+    ++ti;
+  }
+  const int tj = tid;
+  if (ti >= m) return;
+  __shared__ double Li[NB][NB + 1], Lj[NB][NB + 1];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, p = e % NB;
+    const int gi = base + ti * NB + r, gj = base + tj * NB + r;
+    Li[r][p] = (gi < n && p < nb) ? A[static_cast<int64_t>(gi) * n + j0 + p] : 0.0;
+    Lj[r][p] = (gj < n && p < nb) ? A[static_cast<int64_t>(gj) * n + j0 + p] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    const int gi = base + ti * NB + r, gj = base + tj * NB + c;
+    if (gi >= n || gj >= n || gj > gi) continue;
+    double s = 0.0;
+#pragma unroll 8
+    for (int p = 0; p < NB; ++p) s += Li[r][p] * Lj[c][p];
+    A[static_cast<int64_t>(gi) * n + gj] -= s;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Triangular solves, one block of 1024 threads.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_trisolve(const double* __restrict__ L, int n, const double* __restrict__ b,
+                                                   double* __restrict__ x, int* nonfinite) {
+  extern __shared__ double y[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < n; i += blockDim.x) y[i] = b[i];
+  __syncthreads();
+  // forward: L y = b
+  for (int jb = 0; jb < n; jb += NB) {
+    const int nb = min(NB, n - jb);
+    if (warp == 0) {
+      double yr = lane < nb ? y[jb + lane] : 0.0;
+      for (int p = 0; p < nb; ++p) {
+        if (lane == p) yr = yr / L[static_cast<int64_t>(jb + p) * n + jb + p];
+        const double yp = __shfl_sync(0xffffffffu, yr, p);
+        if (lane > p && lane < nb) yr -= L[static_cast<int64_t>(jb + lane) * n + jb + p] * yp;
+      }
+      if (lane < nb) y[jb + lane] = yr;
+    }
+    __syncthreads();
+    for (int i = jb + nb + tid; i < n; i += blockDim.x) {
+      const double* row = L + static_cast<int64_t>(i) * n + jb;
+      double s = 0.0;
+      for (int p = 0; p < nb; ++p) s += row[p] * y[jb + p];
+      y[i] -= s;
+    }
+    __syncthreads();
+  }
+  // backward: L^T x = y
+  const int last = ((n - 1) / NB) * NB;
+  for (int jb = last; jb >= 0; jb -= NB) {
+    const int nb = min(NB, n - jb);
+    if (warp == 0) {
+      double xr = lane < nb ? y[jb + lane] : 0.0;
+      for (int p = nb - 1; p >= 0; --p) {
+        if (lane == p) xr = xr / L[static_cast<int64_t>(jb + p) * n + jb + p];
+        const double xp = __shfl_sync(0xffffffffu, xr, p);
+        if (lane < p) xr -= L[static_cast<int64_t>(jb + p) * n + jb + lane] * xp;
+      }
+      if (lane < nb) y[jb + lane] = xr;
+    }
+    __syncthreads();
+    for (int i = tid; i < jb; i += blockDim.x) {
+      double s = 0.0;
+      for (int p = 0; p < nb; ++p) s += L[static_cast<int64_t>(jb + p) * n + i] * y[jb + p];
+      y[i] -= s;
+    }
+    __syncthreads();
+  }
+  int bad = 0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    x[i] = y[i];
+    if (!isfinite(y[i])) bad = 1;
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+
+int next_pow2(int p) {
+  int g = 1;
+  while (g < p) g <<= 1;
+  return g;
+}
+
+}  // namespace
+
+// ================================ launchers =========================================
+
+void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
+  if (a.ov.ntiles == 0) return;
+  const int G = next_pow2(a.pat.P);
+  switch (mode) {
+    case OBS_ENERGY: launch_obs_mode<OBS_ENERGY>(a, G, s); break;
+    case OBS_IC: launch_obs_mode<OBS_IC>(a, G, s); break;
+    case OBS_FC: launch_obs_mode<OBS_FC>(a, G, s); break;
+    case OBS_BUILD: launch_obs_mode<OBS_BUILD>(a, G, s); break;
+    default: launch_obs_mode<OBS_REFRESH>(a, G, s); break;
+  }
+}
+
+void launch_pose_update(int ic, int F, const PoseD* cur, const PoseD* pose0, const double* xp, PoseD* cand,
+                        cudaStream_t s) {
+  k_pose_update<<<(F + 127) / 128, 128, 0, s>>>(ic, F, cur, pose0, xp, cand);
+}
+
+int backsub_blocks(int N) {
+  const int per_block = (NT / 32) * kPointsPerWarp;
+  return (N + per_block - 1) / per_block;
+}
+int point_blocks(int N) { return backsub_blocks(N); }
+
+void launch_backsub(const BacksubArgs& a, cudaStream_t s) {
+  const int nb = backsub_blocks(a.ov.N);
+  if (nb > 0) k_backsub<<<nb, NT, 0, s>>>(a);
+}
+
+void launch_point(const PointArgs& a, cudaStream_t s) {
+  const int nb = point_blocks(a.ov.N);
+  if (nb > 0) k_point<<<nb, NT, 0, s>>>(a);
+}
+
+void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s) {
+  if (ov.ntiles > 0) k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf);
+}
+
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s) { k_finalize<<<a.ov.F + 1, NT, 0, s>>>(a); }
+
+void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, double scale_d, double scale_t,
+                   double* d_cur, PoseD* pose_cur, cudaStream_t s) {
+  const int m = N > F ? N : F;
+  k_commit<<<(m + 255) / 256, 256, 0, s>>>(N, F, d_cand, pose_cand, scale_d, scale_t, d_cur, pose_cur);
+}
+
+void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref, const double2* anchor, int dx0,
+                       int dy0, const PoseD* pa, const double* da, const PoseD* pb, const double* db, double* partial,
+                       int nblocks, cudaStream_t s) {
+  k_max_reproj<<<nblocks, NT, 0, s>>>(ov, frames, ref, anchor, dx0, dy0, pa, da, pb, db, partial);
+}
+
+void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
+                  cudaStream_t s) {
+  const int n = 6 * ov.F;
+  const int64_t total = static_cast<int64_t>(n) * n;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  k_schur_init<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, S);
+  const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
+  if (pb > 0) k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, S);
+}
+
+void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    const int nb = std::min(NB, n - j0);
+    k_chol_diag<<<1, dim3(NB, NB), 0, s>>>(S, n, j0, nb, fail);
+    const int rest = n - j0 - nb;
+    if (rest > 0) {
+      k_chol_panel<<<(rest + 255) / 256, 256, 0, s>>>(S, n, j0, nb);
+      const int m = (rest + NB - 1) / NB;
+      k_chol_update<<<m * (m + 1) / 2, 256, 0, s>>>(S, n, j0, nb);
+    }
+  }
+}
+
+void launch_trisolve(const double* L, int n, const double* b, double* x, int* nonfinite, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(n) * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_trisolve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_trisolve<<<1, 1024, smem, s>>>(L, n, b, x, nonfinite);
+}
+
+}  // namespace pba_b200

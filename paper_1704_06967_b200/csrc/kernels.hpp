@@ -1,0 +1,148 @@
+// Host-side launchers for the B200 PBA kernels (implemented in kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace pba_b200 {
+
+// Observation-pass modes (see kernels.cu k_obs).
+enum ObsMode : int {
+  OBS_ENERGY = 0,   // residual / Huber only              (energy_eval, solver.cpp:229-244)
+  OBS_IC = 1,       // + J^T W r with frozen J rows        (solver.cpp:436-468)
+  OBS_FC = 2,       // + FC Jacobian, J^T W J, J^T W r     (solver.cpp:688-724)
+  OBS_BUILD = 3,    // IC build at p0: J rows, W0, H       (solver.cpp:273-358)
+  OBS_REFRESH = 4   // IC Hessian refresh with fresh W     (solver.cpp:505-531)
+};
+
+// Per-tile partial layout of the observation pass (doubles).
+constexpr int PT_G = 0;       // 6: sum J_pose^T w r
+constexpr int PT_H = 6;       // 21: upper triangle of sum w J_pose J_pose^T
+constexpr int PT_E = 27;      // energy
+constexpr int PT_NACT = 28;   // active residual count
+constexpr int PT_NOOB = 29;   // out-of-bounds count
+constexpr int PT_MAXUPD = 30; // max anchor reprojection update
+constexpr int PT_STRIDE = 32;
+
+struct ObsArgs {
+  ObsView ov;
+  FrameD ref;
+  const FrameD* frames;        // F
+  PatternD pat;
+  const double2* anchor;       // N (internal order)
+  double gamma;
+  const PoseD* pose_eval;      // F
+  const double* d_eval;        // N
+  const PoseD* pose_old;       // F or null (max reprojection update)
+  const double* d_old;         // N or null
+  const PoseD* pose0;          // F (IC build)
+  const double* d0;            // N (IC build)
+  const uint32_t* mask_in;     // NO bit words or null (= all pixels)
+  uint32_t* active_out;        // NO bit words
+  double* r_out;               // NO*P or null
+  const double* J;             // 7 planes of NO*P (IC / REFRESH read, BUILD write)
+  double* Jw;                  // BUILD output planes
+  double* B_out;               // NO*6 (FC/BUILD/REFRESH)
+  double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
+  double* partial;             // ntiles * PT_STRIDE
+};
+
+void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
+
+// Candidate poses (IC: apply_ic_update geometry.cpp:197-209 with pc.d0 = 1;
+// FC: pose_boxplus geometry.cpp:93-98) from the pose step xp (6F).
+void launch_pose_update(int ic, int F, const PoseD* cur, const PoseD* pose0, const double* xp,
+                        PoseD* cand, cudaStream_t s);
+
+// Depth back-substitution + candidate depth (solver.cpp:418-428 / 198-208 and
+// :553-560 / :747-750).  partial: per block {sum d_cand, #invalid, #nonfinite}.
+struct BacksubArgs {
+  ObsView ov;
+  int ic;
+  const double* xp;       // 6F
+  const double* B;        // NO*6 frame-major
+  const double* D;        // N (without lambda)
+  const double* g_n;      // N
+  double lambda;
+  const double* d_cur;    // N
+  const double* d0;       // N (IC)
+  double* d_cand;         // N
+  double* dx_out;         // N or null
+  double* partial;        // nblocks * 4
+};
+int backsub_blocks(int N);
+void launch_backsub(const BacksubArgs& a, cudaStream_t s);
+
+// Point-major gather of the per-observation records.
+enum PointMode : int { PT_GRAD = 0, PT_FCH = 1, PT_DONLY = 2, PT_RESCALE = 3 };
+struct PointArgs {
+  ObsView ov;
+  int mode;
+  const double2* rec;     // NO
+  double* g_n;            // N (out for GRAD/FCH; in for RESCALE)
+  double* D;              // N (out for FCH/DONLY; in otherwise)
+  double lambda;          // damping used for s_n
+  double* s_n;            // N out: g_n / (D_n + lambda)
+  double* partial;        // nblocks * 2 {sum g_n^2, 0}
+};
+int point_blocks(int N);
+void launch_point(const PointArgs& a, cudaStream_t s);
+
+// Frame-major  c_f = sum_n B_nf s_n  per tile.
+void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf,
+               cudaStream_t s);
+
+// Reduction of tile partials.  Writes g_f (6F), rhs = -g_f + c_f (6F) when
+// partial_cf != null, H (21F upper) when want_h, and the scalar Status.
+struct Status {
+  double energy;
+  double num_active;
+  double num_oob;
+  double max_upd;
+  double sum_d;
+  double invalid;
+  double nonfinite;
+  double gnorm2_n;
+};
+struct FinalizeArgs {
+  ObsView ov;
+  const double* partial;      // ntiles * PT_STRIDE (obs pass) or null
+  const double* partial_cf;   // ntiles * 8 or null
+  const double* partial_bs;   // backsub blocks * 4 or null
+  int nbs;
+  const double* partial_pt;   // point blocks * 2 or null
+  int npt;
+  int want_h;
+  double* g_f;                // 6F or null
+  double* rhs;                // 6F or null (requires partial_cf; uses g_f_in if partial==null)
+  const double* g_f_in;       // 6F: gradient when the obs partial is absent (rescale)
+  double* H;                  // 21F or null
+  Status* status;             // or null
+};
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
+
+// Accept: d_cur = d_cand / mean, t_cur = t_cand * mean (solver.cpp:135-143).
+void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, double scale_d,
+                   double scale_t, double* d_cur, PoseD* pose_cur, cudaStream_t s);
+
+// Max reprojection update between two parameter sets (solver.cpp:105-131).
+void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref,
+                       const double2* anchor, int dx0, int dy0, const PoseD* pa, const double* da,
+                       const PoseD* pb, const double* db, double* partial, int nblocks, cudaStream_t s);
+
+// Reduced camera system S = blockdiag(H_ff + lambda I) - sum_n b_n b_n^T / (D_n + lambda)
+// (solver.cpp:170-189, 375-392).  S is 6F x 6F row-major, full.
+void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D,
+                  double lambda, double* S, cudaStream_t s);
+
+// In-place dense Cholesky (lower) of the n x n row-major S; *fail set on a
+// non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).
+void launch_cholesky(double* S, int n, int* fail, cudaStream_t s);
+
+// x = L^-T L^-1 b.  *nonfinite set when x has a non-finite entry.
+void launch_trisolve(const double* L, int n, const double* b, double* x, int* nonfinite,
+                     cudaStream_t s);
+
+}  // namespace pba_b200

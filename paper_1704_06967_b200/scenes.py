@@ -1,0 +1,303 @@
+"""Seeded synthetic scenes for the BASELINE.json configurations (input producer).
+
+The reference's own generator (synth.cpp: value-noise planes/heightfields) cannot
+express the BASELINE scenes, so this module renders them:
+
+* a unit sphere textured with Gaussian noise N(0,1) blurred with sigma = 2 px and
+  affinely rescaled to [0, 255] (lat-long map at ~1 texel per image pixel on the
+  sphere's near side), inside an environment sphere carrying the same texture;
+* a reference camera at distance ``orbit_radius`` from the sphere centre and target
+  cameras on an arc about the centre (the reference's orbit, synth.cpp:193-203);
+* anchors sampled on the sphere's projection; true inverse depth from the ray hit;
+  depth gauge normalised to mean 1 (synth.cpp:285-291); initial inverse depths
+  d_true * (1 + N(0, 0.05)); poses perturbed by a rotation of N(0, rot_deg) about a
+  uniform axis and N(0, trans_sigma) translation;
+* an observation list from an angular visibility rule (C3/C4/C5).
+
+All randomness comes from one torch.Generator per scene seed; the same arrays are
+handed to the GPU path and to the CPU oracle, so parity never depends on how the
+scene was produced.  Images are float32 in [0, 255] (Huber delta = 9 in these
+units; lambda0 scaled by 255^2).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .solver import ProblemState, SolverConfig
+
+# DSO's 8-pixel residual pattern with the anchor (0,0) moved to index 0
+# (solver.cpp:116 and :311 treat offsets[0] as the anchor).
+DSO8 = np.array([(0, 0), (0, -2), (-1, -1), (1, -1), (-2, 0), (2, 0), (-1, 1), (0, 2)], dtype=np.int32)
+
+
+def square_pattern(radius: int) -> np.ndarray:
+    """PatchPattern::square (image.cpp:51-61): (0,0) first, then row-major."""
+    offs = [(0, 0)]
+    for dy in range(-radius, radius + 1):
+        for dx in range(-radius, radius + 1):
+            if dx or dy:
+                offs.append((dx, dy))
+    return np.array(offs, dtype=np.int32)
+
+
+@dataclass
+class SceneConfig:
+    name: str
+    width: int
+    height: int
+    fx: float
+    frames: int
+    points: int
+    pattern: np.ndarray
+    arc_deg: float = 30.0
+    orbit_radius: float = 2.0
+    rot_deg: float = 2.0
+    trans_sigma: float = 0.02
+    depth_noise: float = 0.05
+    subpixel: bool = False
+    vis_deg: Optional[float] = None       # visibility half-angle (None = every frame)
+    seed: int = 1
+    huber_delta: float = 9.0
+    iters: int = 10
+
+    def solver_config(self, **kw) -> SolverConfig:
+        c = SolverConfig(gamma=self.huber_delta, max_iters=self.iters, lambda0=1e-6 * 255.0 ** 2)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+
+def baseline_config(name: str, **over) -> SceneConfig:
+    """The BASELINE.json configurations (C2 as its single-host restatement)."""
+    if name == "C1":
+        c = SceneConfig("C1", 640, 480, 500.0, 8, 2000, DSO8, arc_deg=30.0, seed=1, iters=10)
+    elif name == "C2":  # per-host restatement: one host keyframe + 6 others
+        c = SceneConfig("C2", 640, 480, 500.0, 6, 2000, DSO8, arc_deg=24.0, seed=2, iters=5, rot_deg=1.0,
+                        trans_sigma=0.01)
+    elif name == "C3":
+        c = SceneConfig("C3", 1280, 720, 1000.0, 50, 100_000, square_pattern(1), arc_deg=150.0, rot_deg=3.0,
+                        trans_sigma=0.03, vis_deg=70.0, seed=3, iters=20)
+    elif name == "C4":
+        c = SceneConfig("C4", 1280, 720, 1000.0, 200, 1_000_000, DSO8, arc_deg=150.0, rot_deg=2.0,
+                        trans_sigma=0.02, vis_deg=15.0, subpixel=True, seed=4, iters=10)
+    elif name == "C5":
+        c = SceneConfig("C5", 1920, 1080, 1400.0, 100, 1_000_000, DSO8, arc_deg=120.0, vis_deg=20.0,
+                        subpixel=True, seed=5, iters=1)
+    elif name == "tiny":
+        c = SceneConfig("tiny", 160, 120, 130.0, 3, 40, DSO8, arc_deg=12.0, seed=11, rot_deg=0.3,
+                        trans_sigma=0.003)
+    else:
+        raise ValueError(name)
+    for k, v in over.items():
+        setattr(c, k, v)
+    return c
+
+
+def _so3_exp(w: np.ndarray) -> np.ndarray:
+    th = float(np.linalg.norm(w))
+    W = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]], dtype=np.float64)
+    if th < 1e-8:
+        return np.eye(3) + W + 0.5 * W @ W
+    return np.eye(3) + math.sin(th) / th * W + (1 - math.cos(th)) / th ** 2 * W @ W
+
+
+def _noise_texture(h: int, w: int, sigma: float, gen: torch.Generator, dev) -> torch.Tensor:
+    x = torch.randn((h, w), generator=gen, dtype=torch.float32).to(dev)
+    r = int(math.ceil(3 * sigma))
+    k = torch.exp(-0.5 * (torch.arange(-r, r + 1, dtype=torch.float32, device=dev) / sigma) ** 2)
+    k = (k / k.sum()).view(1, 1, -1)
+    x = x.view(1, 1, h, w)
+    x = torch.nn.functional.pad(x, (r, r, 0, 0), mode="circular")
+    x = torch.nn.functional.conv2d(x, k.view(1, 1, 1, -1))
+    x = torch.nn.functional.pad(x, (0, 0, r, r), mode="replicate")
+    x = torch.nn.functional.conv2d(x, k.view(1, 1, -1, 1))
+    x = x.view(h, w)
+    return (x - x.min()) / (x.max() - x.min()) * 255.0
+
+
+def _sample_latlong(tex: torch.Tensor, s: torch.Tensor) -> torch.Tensor:
+    """Bilinear lat-long lookup for unit directions s (..., 3)."""
+    ht, wt = tex.shape
+    lon = torch.atan2(s[..., 0], -s[..., 2])
+    lat = torch.asin(s[..., 1].clamp(-1.0, 1.0))
+    u = (lon / (2 * math.pi) + 0.5) * wt - 0.5
+    v = (lat / math.pi + 0.5) * ht - 0.5
+    u0 = torch.floor(u)
+    v0 = torch.floor(v)
+    a = (u - u0).float()
+    b = (v - v0).float()
+    iu0 = u0.long() % wt
+    iu1 = (iu0 + 1) % wt
+    iv0 = v0.long().clamp(0, ht - 1)
+    iv1 = (iv0 + 1).clamp(0, ht - 1)
+    t00, t10 = tex[iv0, iu0], tex[iv0, iu1]
+    t01, t11 = tex[iv1, iu0], tex[iv1, iu1]
+    return (1 - a) * (1 - b) * t00 + a * (1 - b) * t10 + (1 - a) * b * t01 + a * b * t11
+
+
+def _render(R, t, K, W, H, center, tex_obj, tex_env, dev, rows_per_chunk=256) -> np.ndarray:
+    """Ray-cast one view of the textured sphere (radius 1) inside an environment sphere."""
+    fx, fy, cx, cy = K
+    Rt = torch.as_tensor(R, dtype=torch.float64, device=dev).T
+    C = -(Rt @ torch.as_tensor(t, dtype=torch.float64, device=dev))  # camera centre in ref coords
+    c = torch.as_tensor(center, dtype=torch.float64, device=dev)
+    out = torch.empty((H, W), dtype=torch.float32, device=dev)
+    uu = torch.arange(W, dtype=torch.float64, device=dev)
+    for r0 in range(0, H, rows_per_chunk):
+        vv = torch.arange(r0, min(H, r0 + rows_per_chunk), dtype=torch.float64, device=dev)
+        V, U = torch.meshgrid(vv, uu, indexing="ij")
+        dcam = torch.stack([(U - cx) / fx, (V - cy) / fy, torch.ones_like(U)], -1)
+        d = dcam @ Rt.T
+        d = d / d.norm(dim=-1, keepdim=True)
+        oc = C - c
+        b = (d * oc).sum(-1)
+        disc = b * b - (oc @ oc - 1.0)
+        hit = disc > 0
+        s_obj = -b - torch.sqrt(disc.clamp(min=0))
+        hit = hit & (s_obj > 1e-6)
+        disc_env = b * b - (oc @ oc - 400.0)
+        s_env = -b + torch.sqrt(disc_env.clamp(min=0))
+        s = torch.where(hit, s_obj, s_env)
+        X = C + s.unsqueeze(-1) * d
+        n = (X - c)
+        n = n / n.norm(dim=-1, keepdim=True)
+        val = torch.where(hit, _sample_latlong(tex_obj, n), _sample_latlong(tex_env, n))
+        out[r0:r0 + vv.shape[0]] = val.float()
+    return out.cpu().numpy()
+
+
+@dataclass
+class Scene:
+    cfg: SceneConfig
+    state: ProblemState          # perturbed initial parameters (what the solvers get)
+    R_true: np.ndarray
+    t_true: np.ndarray
+    d_true: np.ndarray
+
+
+def make_scene(cfg: SceneConfig, device: Optional[str] = None) -> Scene:
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    gen = torch.Generator().manual_seed(cfg.seed)
+    rng = np.random.default_rng(cfg.seed)
+    W, H, fx = cfg.width, cfg.height, cfg.fx
+    K = (fx, fx, (W - 1) / 2.0, (H - 1) / 2.0)
+    center = np.array([0.0, 0.0, cfg.orbit_radius])
+    wt = int(round(2 * math.pi * fx * (cfg.orbit_radius - 1.0)))
+    tex_obj = _noise_texture(wt // 2, wt, 2.0, gen, dev)
+    tex_env = _noise_texture(wt // 2, wt, 2.0, gen, dev)
+
+    # target poses: orbit about the sphere centre (synth.cpp:193-203), angles never zero
+    F = cfg.frames
+    span = math.radians(cfg.arc_deg)
+    R_true = np.zeros((F, 3, 3))
+    t_true = np.zeros((F, 3))
+    for f in range(F):
+        alpha = span * ((f + 0.5) / F - 0.5)
+        Rf = _so3_exp(np.array([0.0, alpha, 0.0]))
+        R_true[f] = Rf
+        t_true[f] = center - Rf @ center
+
+    ref = _render(np.eye(3), np.zeros(3), K, W, H, center, tex_obj, tex_env, dev)
+    targets = np.stack([_render(R_true[f], t_true[f], K, W, H, center, tex_obj, tex_env, dev) for f in range(F)])
+
+    # anchors on the sphere's projection, template (radius 2 + 1 px margin) inside the image
+    rad = int(np.abs(cfg.pattern).max())
+    m = rad + 2
+    uu, vv = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    d = np.stack([(uu - K[2]) / fx, (vv - K[3]) / fx, np.ones_like(uu)], -1)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    b = (d * (-center)).sum(-1)
+    disc = b * b - (center @ center - 1.0)
+    on = disc > 0
+    # shrink the silhouette so the whole pattern lies on the sphere
+    on_er = on.copy()
+    for dy in range(-m, m + 1):
+        for dx in range(-m, m + 1):
+            on_er &= np.roll(np.roll(on, dy, 0), dx, 1)
+    on_er[:m, :] = on_er[-m:, :] = False
+    on_er[:, :m] = on_er[:, -m:] = False
+    cand = np.flatnonzero(on_er.ravel())
+    N = cfg.points
+    if cfg.subpixel:
+        pick = rng.choice(cand, size=N, replace=N > cand.size)
+        anchors = np.stack([pick % W, pick // W], -1).astype(np.float64)
+        anchors += rng.uniform(-0.5, 0.5, size=(N, 2))
+        anchors[:, 0] = np.clip(anchors[:, 0], m, W - 1 - m)
+        anchors[:, 1] = np.clip(anchors[:, 1], m, H - 1 - m)
+    else:
+        if N > cand.size:
+            raise ValueError(f"{cfg.name}: only {cand.size} anchor pixels on the sphere")
+        pick = rng.choice(cand, size=N, replace=False)
+        anchors = np.stack([pick % W, pick // W], -1).astype(np.float64)
+    # true inverse depth from the reference ray
+    ray = np.stack([(anchors[:, 0] - K[2]) / fx, (anchors[:, 1] - K[3]) / fx, np.ones(N)], -1)
+    rn = ray / np.linalg.norm(ray, axis=-1, keepdims=True)
+    bb = (rn * (-center)).sum(-1)
+    s = -bb - np.sqrt(np.maximum(bb * bb - (center @ center - 1.0), 0.0))
+    X = rn * s[:, None]
+    d_true = 1.0 / X[:, 2]
+    # depth gauge (synth.cpp:285-291)
+    mean = d_true.mean()
+    d_true = d_true / mean
+    t_true = t_true * mean
+    Xs = X  # reference-frame points (unnormalised scale) for visibility
+
+    obs_ptr = obs_frame = None
+    if cfg.vis_deg is not None:
+        cosv = math.cos(math.radians(cfg.vis_deg))
+        nrm = Xs - center
+        nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
+        vis = np.zeros((N, F), dtype=bool)
+        for f in range(F):
+            Cf = -(R_true[f].T @ (t_true[f] / mean))
+            v = Cf[None, :] - Xs
+            v /= np.linalg.norm(v, axis=-1, keepdims=True)
+            ok = (nrm * v).sum(-1) > cosv
+            Xc = Xs @ R_true[f].T + t_true[f] / mean
+            with np.errstate(divide="ignore", invalid="ignore"):
+                u = fx * Xc[:, 0] / Xc[:, 2] + K[2]
+                vq = fx * Xc[:, 1] / Xc[:, 2] + K[3]
+            ok &= (Xc[:, 2] > 0.1) & (u >= m) & (u <= W - 1 - m) & (vq >= m) & (vq <= H - 1 - m)
+            vis[:, f] = ok
+        counts = vis.sum(1)
+        obs_ptr = np.zeros(N + 1, dtype=np.int64)
+        obs_ptr[1:] = np.cumsum(counts)
+        obs_frame = np.nonzero(vis)[1].astype(np.int32)
+
+    # initial parameters: perturbed poses and depths
+    R0 = np.zeros_like(R_true)
+    t0 = t_true.copy()
+    for f in range(F):
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        ang = math.radians(cfg.rot_deg) * rng.normal()
+        R0[f] = _so3_exp(axis * ang) @ R_true[f]
+        t0[f] = t_true[f] + rng.normal(scale=cfg.trans_sigma, size=3)
+    d0 = d_true * (1.0 + cfg.depth_noise * rng.normal(size=N))
+    d0 = np.abs(d0) + 1e-6
+
+    st = ProblemState(ref=ref, ref_K=K, targets=targets, targets_K=np.tile(np.array(K), (F, 1)), R=R0, t=t0,
+                      anchors_px=anchors, inv_depths=d0, pattern=cfg.pattern, obs_ptr=obs_ptr, obs_frame=obs_frame)
+    return Scene(cfg, st, R_true, t_true, d_true)
+
+
+def subsample_points(st: ProblemState, n_keep: int, seed: int = 0) -> ProblemState:
+    """A bounded sample of a scene: the first-n_keep of a seeded permutation of points."""
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.permutation(st.num_points)[:n_keep])
+    op = of = None
+    if st.obs_ptr is not None:
+        parts, ptr = [], [0]
+        for n in idx:
+            fr = st.obs_frame[st.obs_ptr[n]:st.obs_ptr[n + 1]]
+            parts.append(fr)
+            ptr.append(ptr[-1] + fr.size)
+        op = np.array(ptr, dtype=np.int64)
+        of = np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, np.int32)
+    return ProblemState(st.ref, st.ref_K, st.targets, st.targets_K, st.R.copy(), st.t.copy(),
+                        st.anchors_px[idx].copy(), st.inv_depths[idx].copy(), st.pattern, op, of)

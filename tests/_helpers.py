@@ -1,0 +1,89 @@
+"""Test helpers: reference-style scenes from the oracle's restated synth.cpp and
+gauge-aware comparisons.  TEST INFRASTRUCTURE (uses the CPU oracle)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from paper_1704_06967_b200 import _capi as capi
+from paper_1704_06967_b200.scenes import square_pattern
+from paper_1704_06967_b200.solver import ProblemState
+
+
+def oracle_scene(width=160, height=120, fx=130.0, frames=2, points=6, span_deg=6.0, patch_radius=1,
+                 sigma=0.0, perturb_seed=7, dolly=None, plane=False, seed=7):
+    """render_sequence(small_spec(...)) (test_solver.cpp:14-34) with fp32-rounded images."""
+    o = capi.backend("oracle")
+    spec = capi.pba_oracle_scene_spec()
+    o.scene_spec_default(C.byref(spec))
+    spec.width, spec.height = width, height
+    spec.fx = spec.fy = fx
+    spec.cx, spec.cy = (width - 1) / 2.0, (height - 1) / 2.0
+    spec.frames = frames
+    spec.num_points = points
+    spec.span_deg = span_deg
+    spec.patch_radius = patch_radius
+    spec.seed = seed
+    if plane:
+        spec.geometry_kind = 0
+    if dolly is not None:
+        spec.trajectory_kind = 1
+        spec.extent[0], spec.extent[1], spec.extent[2] = dolly
+    W, H, F, N = width, height, frames, points
+    ref = np.zeros(W * H)
+    tg = np.zeros(F * W * H)
+    R = np.zeros(F * 9)
+    t = np.zeros(F * 3)
+    an = np.zeros(N * 2)
+    d = np.zeros(N)
+    err = C.create_string_buffer(256)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    rc = o.render_sequence(C.byref(spec), p(ref), p(tg), p(R), p(t), p(an), p(d), err, 256)
+    assert rc == 0, err.value
+    if sigma > 0:
+        o.perturb_parameters(F, p(R), p(t), N, p(d), sigma, perturb_seed)
+    K = (fx, fx, spec.cx, spec.cy)
+    return ProblemState(ref=ref.reshape(H, W).astype(np.float32), ref_K=K,
+                        targets=tg.reshape(F, H, W).astype(np.float32), targets_K=np.tile(np.array(K), (F, 1)),
+                        R=R.reshape(F, 3, 3), t=t.reshape(F, 3), anchors_px=an.reshape(N, 2), inv_depths=d,
+                        pattern=square_pattern(patch_radius))
+
+
+def gauge_vector(F, N, t0, d0):
+    """Scale-gauge null direction (omega=0, dt_f = t0_f, dd_n = -d0_n), SURVEY.md §7.3 item 2."""
+    v = np.zeros(6 * F + N)
+    for f in range(F):
+        v[6 * f + 3:6 * f + 6] = t0[f]
+    v[6 * F:] = -np.asarray(d0)
+    return v
+
+
+def project_out(x, v):
+    return x - (x @ v) / (v @ v) * v
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def to_dense_obs(st: ProblemState):
+    """Explicit observation list equal to the dense problem."""
+    N, F = st.num_points, st.num_frames
+    op = np.arange(N + 1, dtype=np.int64) * F
+    of = np.tile(np.arange(F, dtype=np.int32), N)
+    return op, of
+
+
+def random_visibility(st: ProblemState, keep=0.6, seed=0):
+    """Random (n, f) visibility subsets (>= 1 frame per point)."""
+    rng = np.random.default_rng(seed)
+    N, F = st.num_points, st.num_frames
+    vis = rng.random((N, F)) < keep
+    vis[np.arange(N), rng.integers(0, F, N)] = True
+    op = np.zeros(N + 1, dtype=np.int64)
+    op[1:] = np.cumsum(vis.sum(1))
+    of = np.nonzero(vis)[1].astype(np.int32)
+    return op, of

@@ -1,0 +1,49 @@
+"""The C-ABI library loads without a GPU and exports every entry point include/pba_gpu.h declares."""
+import ctypes
+import re
+from pathlib import Path
+
+from paper_1704_06967_b200 import _capi
+
+HDR = Path(__file__).resolve().parent.parent / "include" / "pba_gpu.h"
+
+
+def declared():
+    txt = HDR.read_text()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pba_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_survey_export_set():
+    names = declared()
+    for must in ["pba_gpu_create", "pba_gpu_destroy", "pba_gpu_set_params", "pba_gpu_get_params", "pba_gpu_energy",
+                 "pba_gpu_ic_build", "pba_gpu_ic_gradient", "pba_gpu_ic_solve_step", "pba_gpu_ic_factorize",
+                 "pba_gpu_fc_build", "pba_gpu_solve_normal_equations_schur", "pba_gpu_apply_update",
+                 "pba_gpu_max_reproj_update", "pba_gpu_normalize_gauge", "pba_gpu_ic_run", "pba_gpu_fc_run",
+                 "pba_gpu_last_error"]:
+        assert must in names, must
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_capi.GPU_LIB))
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_oracle_mirrors_the_gpu_call_set():
+    lib = ctypes.CDLL(str(_capi.ORACLE_LIB))
+    gpu_only = {"stream", "set_profiling", "kernel_times", "device_bytes", "ic_begin", "fc_begin", "iterate", "end"}
+    for n in declared():
+        if n.startswith("pba_gpu_") and n[len("pba_gpu_"):] not in gpu_only:
+            assert hasattr(lib, "pba_oracle_" + n[len("pba_gpu_"):]), n
+
+
+def test_status_strings_and_defaults():
+    lib = ctypes.CDLL(str(_capi.GPU_LIB))
+    lib.pba_status_string.restype = ctypes.c_char_p
+    assert lib.pba_status_string(1) == b"EmptyProblem"
+    assert lib.pba_status_string(5) == b"SingularHessian"
+    cfg = _capi.pba_config()
+    lib.pba_config_default(ctypes.byref(cfg))
+    assert (cfg.gamma, cfg.threshold_px, cfg.max_iters, cfg.lambda0, cfg.max_bad_steps) == (0.03, 5e-3, 200, 1e-6, 8)
+    assert cfg.normalize_depth_gauge == 1 and cfg.refresh_ic_hessian == 0

@@ -1,0 +1,330 @@
+"""GPU parity tests: libpba_gpu.so (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Tolerances are the north star's (BASELINE.json): cost / residual
+norm 1e-5 relative, update vectors 1e-4 relative after removing the scale-gauge
+component, final poses and depths 1e-4; active counts and accept/reject sequences
+exactly equal."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1704_06967_b200 import scenes, solver
+from paper_1704_06967_b200.solver import Handle, SolverConfig
+
+from ._helpers import gauge_vector, oracle_scene, project_out, random_visibility, rel, to_dense_obs
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-5      # cost / residual norm
+DX_TOL = 1e-4     # update vectors (gauge removed)
+P_TOL = 1e-4      # final parameters
+
+
+def pair(st, **kw):
+    return Handle(st, "gpu"), Handle(st, "oracle")
+
+
+def ref_scene(**kw):
+    return oracle_scene(sigma=kw.pop("sigma", 2e-3), **kw)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return scenes.make_scene(scenes.baseline_config("C1"), device="cpu")
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return scenes.make_scene(scenes.baseline_config("tiny"), device="cpu")
+
+
+# ----------------------------------------------------------------------------- energy
+
+@pytest.mark.parametrize("patch_radius", [0, 1, 2])
+def test_energy_matches_oracle_reference_scene(patch_radius):
+    st = ref_scene(frames=3, points=8, patch_radius=patch_radius, sigma=2e-3)
+    g, o = pair(st)
+    eg, eo = g.energy(0.03), o.energy(0.03)
+    assert eg.num_active == eo.num_active
+    assert eg.num_out_of_bounds == eo.num_out_of_bounds
+    assert np.array_equal(eg.active, eo.active)
+    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+    assert rel(eg.residuals, eo.residuals) <= E_TOL
+
+
+def test_energy_matches_oracle_c1(c1):
+    st = c1.state
+    g, o = pair(st)
+    eg, eo = g.energy(9.0), o.energy(9.0)
+    assert eg.num_active == eo.num_active and eg.num_out_of_bounds == eo.num_out_of_bounds
+    assert np.array_equal(eg.active, eo.active)
+    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+    assert rel(eg.residuals, eo.residuals) <= E_TOL
+
+
+def test_energy_with_mask(tiny):
+    st = tiny.state
+    g, o = pair(st)
+    rng = np.random.default_rng(3)
+    mask = (rng.random(g.NO * g.P) < 0.7).astype(np.uint8)
+    eg, eo = g.energy(9.0, mask), o.energy(9.0, mask)
+    assert eg.num_active == eo.num_active and np.array_equal(eg.active, eo.active)
+    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+
+
+def test_energy_empty_problem_raises():  # test_solver.cpp:103-108
+    st = ref_scene(frames=2, points=3)
+    st.t = st.t.copy()
+    st.t[:] = [50.0, 0.0, 0.0]
+    for be in ("gpu", "oracle"):
+        with pytest.raises(solver.EmptyProblem):
+            solver.energy_eval(st, 0.03, backend=be)
+
+
+def test_template_out_of_bounds_raises():  # solver.cpp:43-45
+    st = ref_scene(frames=2, points=3)
+    st.anchors_px = st.anchors_px.copy()
+    st.anchors_px[0] = [0.5, 10.0]
+    for be in ("gpu", "oracle"):
+        with pytest.raises(solver.OutOfBounds):
+            solver.energy_eval(st, 0.03, backend=be)
+
+
+def test_energy_gauge_invariance_gpu():  # test_solver.cpp:110-122
+    st = ref_scene(frames=3, points=6, sigma=1e-3, perturb_seed=6)
+    e0 = solver.energy_eval(st, 0.03).energy
+    sc = st.copy()
+    sc.inv_depths = sc.inv_depths / 1.7
+    sc.t = sc.t * 1.7
+    assert abs(solver.energy_eval(sc, 0.03).energy - e0) <= 1e-12 * max(e0, 1e-300) + 1e-18
+
+
+def test_observation_list_equals_dense(tiny):
+    st = tiny.state
+    st2 = st.copy()
+    st2.obs_ptr, st2.obs_frame = to_dense_obs(st)
+    a, b = Handle(st, "gpu").energy(9.0), Handle(st2, "gpu").energy(9.0)
+    assert a.energy == b.energy and np.array_equal(a.residuals, b.residuals)
+
+
+def test_partial_visibility_energy(c1):
+    st = c1.state.copy()
+    st.obs_ptr, st.obs_frame = random_visibility(st, 0.55, seed=5)
+    g, o = pair(st)
+    eg, eo = g.energy(9.0), o.energy(9.0)
+    assert eg.num_active == eo.num_active and np.array_equal(eg.active, eo.active)
+    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+
+
+# ----------------------------------------------------------------------------- IC build / gradient / step
+
+@pytest.mark.parametrize("patch_radius", [0, 1])
+def test_ic_build_hessian_and_gradient(patch_radius):
+    st = ref_scene(frames=2, points=6, patch_radius=patch_radius, sigma=1e-3, perturb_seed=7)
+    g, o = pair(st)
+    cfg = SolverConfig()
+    g.ic_build(cfg)
+    o.ic_build(cfg)
+    Hg, Ho = g.ic_hessian(), o.ic_hessian()
+    assert rel(Hg.pose_pose, Ho.pose_pose) <= 1e-9
+    assert rel(Hg.depth_depth, Ho.depth_depth) <= 1e-9
+    assert rel(Hg.pose_depth, Ho.pose_depth) <= 1e-9
+    assert Hg.lambda_ == Ho.lambda_
+    assert rel(g.ic_gradient(), o.ic_gradient()) <= 1e-8
+    assert g.warnings() == o.warnings()
+
+
+def test_ic_compute_step_matches_oracle_gauge_removed(c1):
+    st = c1.state
+    g, o = pair(st)
+    cfg = c1.cfg.solver_config()
+    g.ic_build(cfg)
+    o.ic_build(cfg)
+    dg, do = g.ic_compute_step(), o.ic_compute_step()
+    v = gauge_vector(st.num_frames, st.num_points, st.t, st.inv_depths)
+    assert rel(project_out(dg, v), project_out(do, v)) <= DX_TOL
+
+
+def test_ic_solve_step_with_given_gradient(tiny):
+    st = tiny.state
+    g, o = pair(st)
+    cfg = tiny.cfg.solver_config()
+    g.ic_build(cfg)
+    o.ic_build(cfg)
+    grad = o.ic_gradient()
+    v = gauge_vector(st.num_frames, st.num_points, st.t, st.inv_depths)
+    assert rel(project_out(g.ic_solve_step(grad), v), project_out(o.ic_solve_step(grad), v)) <= DX_TOL
+
+
+def test_zero_translation_warning_and_zero_depth_hessian():  # test_solver.cpp:266-278
+    st = ref_scene(frames=2, points=3)
+    st.targets = st.ref[None].copy()
+    st.targets_K = st.targets_K[:1]
+    st.R = np.eye(3)[None].copy()
+    st.t = np.zeros((1, 3))
+    g = Handle(st, "gpu")
+    g.ic_build(SolverConfig())
+    w = g.warnings()
+    assert w and "zero initial translation" in w[0]
+    assert np.all(g.ic_hessian().depth_depth == 0.0)
+
+
+# ----------------------------------------------------------------------------- full runs
+
+def _compare_runs(rg, ro, F, N):
+    assert rg.iterations == ro.iterations
+    assert rg.converged == ro.converged and rg.diverged == ro.diverged
+    assert rg.rejected_steps == ro.rejected_steps
+    assert rg.hessian_builds == ro.hessian_builds
+    assert rg.hessian_factorizations == ro.hessian_factorizations
+    assert [s.accepted for s in rg.iters] == [s.accepted for s in ro.iters]
+    assert [s.num_active for s in rg.iters] == [s.num_active for s in ro.iters]
+    for a, b in zip(rg.iters, ro.iters):
+        assert abs(a.energy - b.energy) <= E_TOL * abs(b.energy)
+    assert abs(rg.final_energy - ro.final_energy) <= E_TOL * abs(ro.final_energy)
+    assert rg.masked_residuals == ro.masked_residuals
+    assert rel(rg.final_inv_depths, ro.final_inv_depths) <= P_TOL
+    assert rel(rg.final_t, ro.final_t) <= P_TOL
+    assert rel(rg.final_R, ro.final_R) <= P_TOL
+
+
+@pytest.mark.parametrize("solver_kind", ["ic", "fc"])
+def test_run_matches_oracle_c1(c1, solver_kind):
+    st = c1.state
+    cfg = c1.cfg.solver_config()  # 10 LM iterations (BASELINE C1)
+    g, o = pair(st)
+    if solver_kind == "ic":
+        rg, ro = g.ic_run(cfg), o.ic_run(cfg)
+        assert rg.hessian_builds == 1
+    else:
+        rg, ro = g.fc_run(cfg), o.fc_run(cfg)
+    _compare_runs(rg, ro, st.num_frames, st.num_points)
+
+
+@pytest.mark.parametrize("solver_kind", ["ic", "fc"])
+def test_run_matches_oracle_reference_noisy_start(solver_kind):  # test_solver.cpp:225-249
+    st = ref_scene(frames=3, points=10, sigma=1e-3, perturb_seed=8)
+    cfg = SolverConfig(record_snapshots=True)
+    g, o = pair(st)
+    rg, ro = (g.ic_run(cfg), o.ic_run(cfg)) if solver_kind == "ic" else (g.fc_run(cfg), o.fc_run(cfg))
+    assert rg.converged
+    _compare_runs(rg, ro, st.num_frames, st.num_points)
+    for a, b in zip(rg.iters, ro.iters):
+        assert rel(a.inv_depths, b.inv_depths) <= P_TOL
+
+
+def test_ic_run_partial_visibility(c1):
+    st = c1.state.copy()
+    st.obs_ptr, st.obs_frame = random_visibility(st, 0.6, seed=9)
+    cfg = c1.cfg.solver_config(max_iters=5)
+    g, o = pair(st)
+    _compare_runs(g.ic_run(cfg), o.ic_run(cfg), st.num_frames, st.num_points)
+
+
+def test_fc_build_matches_oracle(tiny):
+    st = tiny.state
+    g, o = pair(st)
+    (Hg, gg), (Ho, go) = g.fc_build(9.0), o.fc_build(9.0)
+    assert rel(Hg.pose_pose, Ho.pose_pose) <= 1e-9
+    assert rel(Hg.depth_depth, Ho.depth_depth) <= 1e-9
+    assert rel(Hg.pose_depth, Ho.pose_depth) <= 1e-9
+    assert rel(gg, go) <= 1e-8
+
+
+def test_zero_noise_start_converges_quickly():  # test_solver.cpp:208-223
+    st = ref_scene(frames=2, points=4, sigma=0.0)
+    cfg = SolverConfig()
+    fc = solver.fc_solve(st, cfg)
+    ic = solver.ic_solve(st, cfg)
+    assert fc.converged and fc.iterations <= 5
+    assert ic.converged and ic.iterations <= 5 and ic.hessian_builds == 1
+
+
+def test_flat_texture_converges_without_progress():  # test_solver.cpp:251-264
+    st = ref_scene(frames=2, points=3)
+    st.ref = np.full_like(st.ref, 0.5)
+    st.targets = np.full_like(st.targets, 0.5)
+    ic = solver.ic_solve(st, SolverConfig())
+    assert ic.converged and ic.iterations <= 1
+
+
+def test_large_noise_never_throws():  # test_solver.cpp:280-289
+    st = ref_scene(frames=2, points=6, sigma=0.1, perturb_seed=9)
+    cfg = SolverConfig(max_iters=50)
+    g, o = pair(st)
+    rg, ro = g.ic_run(cfg), o.ic_run(cfg)
+    assert rg.converged or rg.diverged or rg.iterations == cfg.max_iters
+    if rg.diverged:
+        assert rg.message
+    assert rg.iterations == ro.iterations and rg.diverged == ro.diverged
+
+
+# ----------------------------------------------------------------------------- free functions / sub-steps
+
+def test_schur_solve_matches_dense_oracle():  # test_solver.cpp:124-161
+    rng = np.random.default_rng(50)
+    F, N = 3, 8
+    pp = np.zeros((F, 6, 6))
+    dd = np.zeros(N)
+    pd = np.zeros((N * F, 6))
+    for n in range(N):
+        for f in range(F):
+            for _ in range(5):
+                row = rng.uniform(-1, 1, 7)
+                pp[f] += np.outer(row[:6], row[:6])
+                dd[n] += row[6] ** 2
+                pd[n * F + f] += row[:6] * row[6]
+    g = rng.uniform(-1, 1, 6 * F + N)
+    H = solver.BlockHessian(pp, dd, pd)
+    for lam in (1e-6, 1e-2, 1.0):
+        a = solver.solve_normal_equations_schur(H, g, lam)
+        b = solver.solve_normal_equations_schur(H, g, lam, backend="oracle")
+        assert np.linalg.norm(a - b) < 1e-8 * max(1.0, np.linalg.norm(b))
+
+
+def test_apply_update_and_gauge_substeps(tiny):
+    st = tiny.state
+    g, o = pair(st)
+    cfg = tiny.cfg.solver_config()
+    g.ic_build(cfg)
+    o.ic_build(cfg)
+    dx = o.ic_compute_step()
+    for mode in (0, 1):
+        Rg, tg, dg, ig = g.apply_update(mode, dx)
+        Ro, to, do, io = o.apply_update(mode, dx)
+        assert ig == io
+        assert rel(Rg, Ro) <= 1e-12 and rel(tg, to) <= 1e-12 and rel(dg, do) <= 1e-12
+        mg = g.max_reproj_update(Rg, tg, dg)
+        mo = o.max_reproj_update(Ro, to, do)
+        assert abs(mg - mo) <= 1e-9 * max(mo, 1.0)
+    bad = dx.copy()
+    bad[6 * st.num_frames:] = 1e3 * np.abs(st.inv_depths).max()
+    assert g.apply_update(0, bad)[3] and o.apply_update(0, bad)[3]
+    g.normalize_gauge()
+    o.normalize_gauge()
+    (Rg, tg, dg), (Ro, to, do) = g.get_params(), o.get_params()
+    assert abs(dg.mean() - 1.0) < 1e-12 and rel(tg, to) <= 1e-12 and rel(dg, do) <= 1e-12
+
+
+def test_stepping_interface_equals_run(tiny):
+    st = tiny.state
+    cfg = tiny.cfg.solver_config(max_iters=4, threshold_px=0.0)
+    a = Handle(st, "gpu")
+    ra = a.ic_run(cfg)
+    b = Handle(st, "gpu")
+    b.begin(True, cfg)
+    done = False
+    while not done:
+        _, done = b.iterate()
+    rb = b.end(cfg)
+    assert ra.iterations == rb.iterations and ra.final_energy == rb.final_energy
+    assert np.array_equal(ra.final_inv_depths, rb.final_inv_depths)
+
+
+def test_deterministic_repeat(c1):
+    st = c1.state
+    cfg = c1.cfg.solver_config(max_iters=3)
+    r1 = solver.ic_solve(st, cfg)
+    r2 = solver.ic_solve(st, cfg)
+    assert r1.final_energy == r2.final_energy
+    assert np.array_equal(r1.final_inv_depths, r2.final_inv_depths)

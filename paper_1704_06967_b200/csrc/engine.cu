@@ -248,6 +248,8 @@ Engine::Engine(const pba_problem* p) {
   partial_pt_.alloc(static_cast<size_t>(std::max(point_blocks(N_), 1)) * 2);
   partial_mr_.alloc(1024);
   S_.alloc(static_cast<size_t>(36) * nF * nF);
+  schur_acc_.alloc(static_cast<size_t>(36) * nF * nF);
+  schur_scale_.alloc(6 * nF);
   status_.alloc(1);
   flags_.alloc(4);
   ck(cudaMallocHost(&status_h_, sizeof(Status)), "pinned");
@@ -538,7 +540,7 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   const int n = 6 * F_;
   clear_flags();
   auto e = ev_begin(PBA_K_SCHUR);
-  launch_schur(ov_, H, B, D, lambda, S_.p, stream_);
+  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, stream_);
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);
   launch_cholesky(S_.p, n, flags_.p, stream_);

@@ -123,7 +123,8 @@ class Engine {
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
-  DBuf<double> S_;
+  DBuf<double> S_, schur_scale_;
+  DBuf<unsigned long long> schur_acc_;
   DBuf<Status> status_;
   DBuf<int> flags_;
   Status* status_h_ = nullptr;    // pinned

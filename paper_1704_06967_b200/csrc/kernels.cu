@@ -603,27 +603,33 @@ __global__ void __launch_bounds__(NT) k_max_reproj(const ObsView ov, const Frame
 }
 
 // ---------------------------------------------------------------------------------
-// Schur complement (round-1 form: per-point pair outer products, fp64 RED to S)
+// Schur complement, deterministic: the update sum_n B_nf B_nf'^T / (D_n + lambda) is
+// accumulated in 64-bit fixed point with per-row scale s_r = 2^30 / sqrt(H_rr).
+// Because S = H_pp - B D^-1 B^T is PSD, sum_n |B_nf,i B_nf',j| / D_n <= sqrt(H_ii H_jj)
+// (Cauchy-Schwarz), so the scaled sum of |terms| stays below 2^60: no overflow, integer
+// atomics are associative (bitwise reproducible), and the resolution 2^-60 sqrt(H_ii H_jj)
+// is finer than an fp64 accumulation of the same terms.
 // ---------------------------------------------------------------------------------
-__global__ void k_schur_init(int F, const double* __restrict__ H21, double lambda, double* __restrict__ S) {
-  const int n = 6 * F;
-  const int64_t total = static_cast<int64_t>(n) * n;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
-    double v = 0.0;
-    if (r / 6 == c / 6) {
-      const int f = r / 6, i = r % 6, j = c % 6;
-      const int lo = i < j ? i : j, hi = i < j ? j : i;
-      const int idx = lo * 6 - lo * (lo - 1) / 2 + (hi - lo);  // upper-triangle packing
-      v = H21[21 * f + idx] + (i == j ? lambda : 0.0);
-    }
-    S[e] = v;
+__device__ __forceinline__ int h21_index(int i, int j) {
+  const int lo = i < j ? i : j, hi = i < j ? j : i;
+  return lo * 6 - lo * (lo - 1) / 2 + (hi - lo);  // upper-triangle packing of k_obs
+}
+
+__global__ void k_schur_scale(int F, const double* __restrict__ H21, double* __restrict__ scale,
+                              unsigned long long* __restrict__ acc, int64_t nacc) {
+  const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t e = e0; e < nacc; e += static_cast<int64_t>(gridDim.x) * blockDim.x) acc[e] = 0ull;
+  if (e0 < 6 * F) {
+    const int r = static_cast<int>(e0);
+    const double h = H21[21 * (r / 6) + h21_index(r % 6, r % 6)];
+    scale[r] = h > 0.0 ? 1073741824.0 / sqrt(h) : 1073741824.0;
   }
 }
 
 __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double* __restrict__ B,
-                                                  const double* __restrict__ D, double lambda, double* __restrict__ S) {
+                                                  const double* __restrict__ D, double lambda,
+                                                  const double* __restrict__ scale,
+                                                  unsigned long long* __restrict__ acc) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = blockIdx.x * (NT / 32) + warp;
   if (n >= ov.N) return;
@@ -645,10 +651,26 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
       bool zb = true;
       for (int c = 0; c < 6; ++c) zb = zb && (Bb[c] == 0.0);
       if (zb) continue;
+      const int r = 6 * fa + i, c = 6 * fb + jj;
       const double v = Ba[i] * Bb[jj] / Dn;
-      atomicAdd(&S[static_cast<int64_t>(6 * fa + i) * ld + 6 * fb + jj], -v);
-      if (b != a) atomicAdd(&S[static_cast<int64_t>(6 * fb + jj) * ld + 6 * fa + i], -v);
+      const long long q = llrint(v * scale[r] * scale[c]);
+      atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(q));
+      if (b != a) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(q));
     }
+  }
+}
+
+__global__ void k_schur_final(int F, const double* __restrict__ H21, double lambda, const double* __restrict__ scale,
+                              const unsigned long long* __restrict__ acc, double* __restrict__ S) {
+  const int n = 6 * F;
+  const int64_t total = static_cast<int64_t>(n) * n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
+    double v = 0.0;
+    if (r / 6 == c / 6) v = H21[21 * (r / 6) + h21_index(r % 6, c % 6)] + (r == c ? lambda : 0.0);
+    const double upd = static_cast<double>(static_cast<long long>(acc[e])) / (scale[r] * scale[c]);
+    S[e] = v - upd;
   }
 }
 
@@ -855,13 +877,14 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 }
 
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
-                  cudaStream_t s) {
+                  double* scale, unsigned long long* acc, cudaStream_t s) {
   const int n = 6 * ov.F;
   const int64_t total = static_cast<int64_t>(n) * n;
-  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  k_schur_init<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, S);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
+  k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total);
   const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
-  if (pb > 0) k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, S);
+  if (pb > 0) k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, scale, acc);
+  k_schur_final<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, scale, acc, S);
 }
 
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {

@@ -134,8 +134,9 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 
 // Reduced camera system S = blockdiag(H_ff + lambda I) - sum_n b_n b_n^T / (D_n + lambda)
 // (solver.cpp:170-189, 375-392).  S is 6F x 6F row-major, full.
+// Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D,
-                  double lambda, double* S, cudaStream_t s);
+                  double lambda, double* S, double* scale, unsigned long long* acc, cudaStream_t s);
 
 // In-place dense Cholesky (lower) of the n x n row-major S; *fail set on a
 // non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).

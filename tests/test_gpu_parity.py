@@ -179,9 +179,13 @@ def _compare_runs(rg, ro, F, N):
     assert rg.hessian_factorizations == ro.hessian_factorizations
     assert [s.accepted for s in rg.iters] == [s.accepted for s in ro.iters]
     assert [s.num_active for s in rg.iters] == [s.num_active for s in ro.iters]
+    # Along a trajectory the parameters themselves differ by roundoff amplified along the
+    # scale-gauge direction (damped only by lambda0), so energies of
+    # the two trajectories are compared at the parameter tolerance; the cost computation
+    # itself is checked to E_TOL at identical parameters (test_reported_energy_...).
     for a, b in zip(rg.iters, ro.iters):
-        assert abs(a.energy - b.energy) <= E_TOL * abs(b.energy)
-    assert abs(rg.final_energy - ro.final_energy) <= E_TOL * abs(ro.final_energy)
+        assert abs(a.energy - b.energy) <= P_TOL * abs(b.energy)
+    assert abs(rg.final_energy - ro.final_energy) <= P_TOL * abs(ro.final_energy)
     assert rg.masked_residuals == ro.masked_residuals
     assert rel(rg.final_inv_depths, ro.final_inv_depths) <= P_TOL
     assert rel(rg.final_t, ro.final_t) <= P_TOL
@@ -211,6 +215,20 @@ def test_run_matches_oracle_reference_noisy_start(solver_kind):  # test_solver.c
     _compare_runs(rg, ro, st.num_frames, st.num_points)
     for a, b in zip(rg.iters, ro.iters):
         assert rel(a.inv_depths, b.inv_depths) <= P_TOL
+
+
+@pytest.mark.parametrize("solver_kind", ["ic", "fc"])
+def test_reported_energy_is_the_cost_of_the_reported_parameters(solver_kind):
+    st = ref_scene(frames=3, points=10, sigma=1e-3, perturb_seed=8)
+    cfg = SolverConfig(record_snapshots=True)
+    g = Handle(st, "gpu")
+    rg = g.ic_run(cfg) if solver_kind == "ic" else g.fc_run(cfg)
+    for it in rg.iters:
+        s2 = st.copy()
+        s2.R, s2.t, s2.inv_depths = it.R, it.t, it.inv_depths
+        eo = solver.energy_eval(s2, cfg.gamma, backend="oracle")
+        assert abs(it.energy - eo.energy) <= E_TOL * eo.energy
+        assert it.num_active == eo.num_active
 
 
 def test_ic_run_partial_visibility(c1):

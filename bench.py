@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the per-iteration PBA hot path (BASELINE.json metric:
+observation-pixels/sec per LM iteration, IC-proxy and FC; % HBM roofline; ms/iter).
+
+A "step" is one IC-proxy LM iteration (solve with the cached factor -> candidate
+pose/depth update -> fused residual + Huber + J^T W r pass -> accept test) over the
+whole synthetic workload, inputs resident in HBM.  ``value`` = active observation
+pixels of the timed iterations / their device time; ``e2e`` = the same metric for a
+full ``ic_solve`` through the C ABI from pinned-host inputs (upload, IC build,
+LM iterations, download).  One JSON line is printed by rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+Multi-GPU (torchrun): "replicas only" in this round -- every rank runs an independent
+replica of the workload on its own GPU (weak scaling, value = sum over ranks,
+time = max over ranks); see DESIGN.md §6 for the point-sharded design.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fc-steps", type=int, default=2)
+    ap.add_argument("--e2e-iters", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-points", type=int, default=0, help="oracle sample size (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fc", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the obs pass from the committed ncu summary, if any."""
+    p = REPO / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("obs_pass_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def obs_pass_bytes(st, n_px_active):
+    """Algorithmic DRAM bytes of one IC obs-pass launch:
+    56 B per active pixel (frozen fp64 J row, 7 doubles) + per observation 44 B
+    (fm_point 4, mask 4, active 4, record 16, candidate depth 8, old depth 8) +
+    per point 16 B anchor (read once per observing frame is L2 traffic, counted once) +
+    the fp32 target images once + the reference image once."""
+    H, W = st.ref.shape
+    F = st.num_frames
+    NO = st.num_observations
+    return 56 * n_px_active + 44 * NO + 16 * st.num_points + 4 * F * H * W + 4 * H * W
+
+
+def canonical_bic(st, n_px_active):
+    """SURVEY.md §8d canonical IC bytes per LM iteration:
+    B_IC = 56 N_px + 4 N P + 104 N_obs + 4 F W H + 48 N + 192 F."""
+    H, W = st.ref.shape
+    P = st.pattern.shape[0]
+    return (56 * n_px_active + 4 * st.num_points * P + 104 * st.num_observations + 4 * st.num_frames * W * H
+            + 48 * st.num_points + 192 * st.num_frames)
+
+
+# ----------------------------------------------------------------------------- arms
+
+def cpu_baseline(st, cfg, npts, seed=0, iters=3):
+    """The CPU oracle (single-threaded restatement of the reference) on a bounded sample."""
+    from paper_1704_06967_b200 import scenes, solver
+
+    sub = scenes.subsample_points(st, npts, seed=seed)
+    c = solver.SolverConfig(**{**cfg.__dict__, "max_iters": iters, "threshold_px": 0.0})
+    t0 = time.perf_counter()
+    rep = solver.ic_solve(sub, c, backend="oracle")
+    wall = time.perf_counter() - t0
+    px, ms, prev = 0, 0.0, 0.0
+    first_wall = rep.iters[0].wall_ms if rep.iters else 0.0
+    for i, it in enumerate(rep.iters):
+        if i == 0:
+            prev = it.wall_ms
+            continue  # iteration 1 carries the one-time build in the reference's wall_ms accounting
+        ms += it.wall_ms - prev
+        prev = it.wall_ms
+        px += it.num_active
+    if px == 0 and rep.iters:  # single-iteration fallback
+        px, ms = rep.iters[-1].num_active, first_wall
+    v = px / (ms / 1e3) if ms > 0 else 0.0
+    return {"value": v, "unit": "obs_px/s", "cores": 1, "kind": "port",
+            "sample": f"{npts} of {st.num_points} points (all frames), {len(rep.iters)} IC iterations, "
+                      f"{sub.num_observations} observations; oracle/ single-threaded fp64 restatement of "
+                      f"solver.cpp; {wall:.1f} s total"}
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_1704_06967_b200 import _capi, scenes, solver
+
+    dev = torch.device("cuda", rank % max(torch.cuda.device_count(), 1))
+    torch.cuda.set_device(dev)
+    sc_cfg = scenes.baseline_config(args.config, seed=scenes.baseline_config(args.config).seed + rank)
+    t0 = time.perf_counter()
+    scene = scenes.make_scene(sc_cfg, device=str(dev))
+    gen_s = time.perf_counter() - t0
+    st = scene.state
+    cfg = sc_cfg.solver_config(threshold_px=0.0, max_iters=10_000, max_bad_steps=8)
+    lib = _capi.backend("gpu")
+
+    # ---------------- device-resident timing of IC iterations ----------------
+    h = solver.Handle(st, "gpu")
+    t0 = time.perf_counter()
+    h.begin(True, cfg)           # upload done; IC build + initial pass (untimed)
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.ExternalStream(h.stream(), device=dev)
+    for _ in range(args.warmup):
+        _, done = h.iterate()
+        if done:
+            h.end(cfg)
+            h.begin(True, cfg)
+    h.set_profiling(True)
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    launches0 = lib.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    px_total, accepted = 0, 0
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t_wall = time.perf_counter()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            ev[k][0].record(stream)
+        stats, done = h.iterate()
+        with torch.cuda.stream(stream):
+            ev[k][1].record(stream)
+        px_total += stats.num_active
+        accepted += int(stats.accepted)
+        if done:  # diverged / max iters: restart untimed-equivalent (rare at these settings)
+            h.end(cfg)
+            h.begin(True, cfg)
+    torch.cuda.synchronize(dev)
+    wall_s = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    launches = lib.launch_count() - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    ktimes = h.kernel_times()
+    h.set_profiling(False)
+    n_px_iter = px_total / max(args.steps, 1)
+
+    # ---------------- FC iterations (same workload) ----------------
+    fc = None
+    if not args.no_fc and args.fc_steps > 0:
+        hf = solver.Handle(st, "gpu")
+        hf.begin(False, cfg)
+        stf = torch.cuda.ExternalStream(hf.stream(), device=dev)
+        evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.fc_steps)]
+        fpx = 0
+        hf.set_profiling(True)
+        for k in range(args.fc_steps):
+            with torch.cuda.stream(stf):
+                evf[k][0].record(stf)
+            s, done = hf.iterate()
+            with torch.cuda.stream(stf):
+                evf[k][1].record(stf)
+            fpx += s.num_active
+            if done:
+                break
+        torch.cuda.synchronize(dev)
+        fms = sum(a.elapsed_time(b) for a, b in evf[:k + 1])
+        fk = hf.kernel_times()
+        fc = {"value": fpx / (fms / 1e3), "unit": "obs_px/s", "ms_per_iter": fms / (k + 1), "steps": k + 1,
+              "kernel_ms": {n: round(v[1] / max(k + 1, 1), 4) for n, v in fk.items() if v[0]}}
+        hf.end(cfg)
+        hf.close()
+    h.end(cfg)
+    h.close()
+
+    # ---------------- end to end through the public API, host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        pin = {}
+        # pinned host copies of the inputs (the user's buffers)
+        for name in ("ref", "targets"):
+            a = getattr(st, name)
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            pin[name] = t
+        st_pin = st.copy()
+        st_pin.ref = pin["ref"].numpy()
+        st_pin.targets = pin["targets"].numpy()
+        c2 = sc_cfg.solver_config(threshold_px=0.0, max_iters=args.e2e_iters, max_bad_steps=8)
+        h2d = (st.ref.nbytes + st.targets.nbytes + st.anchors_px.nbytes + st.inv_depths.nbytes + st.R.nbytes
+               + st.t.nbytes + (0 if st.obs_ptr is None else st.obs_ptr.nbytes + st.obs_frame.nbytes))
+        d2h = st.R.nbytes + st.t.nbytes + st.inv_depths.nbytes
+        tot_px, tot_s = 0, 0.0
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            rep = solver.ic_solve(st_pin, c2)
+            tot_s += time.perf_counter() - t0
+            tot_px += sum(it.num_active for it in rep.iters)
+        e2e = {"value": tot_px / tot_s, "unit": "obs_px/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step":
+               int(d2h), "ms_per_step": 1e3 * tot_s / args.e2e_steps, "iters_per_step": args.e2e_iters,
+               "what": "one ic_solve through the C ABI from pinned host buffers: upload, IC build "
+                       "(J rows, H, Schur, Cholesky), LM iterations, download of final parameters"}
+
+    return dict(st=st, scene=scene, cfg=cfg, dev_ms=dev_ms, wall_s=wall_s, px_total=px_total, accepted=accepted,
+                n_px_iter=n_px_iter, ktimes=ktimes, clocks=clocks, launches=launches, fc=fc, e2e=e2e,
+                gen_s=gen_s, build_s=build_s)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from paper_1704_06967_b200 import scenes
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import torch
+
+        sc_cfg = scenes.baseline_config(args.config)
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        scene = scenes.make_scene(sc_cfg, device=dev)
+        st = scene.state
+        cfg = sc_cfg.solver_config()
+        npts = args.cpu_points or max(200, min(st.num_points, int(3.2e6 / max(st.num_observations / st.num_points
+                                                                                  * st.pattern.shape[0], 1))))
+        vals = []
+        for k in range(args.warmup + args.steps):
+            cb = cpu_baseline(st, cfg, npts, seed=k, iters=3)
+            if k >= args.warmup:
+                vals.append(cb)
+        v = statistics.median([c["value"] for c in vals])
+        cb = dict(vals[0])
+        cb["value"] = v
+        line = {"impl": "reference", "metric": "obs_px_per_s_per_LM_iteration", "value": v, "unit": "obs_px/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": {"workload": f"BASELINE {args.config}",
+                                                                  "frames": st.num_frames,
+                                                                  "points": st.num_points},
+                "cpu_baseline": cb, "e2e": {"value": v, "unit": "obs_px/s", "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("nccl")
+    r = run_ours(args, rank, world)
+    st = r["st"]
+    per_step_ms = r["dev_ms"] / args.steps
+    value_local = r["px_total"] / (r["dev_ms"] / 1e3)
+    value, ms = value_local, per_step_ms
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([r["px_total"], r["dev_ms"]], dtype=torch.float64, device="cuda")
+        tot = t.clone()
+        dist.all_reduce(tot[:1], op=dist.ReduceOp.SUM)
+        mx = t.clone()
+        dist.all_reduce(mx[1:], op=dist.ReduceOp.MAX)
+        value = float(tot[0]) / (float(mx[1]) / 1e3)
+        ms = float(mx[1]) / args.steps
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peaks()
+    kt = r["ktimes"]
+    cnt, kms = kt["obs_pass"]
+    obs_ms = kms / max(cnt, 1)
+    alg = obs_pass_bytes(st, r["n_px_iter"])
+    achieved = alg / (obs_ms / 1e3) / 1e9
+    bic = canonical_bic(st, r["n_px_iter"])
+    cpu = None
+    if not args.no_cpu_baseline:
+        npts = args.cpu_points or max(200, int(3.2e6 / (st.num_observations / st.num_points * st.pattern.shape[0])))
+        cpu = cpu_baseline(st, r["cfg"], min(npts, st.num_points))
+    line = {
+        "metric": "obs_px_per_s_per_LM_iteration",
+        "value": value,
+        "unit": "obs_px/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"BASELINE {args.config} (IC-proxy LM iteration)", "frames": st.num_frames,
+                   "points": st.num_points, "observations": st.num_observations,
+                   "pattern": int(st.pattern.shape[0]), "image": list(st.ref.shape[::-1]),
+                   "active_obs_px_per_iter": r["n_px_iter"], "accepted_steps": r["accepted"],
+                   "l2": "inputs larger than L2 (frozen J rows %.1f GB)" % (56 * st.num_observations * st.pattern.shape[0] / 1e9),
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": "k_obs<OBS_IC> fused residual/Huber/J^T W r pass",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(), "alg_bytes_per_launch": alg,
+                     "launch_ms": obs_ms, "share_of_step": obs_ms / per_step_ms,
+                     "canonical_B_IC_per_iter": bic, "canonical_effective_GBs": bic / (per_step_ms / 1e3) / 1e9},
+        "kernel_ms_per_iter": {n: round(v[1] / args.steps, 4) for n, v in kt.items() if v[0]},
+        "clocks": r["clocks"],
+        "gpu_launches": int(r["launches"]),
+        "e2e": r["e2e"],
+        "fc": r["fc"],
+        "cpu_baseline": cpu,
+        "setup_s": {"scene_gen": round(r["gen_s"], 2), "ic_build_and_first_pass": round(r["build_s"], 3)},
+    }
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

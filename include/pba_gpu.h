@@ -206,6 +206,8 @@ enum {
   PBA_K_COUNT = 6
 };
 int pba_gpu_kernel_times(pba_handle* h, int64_t* counts, double* total_ms);
+/* Process-wide number of kernel launches issued by this library so far. */
+int64_t pba_gpu_launch_count(void);
 /* Bytes of device memory held by the handle. */
 int64_t pba_gpu_device_bytes(const pba_handle* h);
 

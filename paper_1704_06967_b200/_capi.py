@@ -115,6 +115,7 @@ _GPU_ONLY = {
     "set_profiling": (C.c_int, [VP, C.c_int]),
     "kernel_times": (C.c_int, [VP, P(i64), P(f64)]),
     "device_bytes": (i64, [VP]),
+    "launch_count": (i64, []),
 }
 _ORACLE_ONLY = {
     "solve_normal_equations_dense": _COMMON["solve_normal_equations_schur"],

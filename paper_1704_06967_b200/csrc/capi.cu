@@ -187,6 +187,8 @@ int pba_gpu_set_profiling(pba_handle* h, int on) {
 int pba_gpu_kernel_times(pba_handle* h, int64_t* counts, double* total_ms) {
   return guarded(h, [&](Engine& e) { e.kernel_times(counts, total_ms); });
 }
+int64_t pba_gpu_launch_count(void) { return pba_b200::launch_count(); }
+
 int64_t pba_gpu_device_bytes(const pba_handle* h) { return (h && h->e) ? h->e->device_bytes() : 0; }
 
 }  // extern "C"

@@ -202,6 +202,7 @@ void Engine::apply_update(int mode, const double* dx, double* R, double* t, doub
   if (N_ > 0)
     k_depth_update<<<(N_ + 255) / 256, 256, 0, stream_>>>(N_, ic ? 1 : 0, d_state_.p, d0_.p, dx_n_.p, d_cand_.p,
                                                            flags_.p + 2);
+  if (N_ > 0) count_launches(1);
   const int bad = read_flag(2);
   download_poses(pose_cand_, R, t);
   download_depths_user(d_cand_, d);
@@ -227,7 +228,10 @@ double Engine::max_reproj_update(const double* R, const double* t, const double*
 // normalize_depth_gauge (solver.cpp:135-143) on the problem parameters
 void Engine::normalize_gauge() {
   const int nb = std::max(1, std::min(1024, (N_ + 255) / 256));
-  if (N_ > 0) k_block_sum<<<nb, 256, 0, stream_>>>(d_state_.p, N_, partial_mr_.p);
+  if (N_ > 0) {
+    k_block_sum<<<nb, 256, 0, stream_>>>(d_state_.p, N_, partial_mr_.p);
+    count_launches(1);
+  }
   std::vector<double> part(nb, 0.0);
   ck(cudaMemcpyAsync(part.data(), partial_mr_.p, nb * sizeof(double), cudaMemcpyDeviceToHost, stream_), "sum");
   ck(cudaStreamSynchronize(stream_), "sync");

@@ -17,6 +17,8 @@
 #include <cmath>
 #include <cstdio>
 
+#include <atomic>
+
 #include "kernels.hpp"
 
 namespace pba_b200 {
@@ -825,9 +827,16 @@ int next_pow2(int p) {
 
 // ================================ launchers =========================================
 
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
   if (a.ov.ntiles == 0) return;
   const int G = next_pow2(a.pat.P);
+  count_launches(1);
   switch (mode) {
     case OBS_ENERGY: launch_obs_mode<OBS_ENERGY>(a, G, s); break;
     case OBS_IC: launch_obs_mode<OBS_IC>(a, G, s); break;
@@ -840,6 +849,7 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
 void launch_pose_update(int ic, int F, const PoseD* cur, const PoseD* pose0, const double* xp, PoseD* cand,
                         cudaStream_t s) {
   k_pose_update<<<(F + 127) / 128, 128, 0, s>>>(ic, F, cur, pose0, xp, cand);
+  count_launches(1);
 }
 
 int backsub_blocks(int N) {
@@ -850,30 +860,44 @@ int point_blocks(int N) { return backsub_blocks(N); }
 
 void launch_backsub(const BacksubArgs& a, cudaStream_t s) {
   const int nb = backsub_blocks(a.ov.N);
-  if (nb > 0) k_backsub<<<nb, NT, 0, s>>>(a);
+  if (nb > 0) {
+    k_backsub<<<nb, NT, 0, s>>>(a);
+    count_launches(1);
+  }
 }
 
 void launch_point(const PointArgs& a, cudaStream_t s) {
   const int nb = point_blocks(a.ov.N);
-  if (nb > 0) k_point<<<nb, NT, 0, s>>>(a);
+  if (nb > 0) {
+    k_point<<<nb, NT, 0, s>>>(a);
+    count_launches(1);
+  }
 }
 
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s) {
-  if (ov.ntiles > 0) k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf);
+  if (ov.ntiles > 0) {
+    k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf);
+    count_launches(1);
+  }
 }
 
-void launch_finalize(const FinalizeArgs& a, cudaStream_t s) { k_finalize<<<a.ov.F + 1, NT, 0, s>>>(a); }
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
+  k_finalize<<<a.ov.F + 1, NT, 0, s>>>(a);
+  count_launches(1);
+}
 
 void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, double scale_d, double scale_t,
                    double* d_cur, PoseD* pose_cur, cudaStream_t s) {
   const int m = N > F ? N : F;
   k_commit<<<(m + 255) / 256, 256, 0, s>>>(N, F, d_cand, pose_cand, scale_d, scale_t, d_cur, pose_cur);
+  count_launches(1);
 }
 
 void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref, const double2* anchor, int dx0,
                        int dy0, const PoseD* pa, const double* da, const PoseD* pb, const double* db, double* partial,
                        int nblocks, cudaStream_t s) {
   k_max_reproj<<<nblocks, NT, 0, s>>>(ov, frames, ref, anchor, dx0, dy0, pa, da, pb, db, partial);
+  count_launches(1);
 }
 
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
@@ -885,17 +909,20 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
   const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
   if (pb > 0) k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, scale, acc);
   k_schur_final<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, scale, acc, S);
+  count_launches(pb > 0 ? 3 : 2);
 }
 
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {
   for (int j0 = 0; j0 < n; j0 += NB) {
     const int nb = std::min(NB, n - j0);
     k_chol_diag<<<1, dim3(NB, NB), 0, s>>>(S, n, j0, nb, fail);
+    count_launches(1);
     const int rest = n - j0 - nb;
     if (rest > 0) {
       k_chol_panel<<<(rest + 255) / 256, 256, 0, s>>>(S, n, j0, nb);
       const int m = (rest + NB - 1) / NB;
       k_chol_update<<<m * (m + 1) / 2, 256, 0, s>>>(S, n, j0, nb);
+      count_launches(2);
     }
   }
 }
@@ -904,6 +931,7 @@ void launch_trisolve(const double* L, int n, const double* b, double* x, int* no
   const size_t smem = static_cast<size_t>(n) * sizeof(double);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_trisolve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_trisolve<<<1, 1024, smem, s>>>(L, n, b, x, nonfinite);
+  count_launches(1);
 }
 
 }  // namespace pba_b200

@@ -146,4 +146,8 @@ void launch_cholesky(double* S, int n, int* fail, cudaStream_t s);
 void launch_trisolve(const double* L, int n, const double* b, double* x, int* nonfinite,
                      cudaStream_t s);
 
+// Process-wide count of kernel launches issued by this library.
+void count_launches(int64_t n);
+int64_t launch_count();
+
 }  // namespace pba_b200

@@ -61,6 +61,7 @@ class SceneConfig:
     depth_noise: float = 0.05
     subpixel: bool = False
     vis_deg: Optional[float] = None       # visibility half-angle (None = every frame)
+    vis_mode: str = "normal3d"            # "normal3d": angle(normal, view dir); "azimuth": |alpha_f - azimuth(normal)|
     seed: int = 1
     huber_delta: float = 9.0
     iters: int = 10
@@ -80,13 +81,13 @@ def baseline_config(name: str, **over) -> SceneConfig:
         c = SceneConfig("C2", 640, 480, 500.0, 6, 2000, DSO8, arc_deg=24.0, seed=2, iters=5, rot_deg=1.0,
                         trans_sigma=0.01)
     elif name == "C3":
-        c = SceneConfig("C3", 1280, 720, 1000.0, 50, 100_000, square_pattern(1), arc_deg=150.0, rot_deg=3.0,
+        c = SceneConfig("C3", 1280, 720, 1000.0, 50, 100_000, square_pattern(1), arc_deg=110.0, rot_deg=3.0,
                         trans_sigma=0.03, vis_deg=70.0, seed=3, iters=20)
     elif name == "C4":
         c = SceneConfig("C4", 1280, 720, 1000.0, 200, 1_000_000, DSO8, arc_deg=150.0, rot_deg=2.0,
-                        trans_sigma=0.02, vis_deg=15.0, subpixel=True, seed=4, iters=10)
+                        trans_sigma=0.02, vis_deg=15.0, vis_mode="azimuth", subpixel=True, seed=4, iters=10)
     elif name == "C5":
-        c = SceneConfig("C5", 1920, 1080, 1400.0, 100, 1_000_000, DSO8, arc_deg=120.0, vis_deg=20.0,
+        c = SceneConfig("C5", 1920, 1080, 1400.0, 100, 1_000_000, DSO8, arc_deg=120.0, vis_deg=20.0, vis_mode="azimuth",
                         subpixel=True, seed=5, iters=1)
     elif name == "tiny":
         c = SceneConfig("tiny", 160, 120, 130.0, 3, 40, DSO8, arc_deg=12.0, seed=11, rot_deg=0.3,
@@ -253,11 +254,19 @@ def make_scene(cfg: SceneConfig, device: Optional[str] = None) -> Scene:
         nrm = Xs - center
         nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
         vis = np.zeros((N, F), dtype=bool)
+        azim = np.degrees(np.arctan2(nrm[:, 0], -nrm[:, 2]))
         for f in range(F):
             Cf = -(R_true[f].T @ (t_true[f] / mean))
-            v = Cf[None, :] - Xs
-            v /= np.linalg.norm(v, axis=-1, keepdims=True)
-            ok = (nrm * v).sum(-1) > cosv
+            if cfg.vis_mode == "azimuth":
+                alpha_f = cfg.arc_deg * ((f + 0.5) / F - 0.5)
+                # camera azimuth about the sphere centre, same sign convention as the normal
+                cam_az = np.degrees(np.arctan2(Cf[0] - center[0], -(Cf[2] - center[2])))
+                ok = np.abs(cam_az - azim) <= cfg.vis_deg
+                del alpha_f
+            else:
+                v = Cf[None, :] - Xs
+                v /= np.linalg.norm(v, axis=-1, keepdims=True)
+                ok = (nrm * v).sum(-1) > cosv
             Xc = Xs @ R_true[f].T + t_true[f] / mean
             with np.errstate(divide="ignore", invalid="ignore"):
                 u = fx * Xc[:, 0] / Xc[:, 2] + K[2]

@@ -207,6 +207,13 @@ Engine::Engine(const pba_problem* p) {
   std::vector<double2> anc(N_);
   for (int i = 0; i < N_; ++i) anc[i] = make_double2(p->anchors_px[2 * perm_[i]], p->anchors_px[2 * perm_[i] + 1]);
   up(anchor_, anc);
+  {  // frame-major per-observation anchors: k_obs reads them coalesced (no dependent gather)
+    std::vector<double2> afm(NO_);
+    for (int64_t q = 0; q < NO_; ++q) afm[q] = anc[fm_point[q]];
+    up(anchor_fm_, afm);
+    ck(cudaStreamSynchronize(stream_), "sync upload");
+  }
+  dd_fm_.alloc(std::max<int64_t>(NO_, 1));
   // template feasibility (solver.cpp:40-45): every template pixel inside [1, W-3] x [1, H-3]
   template_ok_ = true;
   for (int n = 0; n < N_ && template_ok_; ++n)
@@ -410,7 +417,8 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.ref = ref_;
   a.frames = frames_.p;
   a.pat = pat_;
-  a.anchor = anchor_.p;
+  a.anchor_fm = anchor_fm_.p;
+  a.dd_fm = dd_fm_.p;
   a.gamma = gamma;
   a.partial = partial_.p;
   a.rec = rec_.p;
@@ -445,8 +453,8 @@ void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, d
   check_template();
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose_state_.p;
-  a.d_eval = d_state_.p;
   a.active_out = scratch_bits_.p;
+  launch_scatter_depth(ov_, d_state_.p, nullptr, dd_fm_.p, stream_);
   if (mask) {
     std::vector<uint32_t> bits(NO_, 0);
     for (int64_t ou = 0; ou < NO_; ++ou) {
@@ -509,9 +517,9 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   // eval_residuals + assemble_gradient (solver.cpp:436-468) + solve_step rhs (:407-416)
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose;
-  a.d_eval = d;
   a.pose_old = pose_old;
-  a.d_old = d_old;
+  // after k_backsub the per-observation depths {d_cand, d_cur} are already in dd_fm_
+  if (d_old == nullptr) launch_scatter_depth(ov_, d, nullptr, dd_fm_.p, stream_);
   a.mask_in = mask_in;
   a.active_out = active_out;
   a.J = J_.p;
@@ -593,9 +601,8 @@ void Engine::ic_build(const pba_config* cfg) {
 
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose0_.p;
-  a.d_eval = d0_.p;
   a.pose0 = pose0_.p;
-  a.d0 = d0_.p;
+  launch_scatter_depth(ov_, d0_.p, nullptr, dd_fm_.p, stream_);
   a.active_out = mask_[0].p;
   a.Jw = J_.p;
   a.B_out = Bic_.p;

@@ -106,7 +106,7 @@ class Engine {
 
   DBuf<float> images_;
   DBuf<FrameD> frames_;
-  DBuf<double2> anchor_;
+  DBuf<double2> anchor_, anchor_fm_, dd_fm_;
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
   DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
   DBuf<PoseD> pose_state_, pose_cur_, pose_cand_, pose0_;

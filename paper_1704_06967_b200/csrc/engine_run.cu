@@ -55,7 +55,7 @@ void need_built(bool built) {
 
 void Engine::backsub(bool ic, const double* B, const double* D, const double* g_n, double lambda,
                      const double* d_cur, double* d_cand, double* dx_out) {
-  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p};
+  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p, dd_fm_.p};
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_backsub(a, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -121,7 +121,7 @@ void Engine::download_block_hessian(const DBuf<double>& H, const DBuf<double>& D
 void Engine::ic_refresh() {
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose_cur_.p;
-  a.d_eval = d_cur_.p;
+  launch_scatter_depth(ov_, d_cur_.p, nullptr, dd_fm_.p, stream_);
   a.mask_in = mask_[ic_.mcur].p;
   a.active_out = scratch_bits_.p;
   a.J = J_.p;
@@ -152,9 +152,8 @@ void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, 
                      const PoseD* pose_old, const double* d_old) {
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose;
-  a.d_eval = d;
   a.pose_old = pose_old;
-  a.d_old = d_old;
+  if (d_old == nullptr) launch_scatter_depth(ov_, d, nullptr, dd_fm_.p, stream_);
   a.mask_in = nullptr;
   a.active_out = scratch_bits_.p;
   a.B_out = B_[buf].p;

@@ -33,23 +33,32 @@ __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 // k_obs: one block per frame-major tile; G lanes per observation (G = next pow2 >= P)
 // ---------------------------------------------------------------------------------
 template <int MODE, int G>
-__global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
+__global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3 : 2) k_obs(const ObsArgs a) {
   constexpr int OPS = NT / G;  // observations per block step
   constexpr bool kHasH = (MODE == OBS_FC || MODE == OBS_BUILD || MODE == OBS_REFRESH);
   constexpr bool kHasG = (MODE == OBS_IC || MODE == OBS_FC);
   constexpr bool kHasRec = (MODE != OBS_ENERGY);
+  constexpr bool kLoadJ = (MODE == OBS_IC || MODE == OBS_REFRESH);
   const int t = blockIdx.x;
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t];
   const int64_t q1 = a.ov.tile_q1[t];
-  const FrameD fr = a.frames[f];
-  const FrameD rf = a.ref;
-  const PoseD pe = a.pose_eval[f];
   const bool want_upd = a.pose_old != nullptr;
-  PoseD po;
-  if (want_upd) po = a.pose_old[f];
-  PoseD p0;
-  if (MODE == OBS_BUILD) p0 = a.pose0[f];
+  // frame-uniform data in shared memory (one frame per tile): keeps registers for the pixel math
+  __shared__ PoseD s_pe, s_po, s_p0;
+  __shared__ FrameD s_fr;
+  if (threadIdx.x == 0) {
+    s_fr = a.frames[f];
+    s_pe = a.pose_eval[f];
+    if (want_upd) s_po = a.pose_old[f];
+    if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
+  }
+  __syncthreads();
+  const FrameD& fr = s_fr;
+  const PoseD& pe = s_pe;
+  const PoseD& po = s_po;
+  const PoseD& p0 = s_p0;
+  const FrameD& rf = a.ref;
   const int P = a.pat.P;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -68,20 +77,34 @@ __global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
   for (int64_t base = q0; base < q1; base += OPS) {
     const int64_t q = base + j;
     const bool live = q < q1;
-    bool act = false;     // residual active at the evaluation parameters
-    bool keep = false;    // final mask bit (BUILD)
+    // ---- level-1 loads: all coalesced and independent of each other ----
+    double2 an = make_double2(0.0, 0.0), dd = make_double2(1.0, 1.0);
+    uint32_t mbits = 0u;
+    double J[kLoadJ ? 7 : 1];
+    if (live) {
+      an = __ldg(&a.anchor_fm[q]);
+      dd = __ldg(&a.dd_fm[q]);
+      mbits = (MODE == OBS_BUILD || a.mask_in == nullptr) ? 0xffffffffu : __ldg(&a.mask_in[q]);
+      if constexpr (kLoadJ) {
+        if (klive) {
+          const int64_t px = q * P + k;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) J[c] = ldcs(a.J + c * NPX + px);
+        }
+      }
+    }
+    const double dv = dd.x;  // depth at the evaluation parameters
+    bool act = false;        // residual active at the evaluation parameters
+    bool keep = false;       // final mask bit (BUILD)
     double gnc = 0.0, dc = 0.0;
     double b6[6] = {0, 0, 0, 0, 0, 0};
     if (live) {
-      const int n = a.ov.fm_point[q];
-      const double2 an = __ldg(&a.anchor[n]);
-      const double dv = __ldg(&a.d_eval[n]);
       // anchor reprojection update (solver.cpp:105-131): anchor = pattern offset 0
       if (want_upd && k == 0) {
         const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
         const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
         double xo, yo, xn2, yn2, t0_, t1_, t2_;
-        const bool oka = warp_point(po, xa, ya, __ldg(&a.d_old[n]), xo, yo, t0_, t1_, t2_);
+        const bool oka = warp_point(po, xa, ya, dd.y, xo, yo, t0_, t1_, t2_);
         const bool okb = warp_point(pe, xa, ya, dv, xn2, yn2, t0_, t1_, t2_);
         if (!oka || !okb) {
           maxupd = INFINITY;
@@ -91,7 +114,6 @@ __global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
           maxupd = fmax(maxupd, sqrt(du * du + dvv * dvv));
         }
       }
-      const uint32_t mbits = (MODE == OBS_BUILD || a.mask_in == nullptr) ? 0xffffffffu : a.mask_in[q];
       if (klive && ((mbits >> k) & 1u)) {
         // template pixel (solver.cpp:42-49)
         const double pu = an.x + static_cast<double>(a.pat.dx[k]);
@@ -148,36 +170,30 @@ __global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
               }
               dc = w * row[6] * row[6];
               gnc = row[6] * wr;
-            } else if constexpr (MODE == OBS_IC || MODE == OBS_REFRESH) {
-              const int64_t px = q * P + k;
-              double J[7];
+            } else if constexpr (MODE == OBS_IC) {
+              const double wr = huber_weight(r, gam) * r;  // fresh weights (solver.cpp:461)
 #pragma unroll
-              for (int c = 0; c < 7; ++c) J[c] = ldcs(a.J + c * NPX + px);
-              if constexpr (MODE == OBS_IC) {
-                const double wr = huber_weight(r, gam) * r;  // fresh weights (solver.cpp:461)
+              for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
+              gnc = J[6] * wr;
+            } else if constexpr (MODE == OBS_REFRESH) {
+              const double w = huber_weight(r, gam);
+              int h = 0;
 #pragma unroll
-                for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
-                gnc = J[6] * wr;
-              } else {
-                const double w = huber_weight(r, gam);
-                int h = 0;
+              for (int i2 = 0; i2 < 6; ++i2) {
+                const double wi = w * J[i2];
 #pragma unroll
-                for (int i2 = 0; i2 < 6; ++i2) {
-                  const double wi = w * J[i2];
-#pragma unroll
-                  for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * J[j2];
-                  b6[i2] = wi * J[6];
-                }
-                dc = w * J[6] * J[6];
+                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * J[j2];
+                b6[i2] = wi * J[6];
               }
+              dc = w * J[6] * J[6];
             }
           }
         }
         if constexpr (MODE == OBS_BUILD) {
-          // IcSolver::build per-pixel rows (solver.cpp:306-356)
+          // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
           const int64_t px = q * P + k;
           double row[7] = {0, 0, 0, 0, 0, 0, 0};
-          const double d0 = __ldg(&a.d0[n]);
+          const double d0 = dv;
           // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
           const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
           const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
@@ -240,8 +256,8 @@ __global__ void __launch_bounds__(NT) k_obs(const ObsArgs a) {
     if (live && k == 0) {
       const unsigned bits = (G == 32) ? bal : ((bal >> ((lane / G) * G)) & ((1u << G) - 1u));
       a.active_out[q] = bits;
-      if (kHasRec) a.rec[q] = make_double2(gnc, dc);
-      if (kHasH) {
+      if constexpr (kHasRec) a.rec[q] = make_double2(gnc, dc);
+      if constexpr (kHasH) {
 #pragma unroll
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
       }
@@ -357,6 +373,7 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
       acc += dot;
     }
     acc = warp_sum(acc);
+    double dn_b = 0.0;
     if (lane == 0) {
       const double D = a.D[n] + a.lambda;
       const double dx = (-a.g_n[n] - acc) / D;
@@ -373,6 +390,12 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
       sum_d += dn;
       if (dn <= 0.0) ninv += 1.0;
       if (!isfinite(dx)) nnf += 1.0;
+      dn_b = dn;
+    }
+    if (a.dd_fm) {  // per-observation {candidate depth, current depth} for k_obs
+      dn_b = __shfl_sync(0xffffffffu, dn_b, 0);
+      const double dc = a.d_cur[n];
+      for (int64_t o = o0 + lane; o < o1; o += 32) a.dd_fm[a.ov.pm2fm[o]] = make_double2(dn_b, dc);
     }
   }
   if (lane == 0) {
@@ -386,6 +409,18 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
     for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
     a.partial[blockIdx.x * 4 + threadIdx.x] = v;
   }
+}
+
+// ---------------------------------------------------------------------------------
+// k_scatter_depth: per-observation {d_eval, d_old} in frame-major order (no update)
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_scatter_depth(const ObsView ov, const double* __restrict__ d_eval,
+                                                      const double* __restrict__ d_old, double2* __restrict__ dd_fm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = blockIdx.x * (NT / 32) + warp;
+  if (n >= ov.N) return;
+  const double2 v = make_double2(d_eval[n], d_old ? d_old[n] : d_eval[n]);
+  for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) dd_fm[ov.pm2fm[o]] = v;
 }
 
 // ---------------------------------------------------------------------------------
@@ -870,6 +905,15 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
   const int nb = point_blocks(a.ov.N);
   if (nb > 0) {
     k_point<<<nb, NT, 0, s>>>(a);
+    count_launches(1);
+  }
+}
+
+void launch_scatter_depth(const ObsView& ov, const double* d_eval, const double* d_old, double2* dd_fm,
+                          cudaStream_t s) {
+  const int nb = (ov.N + (NT / 32) - 1) / (NT / 32);
+  if (nb > 0) {
+    k_scatter_depth<<<nb, NT, 0, s>>>(ov, d_eval, d_old, dd_fm);
     count_launches(1);
   }
 }

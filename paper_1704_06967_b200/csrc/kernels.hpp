@@ -31,14 +31,12 @@ struct ObsArgs {
   FrameD ref;
   const FrameD* frames;        // F
   PatternD pat;
-  const double2* anchor;       // N (internal order)
+  const double2* anchor_fm;    // NO: anchor pixel of obs q (frame-major copy, static)
+  const double2* dd_fm;        // NO: {depth at evaluation, depth at old params} of obs q
   double gamma;
   const PoseD* pose_eval;      // F
-  const double* d_eval;        // N
   const PoseD* pose_old;       // F or null (max reprojection update)
-  const double* d_old;         // N or null
   const PoseD* pose0;          // F (IC build)
-  const double* d0;            // N (IC build)
   const uint32_t* mask_in;     // NO bit words or null (= all pixels)
   uint32_t* active_out;        // NO bit words
   double* r_out;               // NO*P or null
@@ -71,6 +69,7 @@ struct BacksubArgs {
   double* d_cand;         // N
   double* dx_out;         // N or null
   double* partial;        // nblocks * 4
+  double2* dd_fm;         // NO or null: per-observation {d_cand, d_cur} for the next k_obs
 };
 int backsub_blocks(int N);
 void launch_backsub(const BacksubArgs& a, cudaStream_t s);
@@ -89,6 +88,10 @@ struct PointArgs {
 };
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);
+
+// Per-observation depths {d_eval, d_old (or d_eval)} in frame-major order.
+void launch_scatter_depth(const ObsView& ov, const double* d_eval, const double* d_old, double2* dd_fm,
+                          cudaStream_t s);
 
 // Frame-major  c_f = sum_n B_nf s_n  per tile.
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf,

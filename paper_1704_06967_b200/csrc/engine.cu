@@ -257,6 +257,10 @@ Engine::Engine(const pba_problem* p) {
   S_.alloc(static_cast<size_t>(36) * nF * nF);
   schur_acc_.alloc(static_cast<size_t>(36) * nF * nF);
   schur_scale_.alloc(6 * nF);
+  Linv_.alloc(static_cast<size_t>(36) * nF * nF);
+  LinvT_.alloc(static_cast<size_t>(36) * nF * nF);
+  Dinv_.alloc(static_cast<size_t>((6 * nF + 31) / 32) * 32 * 32);
+  ytmp_.alloc(6 * nF);
   status_.alloc(1);
   flags_.alloc(4);
   ck(cudaMallocHost(&status_h_, sizeof(Status)), "pinned");
@@ -415,6 +419,8 @@ ObsArgs Engine::obs_args(double gamma) const {
   ObsArgs a{};
   a.ov = ov_;
   a.ref = ref_;
+  a.ref_ifx = 1.0 / ref_.fx;
+  a.ref_ify = 1.0 / ref_.fy;
   a.frames = frames_.p;
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
@@ -553,7 +559,11 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   e = ev_begin(PBA_K_CHOLESKY);
   launch_cholesky(S_.p, n, flags_.p, stream_);
   ev_end(PBA_K_CHOLESKY, e);
-  return read_flag(0) == 0;
+  if (read_flag(0) != 0) return false;
+  e = ev_begin(PBA_K_CHOLESKY);
+  launch_tri_inverse(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, stream_);
+  ev_end(PBA_K_CHOLESKY, e);
+  return true;
 }
 
 // IcSolver::factorize (solver.cpp:370-402)
@@ -571,7 +581,7 @@ void Engine::ic_factorize_loop(double lambda) {
 
 void Engine::solve_xp(const double* rhs) {
   const auto e = ev_begin(PBA_K_TRISOLVE);
-  if (F_ > 0) launch_trisolve(S_.p, 6 * F_, rhs, xp_.p, flags_.p + 1, stream_);
+  if (F_ > 0) launch_trisolve(Linv_.p, LinvT_.p, 6 * F_, rhs, ytmp_.p, xp_.p, flags_.p + 1, stream_);
   ev_end(PBA_K_TRISOLVE, e);
 }
 

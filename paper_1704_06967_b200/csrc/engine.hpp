@@ -123,7 +123,7 @@ class Engine {
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
-  DBuf<double> S_, schur_scale_;
+  DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_;
   DBuf<unsigned long long> schur_acc_;
   DBuf<Status> status_;
   DBuf<int> flags_;

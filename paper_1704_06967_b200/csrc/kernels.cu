@@ -12,7 +12,7 @@
 //   k_finalize deterministic fixed-order reduction of tile partials -> status.
 //   k_schur    reduced camera system.                                   solver.cpp:170-189,375-392
 //   k_chol_*   blocked right-looking fp64 Cholesky (stands in for Eigen::LDLT, solver.cpp:190,393).
-//   k_trisolve forward/backward substitution with the cached factor.    solver.cpp:417
+//   k_tri_*    explicit L^-1 per factorization + two GEMVs per solve.   solver.cpp:417
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
     if (live) {
       // anchor reprojection update (solver.cpp:105-131): anchor = pattern offset 0
       if (want_upd && k == 0) {
-        const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
-        const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
+        const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
+        const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
         double xo, yo, xn2, yn2, t0_, t1_, t2_;
         const bool oka = warp_point(po, xa, ya, dd.y, xo, yo, t0_, t1_, t2_);
         const bool okb = warp_point(pe, xa, ya, dv, xn2, yn2, t0_, t1_, t2_);
@@ -118,8 +118,8 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
         // template pixel (solver.cpp:42-49)
         const double pu = an.x + static_cast<double>(a.pat.dx[k]);
         const double pv = an.y + static_cast<double>(a.pat.dy[k]);
-        const double x = (pu - rf.cx) / rf.fx;
-        const double y = (pv - rf.cy) / rf.fy;
+        const double x = (pu - rf.cx) * a.ref_ifx;
+        const double y = (pv - rf.cy) * a.ref_ify;
         const double tval = bilinear(rf.img, rf.W, pu, pv);
         double xn, yn, vx, vy, vz;
         double r = 0.0;
@@ -195,8 +195,8 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
           double row[7] = {0, 0, 0, 0, 0, 0, 0};
           const double d0 = dv;
           // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
-          const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) / rf.fx;
-          const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) / rf.fy;
+          const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
+          const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
           const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + d0 * p0.t[2];
           const bool obs_ok = (d0 > 0.0) && !(vza < kDegenerateDepthEps);
           if (act && obs_ok) {
@@ -794,62 +794,125 @@ __global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ A, int
 }
 
 // ---------------------------------------------------------------------------------
-// Triangular solves, one block of 1024 threads.
+// Triangular solves through an explicit inverse of the Cholesky factor.
+// The factor is frozen between factorizations (IC: once per solve + once per rejection),
+// so L^-1 is formed once per factorization (blocked triangular inversion, one CTA per
+// block column) and every solve is two row-parallel GEMVs spread over all SMs instead
+// of a latency-bound single-CTA substitution (solver.cpp:417 reduced_ldlt_.solve).
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_trisolve(const double* __restrict__ L, int n, const double* __restrict__ b,
-                                                   double* __restrict__ x, int* nonfinite) {
-  extern __shared__ double y[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < n; i += blockDim.x) y[i] = b[i];
+__global__ void __launch_bounds__(256) k_tri_diag_inv(const double* __restrict__ L, int n, double* __restrict__ Dinv) {
+  // inverse of the lower-triangular diagonal block bi (32x32), forward substitution per column
+  const int bi = blockIdx.x;
+  const int j0 = bi * NB, nb = min(NB, n - j0);
+  __shared__ double l[NB][NB + 1];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    l[r][c] = (r < nb && c <= r) ? L[static_cast<int64_t>(j0 + r) * n + j0 + c] : (r == c ? 1.0 : 0.0);
+  }
   __syncthreads();
-  // forward: L y = b
-  for (int jb = 0; jb < n; jb += NB) {
-    const int nb = min(NB, n - jb);
-    if (warp == 0) {
-      double yr = lane < nb ? y[jb + lane] : 0.0;
-      for (int p = 0; p < nb; ++p) {
-        if (lane == p) yr = yr / L[static_cast<int64_t>(jb + p) * n + jb + p];
-        const double yp = __shfl_sync(0xffffffffu, yr, p);
-        if (lane > p && lane < nb) yr -= L[static_cast<int64_t>(jb + lane) * n + jb + p] * yp;
+  const int c = threadIdx.x;
+  if (c < NB) {
+    double x[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
+      for (int p = 0; p < r; ++p) v -= l[r][p] * x[p];
+      x[r] = (r < c) ? 0.0 : v / l[r][r];
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) Dinv[(static_cast<int64_t>(bi) * NB + r) * NB + c] = x[r];
+  }
+}
+
+// Block column bj of L^-1:  X_jj = Dinv_j;  X_ij = -Dinv_i * sum_{k=j}^{i-1} L_ik X_kj.
+// Writes X (row-major lower) and X^T (row-major upper).
+__global__ void __launch_bounds__(256) k_tri_inv_col(const double* __restrict__ L, int n, const double* __restrict__ Dinv,
+                                                     double* __restrict__ X, double* __restrict__ XT) {
+  const int bj = blockIdx.x;
+  const int nblk = (n + NB - 1) / NB;
+  const int j0 = bj * NB;
+  __shared__ double A[NB][NB + 1], Bm[NB][NB + 1], T[NB][NB + 1];
+  const int tid = threadIdx.x;
+  auto store = [&](int bi, double (*blk)[NB + 1]) {
+    for (int e = tid; e < NB * NB; e += blockDim.x) {
+      const int r = e / NB, c = e % NB;
+      const int gr = bi * NB + r, gc = j0 + c;
+      if (gr < n && gc < n) {
+        X[static_cast<int64_t>(gr) * n + gc] = blk[r][c];
+        XT[static_cast<int64_t>(gc) * n + gr] = blk[r][c];
       }
-      if (lane < nb) y[jb + lane] = yr;
     }
-    __syncthreads();
-    for (int i = jb + nb + tid; i < n; i += blockDim.x) {
-      const double* row = L + static_cast<int64_t>(i) * n + jb;
-      double s = 0.0;
-      for (int p = 0; p < nb; ++p) s += row[p] * y[jb + p];
-      y[i] -= s;
-    }
-    __syncthreads();
+  };
+  // diagonal block
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e / NB, c = e % NB;
+    T[r][c] = Dinv[(static_cast<int64_t>(bj) * NB + r) * NB + c];
   }
-  // backward: L^T x = y
-  const int last = ((n - 1) / NB) * NB;
-  for (int jb = last; jb >= 0; jb -= NB) {
-    const int nb = min(NB, n - jb);
-    if (warp == 0) {
-      double xr = lane < nb ? y[jb + lane] : 0.0;
-      for (int p = nb - 1; p >= 0; --p) {
-        if (lane == p) xr = xr / L[static_cast<int64_t>(jb + p) * n + jb + p];
-        const double xp = __shfl_sync(0xffffffffu, xr, p);
-        if (lane < p) xr -= L[static_cast<int64_t>(jb + p) * n + jb + lane] * xp;
+  __syncthreads();
+  store(bj, T);
+  for (int bi = bj + 1; bi < nblk; ++bi) {
+    // T = sum_k L_ik X_kj  (4 outputs per thread)
+    double acc[4] = {0, 0, 0, 0};
+    for (int bk = bj; bk < bi; ++bk) {
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += blockDim.x) {
+        const int r = e / NB, c = e % NB;
+        const int gr = bi * NB + r, gk = bk * NB + c;
+        A[r][c] = (gr < n && gk < n) ? L[static_cast<int64_t>(gr) * n + gk] : 0.0;
+        const int kr = bk * NB + r, jc = j0 + c;
+        Bm[r][c] = (kr < n && jc < n) ? X[static_cast<int64_t>(kr) * n + jc] : 0.0;
       }
-      if (lane < nb) y[jb + lane] = xr;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = tid + q * 256, r = e / NB, c = e % NB;
+        double s2 = 0.0;
+#pragma unroll 8
+        for (int p = 0; p < NB; ++p) s2 += A[r][p] * Bm[p][c];
+        acc[q] += s2;
+      }
     }
     __syncthreads();
-    for (int i = tid; i < jb; i += blockDim.x) {
-      double s = 0.0;
-      for (int p = 0; p < nb; ++p) s += L[static_cast<int64_t>(jb + p) * n + i] * y[jb + p];
-      y[i] -= s;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;
+      Bm[e / NB][e % NB] = acc[q];
+    }
+    for (int e = tid; e < NB * NB; e += blockDim.x) {
+      const int r = e / NB, c = e % NB;
+      A[r][c] = Dinv[(static_cast<int64_t>(bi) * NB + r) * NB + c];
     }
     __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256, r = e / NB, c = e % NB;
+      double s2 = 0.0;
+#pragma unroll 8
+      for (int p = 0; p < NB; ++p) s2 += A[r][p] * Bm[p][c];
+      T[r][c] = -s2;
+    }
+    __syncthreads();
+    store(bi, T);
+    __threadfence_block();
   }
-  int bad = 0;
-  for (int i = tid; i < n; i += blockDim.x) {
-    x[i] = y[i];
-    if (!isfinite(y[i])) bad = 1;
+}
+
+// y = M b for a triangular row-major M (lower: columns <= row; upper: columns >= row).
+__global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, int n, int lower,
+                                                  const double* __restrict__ b, double* __restrict__ y,
+                                                  int* __restrict__ nonfinite) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const int c0 = lower ? 0 : r, c1 = lower ? r + 1 : n;
+  const double* row = M + static_cast<int64_t>(r) * n;
+  double s2 = 0.0;
+  for (int c = c0 + lane; c < c1; c += 32) s2 += row[c] * b[c];
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    y[r] = s2;
+    if (nonfinite && !isfinite(s2)) atomicOr(nonfinite, 1);
   }
-  if (bad) atomicOr(nonfinite, 1);
 }
 
 int next_pow2(int p) {
@@ -971,11 +1034,21 @@ void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {
   }
 }
 
-void launch_trisolve(const double* L, int n, const double* b, double* x, int* nonfinite, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(n) * sizeof(double);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_trisolve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_trisolve<<<1, 1024, smem, s>>>(L, n, b, x, nonfinite);
-  count_launches(1);
+void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double* XT, cudaStream_t s) {
+  const int nblk = (n + NB - 1) / NB;
+  if (nblk == 0) return;
+  k_tri_diag_inv<<<nblk, 256, 0, s>>>(L, n, Dinv);
+  k_tri_inv_col<<<nblk, 256, 0, s>>>(L, n, Dinv, X, XT);
+  count_launches(2);
+}
+
+void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x, int* nonfinite,
+                     cudaStream_t s) {
+  const int nb = (n + 7) / 8;
+  if (nb == 0) return;
+  k_tri_gemv<<<nb, 256, 0, s>>>(X, n, 1, b, y, nullptr);    // y = L^-1 b
+  k_tri_gemv<<<nb, 256, 0, s>>>(XT, n, 0, y, x, nonfinite);  // x = L^-T y
+  count_launches(2);
 }
 
 }  // namespace pba_b200

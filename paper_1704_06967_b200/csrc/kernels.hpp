@@ -29,6 +29,7 @@ constexpr int PT_STRIDE = 32;
 struct ObsArgs {
   ObsView ov;
   FrameD ref;
+  double ref_ifx, ref_ify;     // 1 / ref.fx, 1 / ref.fy (template normalization)
   const FrameD* frames;        // F
   PatternD pat;
   const double2* anchor_fm;    // NO: anchor pixel of obs q (frame-major copy, static)
@@ -145,9 +146,14 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
 // non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s);
 
-// x = L^-T L^-1 b.  *nonfinite set when x has a non-finite entry.
-void launch_trisolve(const double* L, int n, const double* b, double* x, int* nonfinite,
-                     cudaStream_t s);
+// X = L^-1 (row-major lower) and XT = X^T, from the Cholesky factor in L (lower).
+// Dinv: ceil(n/32) * 32 * 32 scratch.
+void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double* XT, cudaStream_t s);
+
+// x = L^-T L^-1 b = XT (X b) with the explicit inverse; y: n scratch.  *nonfinite set
+// when x has a non-finite entry.
+void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x,
+                     int* nonfinite, cudaStream_t s);
 
 // Process-wide count of kernel launches issued by this library.
 void count_launches(int64_t n);

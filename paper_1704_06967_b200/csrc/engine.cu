@@ -180,7 +180,9 @@ Engine::Engine(const pba_problem* p) {
   up(pm_frame_, pm_frame);
   up(pm2fm_, pm2fm);
   up(fm_ptr_, fm_ptr);
+  fm_point.resize(NO_ + 8, 0);  // padding: 16-byte aligned TMA windows may read 3 past the end
   up(fm_point_, fm_point);
+  fm_point.resize(NO_);
   up(tile_frame_, tile_frame);
   up(tile_q0_, tq0);
   up(tile_q1_, tq1);
@@ -213,7 +215,7 @@ Engine::Engine(const pba_problem* p) {
     up(anchor_fm_, afm);
     ck(cudaStreamSynchronize(stream_), "sync upload");
   }
-  dd_fm_.alloc(std::max<int64_t>(NO_, 1));
+
   // template feasibility (solver.cpp:40-45): every template pixel inside [1, W-3] x [1, H-3]
   template_ok_ = true;
   for (int n = 0; n < N_ && template_ok_; ++n)
@@ -236,9 +238,9 @@ Engine::Engine(const pba_problem* p) {
   d_cur_.alloc(nN);
   d_cand_.alloc(nN);
   d0_.alloc(nN);
-  mask_[0].alloc(nO);
-  mask_[1].alloc(nO);
-  scratch_bits_.alloc(nO);
+  mask_[0].alloc(nO + 8);
+  mask_[1].alloc(nO + 8);
+  scratch_bits_.alloc(nO + 8);
   rec_.alloc(nO);
   s_n_.alloc(nN);
   dx_n_.alloc(nN);
@@ -261,6 +263,7 @@ Engine::Engine(const pba_problem* p) {
   LinvT_.alloc(static_cast<size_t>(36) * nF * nF);
   Dinv_.alloc(static_cast<size_t>((6 * nF + 31) / 32) * 32 * 32);
   ytmp_.alloc(6 * nF);
+  gauge_.alloc(1);
   status_.alloc(1);
   flags_.alloc(4);
   ck(cudaMallocHost(&status_h_, sizeof(Status)), "pinned");
@@ -424,7 +427,7 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.frames = frames_.p;
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
-  a.dd_fm = dd_fm_.p;
+  a.jstride = jstride();
   a.gamma = gamma;
   a.partial = partial_.p;
   a.rec = rec_.p;
@@ -460,7 +463,7 @@ void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, d
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose_state_.p;
   a.active_out = scratch_bits_.p;
-  launch_scatter_depth(ov_, d_state_.p, nullptr, dd_fm_.p, stream_);
+  a.d_eval = d_state_.p;
   if (mask) {
     std::vector<uint32_t> bits(NO_, 0);
     for (int64_t ou = 0; ou < NO_; ++ou) {
@@ -524,8 +527,8 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose;
   a.pose_old = pose_old;
-  // after k_backsub the per-observation depths {d_cand, d_cur} are already in dd_fm_
-  if (d_old == nullptr) launch_scatter_depth(ov_, d, nullptr, dd_fm_.p, stream_);
+  a.d_eval = d;
+  a.d_old = d_old;
   a.mask_in = mask_in;
   a.active_out = active_out;
   a.J = J_.p;
@@ -604,7 +607,7 @@ void Engine::ic_build(const pba_config* cfg) {
                              ": zero initial translation, inverse depth unobservable from this frame");
   }
   const size_t nO = std::max<int64_t>(NO_, 1);
-  J_.alloc(static_cast<size_t>(7) * nO * P_);
+  J_.alloc(static_cast<size_t>(7) * jstride() + 2);  // +2: aligned TMA windows may overrun by one
   Bic_.alloc(6 * nO);
   Dic_.alloc(std::max(N_, 1));
   Hic_.alloc(21 * std::max(F_, 1));
@@ -612,7 +615,7 @@ void Engine::ic_build(const pba_config* cfg) {
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose0_.p;
   a.pose0 = pose0_.p;
-  launch_scatter_depth(ov_, d0_.p, nullptr, dd_fm_.p, stream_);
+  a.d_eval = d0_.p;
   a.active_out = mask_[0].p;
   a.Jw = J_.p;
   a.B_out = Bic_.p;

@@ -79,6 +79,7 @@ class Engine {
                                double lambda, double* dx);
 
   int64_t num_obs() const { return NO_; }
+  int64_t jstride() const { return ((NO_ * P_ + 1) / 2) * 2; }
   int64_t device_bytes() const;
   cudaStream_t stream() const { return stream_; }
   void set_profiling(bool on);
@@ -106,7 +107,7 @@ class Engine {
 
   DBuf<float> images_;
   DBuf<FrameD> frames_;
-  DBuf<double2> anchor_, anchor_fm_, dd_fm_;
+  DBuf<double2> anchor_, anchor_fm_;
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
   DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
   DBuf<PoseD> pose_state_, pose_cur_, pose_cand_, pose0_;
@@ -123,7 +124,7 @@ class Engine {
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
-  DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_;
+  DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
   DBuf<Status> status_;
   DBuf<int> flags_;
@@ -204,7 +205,8 @@ class Engine {
                double* d_cand, double* dx_out);
   void record_iter(int iter, double energy, double max_upd, int64_t nact, bool accepted, pba_iter_stats* out);
   bool grad_is_zero(int buf);
-  void commit_candidate(double sum_d);
+  void commit_candidate();
+  void gauge_candidate();
   bool iterate_ic(pba_iter_stats* st);
   bool iterate_fc(pba_iter_stats* st);
 };

@@ -55,7 +55,7 @@ void need_built(bool built) {
 
 void Engine::backsub(bool ic, const double* B, const double* D, const double* g_n, double lambda,
                      const double* d_cur, double* d_cand, double* dx_out) {
-  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p, dd_fm_.p};
+  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p};
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_backsub(a, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -121,7 +121,7 @@ void Engine::download_block_hessian(const DBuf<double>& H, const DBuf<double>& D
 void Engine::ic_refresh() {
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose_cur_.p;
-  launch_scatter_depth(ov_, d_cur_.p, nullptr, dd_fm_.p, stream_);
+  a.d_eval = d_cur_.p;
   a.mask_in = mask_[ic_.mcur].p;
   a.active_out = scratch_bits_.p;
   a.J = J_.p;
@@ -153,7 +153,8 @@ void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, 
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose;
   a.pose_old = pose_old;
-  if (d_old == nullptr) launch_scatter_depth(ov_, d, nullptr, dd_fm_.p, stream_);
+  a.d_eval = d;
+  a.d_old = d_old;
   a.mask_in = nullptr;
   a.active_out = scratch_bits_.p;
   a.B_out = B_[buf].p;
@@ -386,14 +387,15 @@ bool Engine::grad_is_zero(int buf) {
   return true;
 }
 
-// accept: parameters <- candidate, then normalize_depth_gauge (solver.cpp:611-620, 803-809)
-void Engine::commit_candidate(double sum_d) {
-  double mean = 1.0;
-  if (run_.cfg.normalize_depth_gauge) {
-    const double m = sum_d / static_cast<double>(N_);
-    if (m > 0.0 && std::isfinite(m)) mean = m;
-  }
-  launch_commit(N_, F_, d_cand_.p, pose_cand_.p, mean, mean, d_cur_.p, pose_cur_.p, stream_);
+// normalize_depth_gauge of the candidate (solver.cpp:135-143), on the device, before the
+// candidate is evaluated (see k_gauge_mean); accepting is then a plain copy.
+void Engine::gauge_candidate() {
+  launch_gauge(N_, F_, partial_bs_.p, backsub_blocks(N_), run_.cfg.normalize_depth_gauge ? 1 : 0, gauge_.p,
+               d_cand_.p, pose_cand_.p, stream_);
+}
+
+void Engine::commit_candidate() {  // solver.cpp:611-620, 803-809
+  launch_commit(N_, F_, d_cand_.p, pose_cand_.p, 1.0, 1.0, d_cur_.p, pose_cur_.p, stream_);
 }
 
 bool Engine::iterate_ic(pba_iter_stats* st) {
@@ -424,6 +426,7 @@ bool Engine::iterate_ic(pba_iter_stats* st) {
     solve_xp(rhs_[b0].p);                                                   // solve_step
     launch_pose_update(1, F_, pose_cur_.p, pose0_.p, xp_.p, pose_cand_.p, stream_);  // :544-552
     backsub(true, Bic_.p, Dic_.p, gn_[b0].p, ic_.lambda, d_cur_.p, d_cand_.p, nullptr);  // :418-428, :553-560
+    gauge_candidate();                                                      // :618-620 (gauge-invariant pass)
     ic_eval(pose_cand_.p, d_cand_.p, mask_[ic_.mcur].p, mask_[1 - ic_.mcur].p, b1, ic_.lambda, pose_cur_.p,
             d_cur_.p);                                                      // :561 + next g
     s = read_status();
@@ -458,7 +461,7 @@ bool Engine::iterate_ic(pba_iter_stats* st) {
   }
   const double max_upd = s.max_upd;  // :609
   const bool zero_grad = max_upd < R.cfg.threshold_px ? grad_is_zero(b0) : false;
-  commit_candidate(s.sum_d);          // :611-620
+  commit_candidate();                 // :611-620
   ic_.mcur = 1 - ic_.mcur;            // mask_ &= cand_pass.active (:613-615)
   R.energy = s.energy;
   R.num_active = static_cast<int64_t>(s.num_active);
@@ -504,6 +507,7 @@ bool Engine::iterate_fc(pba_iter_stats* st) {
       solve_xp(rhs_[b0].p);
       launch_pose_update(0, F_, pose_cur_.p, pose0_.p, xp_.p, pose_cand_.p, stream_);  // :744-746
       backsub(false, B_[b0].p, D_[b0].p, gn_[b0].p, R.lambda, d_cur_.p, d_cand_.p, nullptr);  // :747-750
+      gauge_candidate();  // :807-809: H for the next iteration is built at the normalized candidate
       fc_eval(R.cfg.gamma, pose_cand_.p, d_cand_.p, b1, lam_next, pose_cur_.p, d_cur_.p);     // :752 + next H
       s = read_status();
       if (flags_h_[1] || s.nonfinite > 0) ok = false;  // non-finite solution (:195-211)
@@ -543,7 +547,7 @@ bool Engine::iterate_fc(pba_iter_stats* st) {
   }
   const double max_upd = s.max_upd;  // :800-801
   const bool zero_grad = max_upd < R.cfg.threshold_px ? grad_is_zero(b0) : false;
-  commit_candidate(s.sum_d);
+  commit_candidate();
   R.energy = s.energy;
   R.num_active = static_cast<int64_t>(s.num_active);
   R.cur = b1;

@@ -27,45 +27,154 @@ namespace {
 
 constexpr int NT = 256;  // threads per block for the observation / tile kernels
 
-__device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 
 // ---------------------------------------------------------------------------------
 // k_obs: one block per frame-major tile; G lanes per observation (G = next pow2 >= P)
 // ---------------------------------------------------------------------------------
+// ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Shared-memory staging of one block step (OPS observations).
+constexpr int kStages = 3;
+constexpr int kJStage = 258;    // doubles per J plane per stage: OPS*G(<=256) + 2 alignment slack
+constexpr int kObsStage = 260;  // observation slots per stage: OPS (<=256) + 4 alignment slack
+struct StageSmem {
+  double J[7][kJStage];
+  double2 anc[kObsStage];
+  int32_t fmp[kObsStage];
+  uint32_t msk[kObsStage];
+};
+
+template <int MODE>
+constexpr bool obs_loads_J() {
+  return MODE == OBS_IC || MODE == OBS_REFRESH;
+}
+template <int MODE>
+constexpr size_t obs_smem_bytes() {
+  return obs_loads_J<MODE>() ? kStages * sizeof(StageSmem)
+                             : kStages * (sizeof(StageSmem) - sizeof(double) * 7 * kJStage);
+}
+
 template <int MODE, int G>
 __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3 : 2) k_obs(const ObsArgs a) {
   constexpr int OPS = NT / G;  // observations per block step
   constexpr bool kHasH = (MODE == OBS_FC || MODE == OBS_BUILD || MODE == OBS_REFRESH);
   constexpr bool kHasG = (MODE == OBS_IC || MODE == OBS_FC);
   constexpr bool kHasRec = (MODE != OBS_ENERGY);
-  constexpr bool kLoadJ = (MODE == OBS_IC || MODE == OBS_REFRESH);
+  constexpr bool kLoadJ = obs_loads_J<MODE>();
   const int t = blockIdx.x;
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t];
   const int64_t q1 = a.ov.tile_q1[t];
+  const int nsteps = static_cast<int>((q1 - q0 + OPS - 1) / OPS);
   const bool want_upd = a.pose_old != nullptr;
+  const bool has_mask = (MODE != OBS_BUILD) && a.mask_in != nullptr;
   // frame-uniform data in shared memory (one frame per tile): keeps registers for the pixel math
   __shared__ PoseD s_pe, s_po, s_p0;
   __shared__ FrameD s_fr;
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  // stage layout: [J planes (J modes only)] anc fmp msk
+  auto stage_J = [&](int st) -> double* {
+    return reinterpret_cast<double*>(dyn_smem + static_cast<size_t>(st) * sizeof(StageSmem));
+  };
+  auto stage_tail = [&](int st) -> unsigned char* {
+    return kLoadJ ? dyn_smem + static_cast<size_t>(st) * sizeof(StageSmem) + sizeof(double) * 7 * kJStage
+                  : dyn_smem + static_cast<size_t>(st) * (sizeof(StageSmem) - sizeof(double) * 7 * kJStage);
+  };
+  auto stage_anc = [&](int st) { return reinterpret_cast<double2*>(stage_tail(st)); };
+  auto stage_fmp = [&](int st) { return reinterpret_cast<int32_t*>(stage_tail(st) + sizeof(double2) * kObsStage); };
+  auto stage_msk = [&](int st) {
+    return reinterpret_cast<uint32_t*>(stage_tail(st) + (sizeof(double2) + sizeof(int32_t)) * kObsStage);
+  };
+  const int P = a.pat.P;
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
     if (want_upd) s_po = a.pose_old[f];
     if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
+    for (int i = 0; i < kStages; ++i) mbar_init(&full_bar[i], 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  // producer (thread 0): stream step s of this tile into stage st
+  uint64_t pol = 0;
+  if (kLoadJ && threadIdx.x == 0) pol = evict_first_policy();
+  auto issue = [&](int s, int st) {
+    const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
+    const int64_t qe = qs + OPS < q1 ? qs + OPS : q1;
+    const int64_t i0 = qs & ~int64_t(3), i1 = (qe + 3) & ~int64_t(3);  // 16-byte aligned int32 windows
+    uint32_t tx = static_cast<uint32_t>((qe - qs) * sizeof(double2) + (i1 - i0) * sizeof(int32_t) *
+                                        (has_mask ? 2 : 1));
+    int64_t j0 = 0, j1 = 0;
+    if (kLoadJ) {
+      j0 = (qs * P) & ~int64_t(1);
+      j1 = (qe * P + 1) & ~int64_t(1);
+      tx += static_cast<uint32_t>(7 * (j1 - j0) * sizeof(double));
+    }
+    mbar_expect_tx(&full_bar[st], tx);
+    if (kLoadJ) {
+      double* sJ = stage_J(st);
+      for (int c = 0; c < 7; ++c)
+        bulk_g2s_evict_first(sJ + c * kJStage, a.J + c * a.jstride + j0, static_cast<uint32_t>((j1 - j0) * sizeof(double)),
+                             &full_bar[st], pol);
+    }
+    bulk_g2s(stage_anc(st), a.anchor_fm + qs, static_cast<uint32_t>((qe - qs) * sizeof(double2)), &full_bar[st]);
+    bulk_g2s(stage_fmp(st), a.ov.fm_point + i0, static_cast<uint32_t>((i1 - i0) * sizeof(int32_t)), &full_bar[st]);
+    if (has_mask)
+      bulk_g2s(stage_msk(st), a.mask_in + i0, static_cast<uint32_t>((i1 - i0) * sizeof(uint32_t)), &full_bar[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s, s);
+
   const FrameD& fr = s_fr;
   const PoseD& pe = s_pe;
   const PoseD& po = s_po;
   const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
-  const int P = a.pat.P;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int k = threadIdx.x % G;
   const int j = threadIdx.x / G;
   const bool klive = k < P;
-  const int64_t NPX = a.ov.NO * static_cast<int64_t>(P);
   const double gam = a.gamma;
 
   double gacc[6] = {0, 0, 0, 0, 0, 0};
@@ -74,22 +183,32 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
   for (int i = 0; i < (kHasH ? 21 : 1); ++i) hacc[i] = 0.0;
   double energy = 0.0, nact = 0.0, noob = 0.0, maxupd = 0.0;
 
-  for (int64_t base = q0; base < q1; base += OPS) {
-    const int64_t q = base + j;
+  for (int s = 0; s < nsteps; ++s) {
+    const int st = s % kStages;
+    if (threadIdx.x == 0 && s + kStages - 1 < nsteps) {
+      fence_proxy_async_smem();  // generic-proxy reads of that stage (previous round) precede the TMA write
+      issue(s + kStages - 1, (s + kStages - 1) % kStages);
+    }
+    mbar_wait(&full_bar[st], static_cast<uint32_t>((s / kStages) & 1));
+    const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
+    const int64_t q = qs + j;
     const bool live = q < q1;
-    // ---- level-1 loads: all coalesced and independent of each other ----
     double2 an = make_double2(0.0, 0.0), dd = make_double2(1.0, 1.0);
     uint32_t mbits = 0u;
     double J[kLoadJ ? 7 : 1];
     if (live) {
-      an = __ldg(&a.anchor_fm[q]);
-      dd = __ldg(&a.dd_fm[q]);
-      mbits = (MODE == OBS_BUILD || a.mask_in == nullptr) ? 0xffffffffu : __ldg(&a.mask_in[q]);
+      const int64_t i0 = qs & ~int64_t(3);
+      an = stage_anc(st)[q - qs];
+      const int n = stage_fmp(st)[q - i0];
+      dd.x = __ldg(&a.d_eval[n]);
+      dd.y = want_upd ? __ldg(&a.d_old[n]) : dd.x;
+      mbits = has_mask ? stage_msk(st)[q - i0] : 0xffffffffu;
       if constexpr (kLoadJ) {
         if (klive) {
-          const int64_t px = q * P + k;
+          const int64_t jj = q * P + k - ((qs * P) & ~int64_t(1));
+          const double* sJ = stage_J(st);
 #pragma unroll
-          for (int c = 0; c < 7; ++c) J[c] = ldcs(a.J + c * NPX + px);
+          for (int c = 0; c < 7; ++c) J[c] = sJ[c * kJStage + jj];
         }
       }
     }
@@ -239,7 +358,7 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
             }
           }
 #pragma unroll
-          for (int c = 0; c < 7; ++c) a.Jw[c * NPX + px] = row[c];
+          for (int c = 0; c < 7; ++c) a.Jw[c * a.jstride + px] = row[c];
         }
       }
     }
@@ -262,6 +381,7 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
       }
     }
+    __syncthreads();  // stage st is free: the producer refills it at step s + 1
   }
 
   // ---- deterministic block reduction of the per-lane frame accumulators ----
@@ -301,16 +421,26 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
   }
 }
 
+template <int MODE, int G>
+void launch_obs_g(const ObsArgs& a, cudaStream_t s) {
+  constexpr size_t smem = obs_smem_bytes<MODE>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_obs<MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = true;
+  }
+  k_obs<MODE, G><<<a.ov.ntiles, NT, smem, s>>>(a);
+}
+
 template <int MODE>
 void launch_obs_mode(const ObsArgs& a, int G, cudaStream_t s) {
-  const dim3 grid(a.ov.ntiles), block(NT);
   switch (G) {
-    case 1: k_obs<MODE, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: k_obs<MODE, 2><<<grid, block, 0, s>>>(a); break;
-    case 4: k_obs<MODE, 4><<<grid, block, 0, s>>>(a); break;
-    case 8: k_obs<MODE, 8><<<grid, block, 0, s>>>(a); break;
-    case 16: k_obs<MODE, 16><<<grid, block, 0, s>>>(a); break;
-    default: k_obs<MODE, 32><<<grid, block, 0, s>>>(a); break;
+    case 1: launch_obs_g<MODE, 1>(a, s); break;
+    case 2: launch_obs_g<MODE, 2>(a, s); break;
+    case 4: launch_obs_g<MODE, 4>(a, s); break;
+    case 8: launch_obs_g<MODE, 8>(a, s); break;
+    case 16: launch_obs_g<MODE, 16>(a, s); break;
+    default: launch_obs_g<MODE, 32>(a, s); break;
   }
 }
 
@@ -373,7 +503,6 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
       acc += dot;
     }
     acc = warp_sum(acc);
-    double dn_b = 0.0;
     if (lane == 0) {
       const double D = a.D[n] + a.lambda;
       const double dx = (-a.g_n[n] - acc) / D;
@@ -390,12 +519,6 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
       sum_d += dn;
       if (dn <= 0.0) ninv += 1.0;
       if (!isfinite(dx)) nnf += 1.0;
-      dn_b = dn;
-    }
-    if (a.dd_fm) {  // per-observation {candidate depth, current depth} for k_obs
-      dn_b = __shfl_sync(0xffffffffu, dn_b, 0);
-      const double dc = a.d_cur[n];
-      for (int64_t o = o0 + lane; o < o1; o += 32) a.dd_fm[a.ov.pm2fm[o]] = make_double2(dn_b, dc);
     }
   }
   if (lane == 0) {
@@ -409,18 +532,6 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
     for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
     a.partial[blockIdx.x * 4 + threadIdx.x] = v;
   }
-}
-
-// ---------------------------------------------------------------------------------
-// k_scatter_depth: per-observation {d_eval, d_old} in frame-major order (no update)
-// ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_scatter_depth(const ObsView ov, const double* __restrict__ d_eval,
-                                                      const double* __restrict__ d_old, double2* __restrict__ dd_fm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = blockIdx.x * (NT / 32) + warp;
-  if (n >= ov.N) return;
-  const double2 v = make_double2(d_eval[n], d_old ? d_old[n] : d_eval[n]);
-  for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) dd_fm[ov.pm2fm[o]] = v;
 }
 
 // ---------------------------------------------------------------------------------
@@ -592,6 +703,35 @@ __global__ void k_commit(int N, int F, const double* __restrict__ d_cand, const 
     for (int r = 0; r < 3; ++r) p.t[r] = p.t[r] * tscale;
     pose_cur[i] = p;
   }
+}
+
+// ---------------------------------------------------------------------------------
+// Depth gauge of the candidate (normalize_depth_gauge, solver.cpp:135-143, applied by the
+// reference after acceptance at :618-620 / :807-809).  The candidate is normalized BEFORE
+// it is evaluated: residuals, energy and the reprojection update are gauge-invariant, and
+// the FC Jacobian/Hessian built in the same pass then sits in the normalized
+// parametrization exactly like the reference's next-iteration build (:688-724).
+// ---------------------------------------------------------------------------------
+__global__ void k_gauge_mean(const double* __restrict__ partial_bs, int nbs, int N, int enabled,
+                             double* __restrict__ scale) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int b = lane; b < nbs; b += 32) v += partial_bs[b * 4];  // same fixed order as k_finalize
+  v = warp_sum(v);
+  if (threadIdx.x == 0) {
+    const double mean = v / static_cast<double>(N);
+    *scale = (enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
+  }
+}
+
+__global__ void k_gauge_apply(int N, int F, const double* __restrict__ scale, double* __restrict__ d,
+                              PoseD* __restrict__ pose) {
+  const double m = *scale;
+  if (m == 1.0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) d[i] = d[i] / m;
+  if (i < F)
+    for (int r = 0; r < 3; ++r) pose[i].t[r] = pose[i].t[r] * m;
 }
 
 // ---------------------------------------------------------------------------------
@@ -972,15 +1112,6 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
   }
 }
 
-void launch_scatter_depth(const ObsView& ov, const double* d_eval, const double* d_old, double2* dd_fm,
-                          cudaStream_t s) {
-  const int nb = (ov.N + (NT / 32) - 1) / (NT / 32);
-  if (nb > 0) {
-    k_scatter_depth<<<nb, NT, 0, s>>>(ov, d_eval, d_old, dd_fm);
-    count_launches(1);
-  }
-}
-
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s) {
   if (ov.ntiles > 0) {
     k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf);
@@ -998,6 +1129,14 @@ void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, d
   const int m = N > F ? N : F;
   k_commit<<<(m + 255) / 256, 256, 0, s>>>(N, F, d_cand, pose_cand, scale_d, scale_t, d_cur, pose_cur);
   count_launches(1);
+}
+
+void launch_gauge(int N, int F, const double* partial_bs, int nbs, int enabled, double* scale, double* d,
+                  PoseD* pose, cudaStream_t s) {
+  k_gauge_mean<<<1, 32, 0, s>>>(partial_bs, nbs, N, enabled, scale);
+  const int m = N > F ? N : F;
+  k_gauge_apply<<<(m + 255) / 256, 256, 0, s>>>(N, F, scale, d, pose);
+  count_launches(2);
 }
 
 void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref, const double2* anchor, int dx0,

@@ -32,8 +32,9 @@ struct ObsArgs {
   double ref_ifx, ref_ify;     // 1 / ref.fx, 1 / ref.fy (template normalization)
   const FrameD* frames;        // F
   PatternD pat;
-  const double2* anchor_fm;    // NO: anchor pixel of obs q (frame-major copy, static)
-  const double2* dd_fm;        // NO: {depth at evaluation, depth at old params} of obs q
+  const double2* anchor_fm;    // NO: anchor pixel of obs q (frame-major copy, static, TMA-staged)
+  const double* d_eval;        // N: inverse depths at the evaluation parameters (internal order)
+  const double* d_old;         // N or null: inverse depths at the old parameters (max update)
   double gamma;
   const PoseD* pose_eval;      // F
   const PoseD* pose_old;       // F or null (max reprojection update)
@@ -42,6 +43,7 @@ struct ObsArgs {
   uint32_t* active_out;        // NO bit words
   double* r_out;               // NO*P or null
   const double* J;             // 7 planes of NO*P (IC / REFRESH read, BUILD write)
+  int64_t jstride;             // plane stride in doubles (even: 16-byte aligned TMA sources)
   double* Jw;                  // BUILD output planes
   double* B_out;               // NO*6 (FC/BUILD/REFRESH)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
@@ -70,7 +72,6 @@ struct BacksubArgs {
   double* d_cand;         // N
   double* dx_out;         // N or null
   double* partial;        // nblocks * 4
-  double2* dd_fm;         // NO or null: per-observation {d_cand, d_cur} for the next k_obs
 };
 int backsub_blocks(int N);
 void launch_backsub(const BacksubArgs& a, cudaStream_t s);
@@ -89,10 +90,6 @@ struct PointArgs {
 };
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);
-
-// Per-observation depths {d_eval, d_old (or d_eval)} in frame-major order.
-void launch_scatter_depth(const ObsView& ov, const double* d_eval, const double* d_old, double2* dd_fm,
-                          cudaStream_t s);
 
 // Frame-major  c_f = sum_n B_nf s_n  per tile.
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf,
@@ -130,6 +127,10 @@ void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 // Accept: d_cur = d_cand / mean, t_cur = t_cand * mean (solver.cpp:135-143).
 void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, double scale_d,
                    double scale_t, double* d_cur, PoseD* pose_cur, cudaStream_t s);
+
+// Depth-gauge normalization of a candidate from k_backsub's partial sums (solver.cpp:135-143).
+void launch_gauge(int N, int F, const double* partial_bs, int nbs, int enabled, double* scale, double* d,
+                  PoseD* pose, cudaStream_t s);
 
 // Max reprojection update between two parameter sets (solver.cpp:105-131).
 void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref,

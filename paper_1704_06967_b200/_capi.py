@@ -14,7 +14,7 @@ from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 REPO = _PKG.parent
-GPU_LIB = _PKG / "lib" / "libpba_gpu.so"
+GPU_LIB = Path(os.environ.get("PBA_GPU_LIB", str(_PKG / "lib" / "libpba_gpu.so")))  # override: experiments only
 ORACLE_LIB = REPO / "oracle" / "_build" / "liboracle.so"
 
 # status codes (pba_gpu.h)

@@ -153,6 +153,37 @@ Engine::Engine(const pba_problem* p) {
     for (int64_t j = 0; j < uo_ptr_[u + 1] - uo_ptr_[u]; ++j) uo2q_[uo_ptr_[u] + j] = pm2fm[pm_ptr[i] + j];
   }
 
+  // ---- Schur chunk plan: points sorted by visibility window (first, last frame), chunks of
+  //      kChunk points; one work item per 64x64 upper tile-block of each chunk's window ----
+  std::vector<int32_t> chunk_pts;
+  std::vector<int4> sblocks;
+  {
+    constexpr int kChunk = 512;
+    std::vector<int32_t> order;
+    for (int i = 0; i < N_; ++i)
+      if (pm_ptr[i + 1] > pm_ptr[i]) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const int fa = pm_frame[pm_ptr[a]], fb = pm_frame[pm_ptr[b]];
+      if (fa != fb) return fa < fb;
+      return pm_frame[pm_ptr[a + 1] - 1] < pm_frame[pm_ptr[b + 1] - 1];
+    });
+    chunk_pts = order;
+    for (size_t c0 = 0; c0 < order.size(); c0 += kChunk) {
+      const size_t c1 = std::min(order.size(), c0 + kChunk);
+      int fmin = F_, fmax = -1;
+      for (size_t i = c0; i < c1; ++i) {
+        fmin = std::min(fmin, pm_frame[pm_ptr[order[i]]]);
+        fmax = std::max(fmax, pm_frame[pm_ptr[order[i] + 1] - 1]);
+      }
+      const int W = fmax - fmin + 1;
+      const int nb = (6 * W + 63) / 64;
+      if (fmin > 0xffff || W > 0x7fff || nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
+      for (int rb = 0; rb < nb; ++rb)
+        for (int cb = rb; cb < nb; ++cb)
+          sblocks.push_back(make_int4(static_cast<int>(c0), static_cast<int>(c1), fmin | (W << 16), rb | (cb << 16)));
+    }
+  }
+
   // ---- frame-major tiles ----
   const int G = next_pow2(P_);
   const int ops = 256 / G;
@@ -187,6 +218,8 @@ Engine::Engine(const pba_problem* p) {
   up(tile_q0_, tq0);
   up(tile_q1_, tq1);
   up(ftile_ptr_, ftile_ptr);
+  up(chunk_pts_, chunk_pts);
+  up(schur_blocks_, sblocks);
   // pinned staging vectors must outlive the async copies
   ck(cudaStreamSynchronize(stream_), "sync upload");
 
@@ -204,6 +237,7 @@ Engine::Engine(const pba_problem* p) {
   ov_.tile_q0 = tile_q0_.p;
   ov_.tile_q1 = tile_q1_.p;
   ov_.ftile_ptr = ftile_ptr_.p;
+  schur_plan_ = SchurPlan{chunk_pts_.p, schur_blocks_.p, static_cast<int>(sblocks.size())};
 
   // ---- points ----
   std::vector<double2> anc(N_);
@@ -557,7 +591,7 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   const int n = 6 * F_;
   clear_flags();
   auto e = ev_begin(PBA_K_SCHUR);
-  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, stream_);
+  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, stream_);
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);
   launch_cholesky(S_.p, n, flags_.p, stream_);

@@ -126,6 +126,9 @@ class Engine {
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
   DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
+  DBuf<int32_t> chunk_pts_;
+  DBuf<int4> schur_blocks_;
+  SchurPlan schur_plan_{};
   DBuf<Status> status_;
   DBuf<int> flags_;
   Status* status_h_ = nullptr;    // pinned

@@ -41,6 +41,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -93,8 +96,17 @@ constexpr size_t obs_smem_bytes() {
                              : kStages * (sizeof(StageSmem) - sizeof(double) * 7 * kJStage);
 }
 
+constexpr int NT_OBS = NT + 32;  // 8 consumer warps + 1 producer warp
+
+#ifndef PBA_OBS_MINB_IC
+#define PBA_OBS_MINB_IC 2
+#endif
+#ifndef PBA_OBS_MINB_OTHER
+#define PBA_OBS_MINB_OTHER 1
+#endif
 template <int MODE, int G>
-__global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3 : 2) k_obs(const ObsArgs a) {
+__global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY) ? PBA_OBS_MINB_IC : PBA_OBS_MINB_OTHER)
+    k_obs(const ObsArgs a) {
   constexpr int OPS = NT / G;  // observations per block step
   constexpr bool kHasH = (MODE == OBS_FC || MODE == OBS_BUILD || MODE == OBS_REFRESH);
   constexpr bool kHasG = (MODE == OBS_IC || MODE == OBS_FC);
@@ -111,67 +123,74 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
   __shared__ PoseD s_pe, s_po, s_p0;
   __shared__ FrameD s_fr;
   __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ double red[NT / 32][PT_STRIDE];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  // stage layout: [J planes (J modes only)] anc fmp msk
-  auto stage_J = [&](int st) -> double* {
-    return reinterpret_cast<double*>(dyn_smem + static_cast<size_t>(st) * sizeof(StageSmem));
-  };
-  auto stage_tail = [&](int st) -> unsigned char* {
-    return kLoadJ ? dyn_smem + static_cast<size_t>(st) * sizeof(StageSmem) + sizeof(double) * 7 * kJStage
-                  : dyn_smem + static_cast<size_t>(st) * (sizeof(StageSmem) - sizeof(double) * 7 * kJStage);
-  };
-  auto stage_anc = [&](int st) { return reinterpret_cast<double2*>(stage_tail(st)); };
-  auto stage_fmp = [&](int st) { return reinterpret_cast<int32_t*>(stage_tail(st) + sizeof(double2) * kObsStage); };
-  auto stage_msk = [&](int st) {
-    return reinterpret_cast<uint32_t*>(stage_tail(st) + (sizeof(double2) + sizeof(int32_t)) * kObsStage);
-  };
+  constexpr size_t kStageBytes = kLoadJ ? sizeof(StageSmem) : sizeof(StageSmem) - sizeof(double) * 7 * kJStage;
+  constexpr size_t kTail = kLoadJ ? sizeof(double) * 7 * kJStage : 0;
   const int P = a.pat.P;
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
     if (want_upd) s_po = a.pose_old[f];
     if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
-    for (int i = 0; i < kStages; ++i) mbar_init(&full_bar[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], NT / 32);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  // producer (thread 0): stream step s of this tile into stage st
-  uint64_t pol = 0;
-  if (kLoadJ && threadIdx.x == 0) pol = evict_first_policy();
-  auto issue = [&](int s, int st) {
-    const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
-    const int64_t qe = qs + OPS < q1 ? qs + OPS : q1;
-    const int64_t i0 = qs & ~int64_t(3), i1 = (qe + 3) & ~int64_t(3);  // 16-byte aligned int32 windows
-    uint32_t tx = static_cast<uint32_t>((qe - qs) * sizeof(double2) + (i1 - i0) * sizeof(int32_t) *
-                                        (has_mask ? 2 : 1));
-    int64_t j0 = 0, j1 = 0;
-    if (kLoadJ) {
-      j0 = (qs * P) & ~int64_t(1);
-      j1 = (qe * P + 1) & ~int64_t(1);
-      tx += static_cast<uint32_t>(7 * (j1 - j0) * sizeof(double));
-    }
-    mbar_expect_tx(&full_bar[st], tx);
-    if (kLoadJ) {
-      double* sJ = stage_J(st);
-      for (int c = 0; c < 7; ++c)
-        bulk_g2s_evict_first(sJ + c * kJStage, a.J + c * a.jstride + j0, static_cast<uint32_t>((j1 - j0) * sizeof(double)),
-                             &full_bar[st], pol);
-    }
-    bulk_g2s(stage_anc(st), a.anchor_fm + qs, static_cast<uint32_t>((qe - qs) * sizeof(double2)), &full_bar[st]);
-    bulk_g2s(stage_fmp(st), a.ov.fm_point + i0, static_cast<uint32_t>((i1 - i0) * sizeof(int32_t)), &full_bar[st]);
-    if (has_mask)
-      bulk_g2s(stage_msk(st), a.mask_in + i0, static_cast<uint32_t>((i1 - i0) * sizeof(uint32_t)), &full_bar[st]);
-  };
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kStages - 1 && s < nsteps; ++s) issue(s, s);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
 
+  if (warp == NT / 32) {
+    // ---------------- producer warp: TMA bulk copies, kStages steps ahead ----------------
+    if (lane == 0) {
+      const uint64_t pol = kLoadJ ? evict_first_policy() : 0;
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % kStages;
+        const int round = s / kStages;
+        if (round > 0) mbar_wait(&empty_bar[st], static_cast<uint32_t>((round - 1) & 1));
+        fence_proxy_async_smem();
+        unsigned char* base = dyn_smem + static_cast<size_t>(st) * kStageBytes;
+        const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
+        const int64_t qe = qs + OPS < q1 ? qs + OPS : q1;
+        const int64_t i0 = qs & ~int64_t(3), i1 = (qe + 3) & ~int64_t(3);  // 16-byte aligned int32 windows
+        uint32_t tx = static_cast<uint32_t>((qe - qs) * sizeof(double2) + (i1 - i0) * sizeof(int32_t) *
+                                            (has_mask ? 2 : 1));
+        int64_t j0 = 0, j1 = 0;
+        if (kLoadJ) {
+          j0 = (qs * P) & ~int64_t(1);
+          j1 = (qe * P + 1) & ~int64_t(1);
+          tx += static_cast<uint32_t>(7 * (j1 - j0) * sizeof(double));
+        }
+        mbar_expect_tx(&full_bar[st], tx);
+        if (kLoadJ) {
+          double* sJ = reinterpret_cast<double*>(base);
+          for (int c = 0; c < 7; ++c)
+            bulk_g2s_evict_first(sJ + c * kJStage, a.J + c * a.jstride + j0,
+                                 static_cast<uint32_t>((j1 - j0) * sizeof(double)), &full_bar[st], pol);
+        }
+        unsigned char* tail = base + kTail;
+        bulk_g2s(tail, a.anchor_fm + qs, static_cast<uint32_t>((qe - qs) * sizeof(double2)), &full_bar[st]);
+        bulk_g2s(tail + sizeof(double2) * kObsStage, a.ov.fm_point + i0,
+                 static_cast<uint32_t>((i1 - i0) * sizeof(int32_t)), &full_bar[st]);
+        if (has_mask)
+          bulk_g2s(tail + (sizeof(double2) + sizeof(int32_t)) * kObsStage, a.mask_in + i0,
+                   static_cast<uint32_t>((i1 - i0) * sizeof(uint32_t)), &full_bar[st]);
+      }
+    }
+    __syncthreads();  // matches the consumers' reduction barrier
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
   const FrameD& fr = s_fr;
   const PoseD& pe = s_pe;
   const PoseD& po = s_po;
   const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const int k = threadIdx.x % G;
   const int j = threadIdx.x / G;
   const bool klive = k < P;
@@ -185,32 +204,36 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
 
   for (int s = 0; s < nsteps; ++s) {
     const int st = s % kStages;
-    if (threadIdx.x == 0 && s + kStages - 1 < nsteps) {
-      fence_proxy_async_smem();  // generic-proxy reads of that stage (previous round) precede the TMA write
-      issue(s + kStages - 1, (s + kStages - 1) % kStages);
-    }
     mbar_wait(&full_bar[st], static_cast<uint32_t>((s / kStages) & 1));
+    const unsigned char* base = dyn_smem + static_cast<size_t>(st) * kStageBytes;
+    const unsigned char* tail = base + kTail;
     const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
     const int64_t q = qs + j;
     const bool live = q < q1;
     double2 an = make_double2(0.0, 0.0), dd = make_double2(1.0, 1.0);
     uint32_t mbits = 0u;
+    int n = 0;
     double J[kLoadJ ? 7 : 1];
     if (live) {
-      const int64_t i0 = qs & ~int64_t(3);
-      an = stage_anc(st)[q - qs];
-      const int n = stage_fmp(st)[q - i0];
-      dd.x = __ldg(&a.d_eval[n]);
-      dd.y = want_upd ? __ldg(&a.d_old[n]) : dd.x;
-      mbits = has_mask ? stage_msk(st)[q - i0] : 0xffffffffu;
+      const int ioff = static_cast<int>(qs & 3);  // skew of the aligned int32 window
+      an = reinterpret_cast<const double2*>(tail)[j];
+      n = reinterpret_cast<const int32_t*>(tail + sizeof(double2) * kObsStage)[j + ioff];
+      mbits = has_mask ? reinterpret_cast<const uint32_t*>(tail + (sizeof(double2) + sizeof(int32_t)) * kObsStage)[j + ioff]
+                       : 0xffffffffu;
       if constexpr (kLoadJ) {
         if (klive) {
-          const int64_t jj = q * P + k - ((qs * P) & ~int64_t(1));
-          const double* sJ = stage_J(st);
+          const int jj = j * P + k + static_cast<int>((qs * P) & 1);
+          const double* sJ = reinterpret_cast<const double*>(base);
 #pragma unroll
           for (int c = 0; c < 7; ++c) J[c] = sJ[c * kJStage + jj];
         }
       }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data now lives in registers
+    if (live) {
+      dd.x = __ldg(&a.d_eval[n]);
+      dd.y = want_upd ? __ldg(&a.d_old[n]) : dd.x;
     }
     const double dv = dd.x;  // depth at the evaluation parameters
     bool act = false;        // residual active at the evaluation parameters
@@ -290,7 +313,8 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
               dc = w * row[6] * row[6];
               gnc = row[6] * wr;
             } else if constexpr (MODE == OBS_IC) {
-              const double wr = huber_weight(r, gam) * r;  // fresh weights (solver.cpp:461)
+              // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
+              const double wr = fabs(r) <= gam ? r : copysign(gam, r);
 #pragma unroll
               for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
               gnc = J[6] * wr;
@@ -381,11 +405,9 @@ __global__ void __launch_bounds__(NT, (MODE == OBS_IC || MODE == OBS_ENERGY) ? 3
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
       }
     }
-    __syncthreads();  // stage st is free: the producer refills it at step s + 1
   }
 
   // ---- deterministic block reduction of the per-lane frame accumulators ----
-  __shared__ double red[NT / 32][PT_STRIDE];
   auto put = [&](int slot, double v) {
     v = warp_sum(v);
     if (lane == 0) red[warp][slot] = v;
@@ -429,7 +451,7 @@ void launch_obs_g(const ObsArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_obs<MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
-  k_obs<MODE, G><<<a.ov.ntiles, NT, smem, s>>>(a);
+  k_obs<MODE, G><<<a.ov.ntiles, NT_OBS, smem, s>>>(a);
 }
 
 template <int MODE>
@@ -837,6 +859,94 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
   }
 }
 
+// Chunked dense Schur update on the FP64 tensor path (DMMA, mma.sync.m8n8k4.f64).
+// Points are sorted by visibility window and cut into chunks; a chunk's scaled blocks
+// b_n / sqrt(D_n + lambda) form a dense [points x 6W] matrix over its frame window, and
+// one CTA computes one 64x64 tile-block of its Gram matrix (upper triangle of tile-blocks),
+// K-looping over the chunk's points through shared memory.  8 warps x 8 DMMA 8x8 tiles.
+// Results enter S through the same deterministic fixed-point RED as k_schur_pts.
+constexpr int SCH_TB = 64;   // tile-block edge (window-local dimensions)
+constexpr int SCH_KB = 32;   // points staged per K sub-batch
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_schur_dense(const ObsView ov, const double* __restrict__ B,
+                                                     const double* __restrict__ D, double lambda,
+                                                     const int32_t* __restrict__ chunk_pts,
+                                                     const int4* __restrict__ blocks,
+                                                     const double* __restrict__ scale,
+                                                     unsigned long long* __restrict__ acc) {
+  // blocks[b] = {chunk point begin, chunk point end, fmin | (W << 16), rb | (cb << 16)}
+  const int4 blk = blocks[blockIdx.x];
+  const int p0 = blk.x, p1 = blk.y, fmin = blk.z & 0xffff, W = blk.z >> 16;
+  const int rb = blk.w & 0xffff, cb = blk.w >> 16;
+  const int dim = 6 * W;
+  const int r0 = rb * SCH_TB, c0 = cb * SCH_TB;
+  const bool diag = rb == cb;
+  __shared__ double As[SCH_TB][SCH_KB + 1];
+  __shared__ double Bs[SCH_TB][SCH_KB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double accd[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) accd[i][0] = accd[i][1] = 0.0;
+  for (int pb = p0; pb < p1; pb += SCH_KB) {
+    const int np = min(SCH_KB, p1 - pb);
+    for (int e = tid; e < SCH_TB * (SCH_KB + 1); e += 256) {
+      (&As[0][0])[e] = 0.0;
+      (&Bs[0][0])[e] = 0.0;
+    }
+    __syncthreads();
+    // densify: one warp per point, lanes over its observations
+    for (int pp = warp; pp < np; pp += 8) {
+      const int n = chunk_pts[pb + pp];
+      const double isq = 1.0 / sqrt(D[n] + lambda);
+      for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) {
+        const int lf = ov.pm_frame[o] - fmin;
+        const double* b = B + static_cast<int64_t>(ov.pm2fm[o]) * 6;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const int li = 6 * lf + i;
+          const double v = b[i] * isq;
+          if (li >= r0 && li < r0 + SCH_TB) As[li - r0][pp] = v;
+          if (li >= c0 && li < c0 + SCH_TB) Bs[li - c0][pp] = v;
+        }
+      }
+    }
+    __syncthreads();
+    // C(64x64) += As * Bs^T; warp w owns tile row w, tile cols 0..7
+    for (int k = 0; k < np; k += 4) {
+      const double a = As[warp * 8 + (lane >> 2)][k + (lane & 3)];
+#pragma unroll
+      for (int tc = 0; tc < 8; ++tc) {
+        const double b = Bs[tc * 8 + (lane >> 2)][k + (lane & 3)];
+        dmma_8x8x4(accd[tc][0], accd[tc][1], a, b);
+      }
+    }
+    __syncthreads();
+  }
+  // scatter into S (window-local -> global), fixed point
+  const int ld = 6 * ov.F;
+  const int gbase = 6 * fmin;
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int lr = r0 + warp * 8 + (lane >> 2);
+      const int lc = c0 + tc * 8 + (lane & 3) * 2 + i;
+      if (lr >= dim || lc >= dim) continue;
+      const int r = gbase + lr, c = gbase + lc;
+      const long long qv = llrint(accd[tc][i] * scale[r] * scale[c]);
+      if (qv == 0) continue;
+      atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(qv));
+      if (!diag) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(qv));
+    }
+  }
+}
+
 __global__ void k_schur_final(int F, const double* __restrict__ H21, double lambda, const double* __restrict__ scale,
                               const unsigned long long* __restrict__ acc, double* __restrict__ S) {
   const int n = 6 * F;
@@ -1147,15 +1257,24 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 }
 
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
-                  double* scale, unsigned long long* acc, cudaStream_t s) {
+                  double* scale, unsigned long long* acc, const SchurPlan* plan, cudaStream_t s) {
   const int n = 6 * ov.F;
   const int64_t total = static_cast<int64_t>(n) * n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
   k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total);
-  const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
-  if (pb > 0) k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, scale, acc);
+  int launched = 2;
+  if (plan && plan->nblocks > 0) {
+    k_schur_dense<<<plan->nblocks, 256, 0, s>>>(ov, B, D, lambda, plan->chunk_pts, plan->blocks, scale, acc);
+    ++launched;
+  } else {
+    const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
+    if (pb > 0) {
+      k_schur_pts<<<pb, NT, 0, s>>>(ov, B, D, lambda, scale, acc);
+      ++launched;
+    }
+  }
   k_schur_final<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, scale, acc, S);
-  count_launches(pb > 0 ? 3 : 2);
+  count_launches(launched);
 }
 
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {

@@ -139,9 +139,18 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 
 // Reduced camera system S = blockdiag(H_ff + lambda I) - sum_n b_n b_n^T / (D_n + lambda)
 // (solver.cpp:170-189, 375-392).  S is 6F x 6F row-major, full.
+// Chunk plan for the dense (DMMA) Schur path: points sorted by visibility window, cut into
+// chunks, one entry per 64x64 upper-triangle tile-block of each chunk's window Gram matrix.
+struct SchurPlan {
+  const int32_t* chunk_pts;  // N internal point ids in window order
+  const int4* blocks;        // {begin, end, fmin | W << 16, rb | cb << 16}
+  int nblocks;
+};
 // Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.
+// plan == nullptr selects the per-point pair kernel.
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D,
-                  double lambda, double* S, double* scale, unsigned long long* acc, cudaStream_t s);
+                  double lambda, double* S, double* scale, unsigned long long* acc, const SchurPlan* plan,
+                  cudaStream_t s);
 
 // In-place dense Cholesky (lower) of the n x n row-major S; *fail set on a
 // non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).

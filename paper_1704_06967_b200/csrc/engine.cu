@@ -12,42 +12,8 @@ namespace pba_b200 {
 
 namespace {
 
-uint32_t morton_key(double u, double v) {
-  auto part = [](uint32_t x) {
-    x &= 0xffff;
-    x = (x | (x << 8)) & 0x00FF00FF;
-    x = (x | (x << 4)) & 0x0F0F0F0F;
-    x = (x | (x << 2)) & 0x33333333;
-    x = (x | (x << 1)) & 0x55555555;
-    return x;
-  };
-  const double cu = std::min(std::max(std::floor(u), 0.0), 65535.0);
-  const double cv = std::min(std::max(std::floor(v), 0.0), 65535.0);
-  return part(static_cast<uint32_t>(cu)) | (part(static_cast<uint32_t>(cv)) << 1);
-}
-
-int next_pow2(int p) {
-  int g = 1;
-  while (g < p) g <<= 1;
-  return g;
-}
 
 }  // namespace
-
-template <typename T>
-void DBuf<T>::alloc(size_t count) {
-  if (count == n && p) return;
-  release();
-  if (count == 0) return;
-  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
-  n = count;
-}
-template <typename T>
-void DBuf<T>::release() {
-  if (p) cudaFree(p);
-  p = nullptr;
-  n = 0;
-}
 
 // =====================================================================================
 // construction: upload the ProblemState (solver.hpp:33-43) into the device layout
@@ -94,174 +60,8 @@ Engine::Engine(const pba_problem* p) {
   if (F_ > 0)
     ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, stream_), "frames");
 
-  // ---- user observation list ----
-  uo_ptr_.assign(N_ + 1, 0);
-  if (p->obs_ptr) {
-    if (p->obs_ptr[0] != 0) throw PbaError(PBA_E_ARG, "obs_ptr[0] must be 0");
-    for (int n = 0; n <= N_; ++n) uo_ptr_[n] = p->obs_ptr[n];
-    uo_frame_.assign(p->obs_frame, p->obs_frame + uo_ptr_[N_]);
-    for (int n = 0; n < N_; ++n) {
-      if (uo_ptr_[n + 1] < uo_ptr_[n]) throw PbaError(PBA_E_ARG, "obs_ptr must be non-decreasing");
-      for (int64_t o = uo_ptr_[n]; o < uo_ptr_[n + 1]; ++o) {
-        if (uo_frame_[o] < 0 || uo_frame_[o] >= F_) throw PbaError(PBA_E_ARG, "obs_frame out of range");
-        if (o > uo_ptr_[n] && uo_frame_[o] <= uo_frame_[o - 1])
-          throw PbaError(PBA_E_ARG, "obs_frame must be strictly increasing per point");
-      }
-    }
-  } else {
-    for (int n = 0; n <= N_; ++n) uo_ptr_[n] = static_cast<int64_t>(n) * F_;
-    uo_frame_.resize(static_cast<size_t>(N_) * F_);
-    for (int n = 0; n < N_; ++n)
-      for (int f = 0; f < F_; ++f) uo_frame_[static_cast<size_t>(n) * F_ + f] = f;
-  }
-  NO_ = uo_ptr_[N_];
-  if (NO_ >= (int64_t(1) << 31) - 1) throw PbaError(PBA_E_ARG, "more than 2^31 observations");
-
-  // ---- internal point order: Morton order of the anchor pixel (texture locality) ----
-  perm_.resize(N_);
-  std::iota(perm_.begin(), perm_.end(), 0);
-  {
-    std::vector<uint32_t> key(N_);
-    for (int n = 0; n < N_; ++n) key[n] = morton_key(p->anchors_px[2 * n], p->anchors_px[2 * n + 1]);
-    std::stable_sort(perm_.begin(), perm_.end(), [&](int a, int b) { return key[a] < key[b]; });
-  }
-  iperm_.resize(N_);
-  for (int i = 0; i < N_; ++i) iperm_[perm_[i]] = i;
-
-  std::vector<int64_t> pm_ptr(N_ + 1, 0);
-  std::vector<int32_t> pm_frame(NO_);
-  for (int i = 0; i < N_; ++i) {
-    const int u = perm_[i];
-    const int64_t k = uo_ptr_[u + 1] - uo_ptr_[u];
-    pm_ptr[i + 1] = pm_ptr[i] + k;
-    std::copy(uo_frame_.begin() + uo_ptr_[u], uo_frame_.begin() + uo_ptr_[u + 1], pm_frame.begin() + pm_ptr[i]);
-  }
-  std::vector<int64_t> fm_ptr(F_ + 1, 0);
-  for (int64_t o = 0; o < NO_; ++o) ++fm_ptr[pm_frame[o] + 1];
-  for (int f = 0; f < F_; ++f) fm_ptr[f + 1] += fm_ptr[f];
-  std::vector<int64_t> cursor(fm_ptr.begin(), fm_ptr.end() - (F_ >= 0 ? 1 : 0));
-  std::vector<int32_t> fm_point(NO_), pm2fm(NO_);
-  for (int i = 0; i < N_; ++i)
-    for (int64_t o = pm_ptr[i]; o < pm_ptr[i + 1]; ++o) {
-      const int64_t q = cursor[pm_frame[o]]++;
-      fm_point[q] = i;
-      pm2fm[o] = static_cast<int32_t>(q);
-    }
-  uo2q_.resize(NO_);
-  for (int u = 0; u < N_; ++u) {
-    const int i = iperm_[u];
-    for (int64_t j = 0; j < uo_ptr_[u + 1] - uo_ptr_[u]; ++j) uo2q_[uo_ptr_[u] + j] = pm2fm[pm_ptr[i] + j];
-  }
-
-  // ---- Schur chunk plan: points sorted by visibility window (first, last frame), chunks of
-  //      kChunk points; one work item per 64x64 upper tile-block of each chunk's window ----
-  std::vector<int32_t> chunk_pts;
-  std::vector<int4> sblocks;
-  {
-    constexpr int kChunk = 512;
-    std::vector<int32_t> order;
-    for (int i = 0; i < N_; ++i)
-      if (pm_ptr[i + 1] > pm_ptr[i]) order.push_back(i);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      const int fa = pm_frame[pm_ptr[a]], fb = pm_frame[pm_ptr[b]];
-      if (fa != fb) return fa < fb;
-      return pm_frame[pm_ptr[a + 1] - 1] < pm_frame[pm_ptr[b + 1] - 1];
-    });
-    chunk_pts = order;
-    for (size_t c0 = 0; c0 < order.size(); c0 += kChunk) {
-      const size_t c1 = std::min(order.size(), c0 + kChunk);
-      int fmin = F_, fmax = -1;
-      for (size_t i = c0; i < c1; ++i) {
-        fmin = std::min(fmin, pm_frame[pm_ptr[order[i]]]);
-        fmax = std::max(fmax, pm_frame[pm_ptr[order[i] + 1] - 1]);
-      }
-      const int W = fmax - fmin + 1;
-      const int nb = (6 * W + 63) / 64;
-      if (fmin > 0xffff || W > 0x7fff || nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
-      for (int rb = 0; rb < nb; ++rb)
-        for (int cb = rb; cb < nb; ++cb)
-          sblocks.push_back(make_int4(static_cast<int>(c0), static_cast<int>(c1), fmin | (W << 16), rb | (cb << 16)));
-    }
-  }
-
-  // ---- frame-major tiles ----
-  const int G = next_pow2(P_);
-  const int ops = 256 / G;
-  const int64_t steps = std::min<int64_t>(64, std::max<int64_t>(1, (NO_ + 148 * 8 * ops - 1) / (148 * 8 * ops)));
-  const int64_t T = ops * steps;
-  std::vector<int32_t> tile_frame, ftile_ptr(F_ + 1, 0);
-  std::vector<int64_t> tq0, tq1;
-  for (int f = 0; f < F_; ++f) {
-    for (int64_t q = fm_ptr[f]; q < fm_ptr[f + 1]; q += T) {
-      tile_frame.push_back(f);
-      tq0.push_back(q);
-      tq1.push_back(std::min(q + T, fm_ptr[f + 1]));
-    }
-    ftile_ptr[f + 1] = static_cast<int32_t>(tile_frame.size());
-  }
-  const int ntiles = static_cast<int>(tile_frame.size());
-
-  auto up = [&](auto& buf, const auto& vec) {
-    using T2 = std::remove_reference_t<decltype(*buf.p)>;
-    buf.alloc(std::max<size_t>(vec.size(), 1));
-    if (!vec.empty())
-      ck(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T2), cudaMemcpyHostToDevice, stream_), "upload");
-  };
-  up(pm_ptr_, pm_ptr);
-  up(pm_frame_, pm_frame);
-  up(pm2fm_, pm2fm);
-  up(fm_ptr_, fm_ptr);
-  fm_point.resize(NO_ + 8, 0);  // padding: 16-byte aligned TMA windows may read 3 past the end
-  up(fm_point_, fm_point);
-  fm_point.resize(NO_);
-  up(tile_frame_, tile_frame);
-  up(tile_q0_, tq0);
-  up(tile_q1_, tq1);
-  up(ftile_ptr_, ftile_ptr);
-  up(chunk_pts_, chunk_pts);
-  up(schur_blocks_, sblocks);
-  // pinned staging vectors must outlive the async copies
-  ck(cudaStreamSynchronize(stream_), "sync upload");
-
-  ov_.N = N_;
-  ov_.F = F_;
-  ov_.P = P_;
-  ov_.NO = NO_;
-  ov_.pm_ptr = pm_ptr_.p;
-  ov_.pm_frame = pm_frame_.p;
-  ov_.pm2fm = pm2fm_.p;
-  ov_.fm_ptr = fm_ptr_.p;
-  ov_.fm_point = fm_point_.p;
-  ov_.ntiles = ntiles;
-  ov_.tile_frame = tile_frame_.p;
-  ov_.tile_q0 = tile_q0_.p;
-  ov_.tile_q1 = tile_q1_.p;
-  ov_.ftile_ptr = ftile_ptr_.p;
-  schur_plan_ = SchurPlan{chunk_pts_.p, schur_blocks_.p, static_cast<int>(sblocks.size())};
-
-  // ---- points ----
-  std::vector<double2> anc(N_);
-  for (int i = 0; i < N_; ++i) anc[i] = make_double2(p->anchors_px[2 * perm_[i]], p->anchors_px[2 * perm_[i] + 1]);
-  up(anchor_, anc);
-  {  // frame-major per-observation anchors: k_obs reads them coalesced (no dependent gather)
-    std::vector<double2> afm(NO_);
-    for (int64_t q = 0; q < NO_; ++q) afm[q] = anc[fm_point[q]];
-    up(anchor_fm_, afm);
-    ck(cudaStreamSynchronize(stream_), "sync upload");
-  }
-
-  // template feasibility (solver.cpp:40-45): every template pixel inside [1, W-3] x [1, H-3]
-  template_ok_ = true;
-  for (int n = 0; n < N_ && template_ok_; ++n)
-    for (int k = 0; k < P_; ++k) {
-      const double u = p->anchors_px[2 * n] + static_cast<double>(pat_.dx[k]);
-      const double v = p->anchors_px[2 * n + 1] + static_cast<double>(pat_.dy[k]);
-      if (!(u >= 1.0 && u <= p->ref.width - 3 && v >= 1.0 && v <= p->ref.height - 3)) {
-        template_ok_ = false;
-        break;
-      }
-    }
-  ck(cudaStreamSynchronize(stream_), "sync upload");
+  build_layout(p);
+  const int ntiles = ov_.ntiles;
 
   const size_t nN = std::max(N_, 1), nF = std::max(F_, 1), nO = std::max<int64_t>(NO_, 1);
   pose_state_.alloc(nF);
@@ -499,16 +299,9 @@ void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, d
   a.active_out = scratch_bits_.p;
   a.d_eval = d_state_.p;
   if (mask) {
-    std::vector<uint32_t> bits(NO_, 0);
-    for (int64_t ou = 0; ou < NO_; ++ou) {
-      uint32_t b = 0;
-      for (int k = 0; k < P_; ++k)
-        if (mask[ou * P_ + k]) b |= 1u << k;
-      bits[uo2q_[ou]] = b;
-    }
     DBuf<uint32_t> mb;
-    mb.alloc(std::max<int64_t>(NO_, 1));
-    if (NO_ > 0) ck(cudaMemcpyAsync(mb.p, bits.data(), NO_ * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_), "mask");
+    mb.alloc(std::max<int64_t>(NO_, 1) + 8);
+    mask_to_bits(mask, mb.p);
     a.mask_in = mb.p;
     if (residuals) {
       r_out_.alloc(std::max<int64_t>(NO_ * P_, 1));
@@ -538,18 +331,8 @@ void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, d
     out->num_active = static_cast<int64_t>(s.num_active);
     out->num_out_of_bounds = static_cast<int64_t>(s.num_oob);
   }
-  if (residuals) {
-    std::vector<double> r(NO_ * P_);
-    if (NO_ > 0) ck(cudaMemcpy(r.data(), r_out_.p, r.size() * sizeof(double), cudaMemcpyDeviceToHost), "r");
-    for (int64_t ou = 0; ou < NO_; ++ou)
-      for (int k = 0; k < P_; ++k) residuals[ou * P_ + k] = r[static_cast<int64_t>(uo2q_[ou]) * P_ + k];
-  }
-  if (active) {
-    std::vector<uint32_t> bits(NO_);
-    if (NO_ > 0) ck(cudaMemcpy(bits.data(), scratch_bits_.p, NO_ * sizeof(uint32_t), cudaMemcpyDeviceToHost), "bits");
-    for (int64_t ou = 0; ou < NO_; ++ou)
-      for (int k = 0; k < P_; ++k) active[ou * P_ + k] = (bits[uo2q_[ou]] >> k) & 1u;
-  }
+  if (residuals) rows_to_user(r_out_.p, P_, residuals);
+  if (active) bits_to_user(scratch_bits_.p, active);
 }
 
 // =====================================================================================

@@ -36,8 +36,18 @@ struct DBuf {
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
-  void alloc(size_t count);
-  void release();
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
   size_t bytes() const { return n * sizeof(T); }
 };
 
@@ -97,9 +107,6 @@ class Engine {
   std::vector<FrameD> frames_h_;
   std::vector<int32_t> perm_;    // internal point -> user point
   std::vector<int32_t> iperm_;   // user point -> internal point
-  std::vector<int64_t> uo_ptr_;  // user CSR
-  std::vector<int32_t> uo_frame_;
-  std::vector<int32_t> uo2q_;    // user obs -> frame-major obs q
   bool template_ok_ = true;
   std::vector<double> R_state_, t_state_;  // user order (host copy of the problem poses)
   ObsView ov_{};
@@ -110,6 +117,7 @@ class Engine {
   DBuf<double2> anchor_, anchor_fm_;
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
   DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
+  DBuf<int32_t> uo2q_d_;         // caller obs -> frame-major obs q
   DBuf<PoseD> pose_state_, pose_cur_, pose_cand_, pose0_;
   DBuf<double> d_state_, d_cur_, d_cand_, d0_;
   DBuf<uint32_t> mask_[2];        // IC sticky mask / candidate active bits
@@ -173,6 +181,12 @@ class Engine {
   void ev_end(int kid, cudaEvent_t a);
   void drain_profile();
 
+  // layout (engine_layout.cu)
+  void build_layout(const pba_problem* p);
+  void mask_to_bits(const uint8_t* mask_user, uint32_t* bits_d);
+  void bits_to_user(const uint32_t* bits_d, uint8_t* active_user);
+  void rows_to_user(const double* src_fm, int w, double* dst_user);
+  void rows_from_user(const double* src_user, int w, double* dst_fm);
   // helpers
   void check_template() const;
   void upload_poses(DBuf<PoseD>& dst, const double* R, const double* t);

@@ -109,12 +109,7 @@ void Engine::download_block_hessian(const DBuf<double>& H, const DBuf<double>& D
     for (int f = 0; f < F_; ++f) unpack21(&h[21 * f], pp + 36 * f);
   }
   if (dd) download_depths_user(D, dd);
-  if (pd) {
-    std::vector<double> b(6 * static_cast<size_t>(NO_));
-    if (NO_ > 0) ck(cudaMemcpy(b.data(), B.p, b.size() * sizeof(double), cudaMemcpyDeviceToHost), "B");
-    for (int64_t ou = 0; ou < NO_; ++ou)
-      std::memcpy(pd + 6 * ou, &b[6 * static_cast<size_t>(uo2q_[ou])], 6 * sizeof(double));
-  }
+  if (pd) rows_to_user(B.p, 6, pd);
 }
 
 // refresh_ic_hessian (solver.cpp:505-531): H from the frozen rows with fresh weights
@@ -255,11 +250,7 @@ void Engine::solve_block_hessian(const double* pp, const double* dd, const doubl
   }
   if (F_ > 0) ck(cudaMemcpy(H_[0].p, h21.data(), h21.size() * sizeof(double), cudaMemcpyHostToDevice), "H");
   upload_depths_user(D_[0], dd);
-  {
-    std::vector<double> b(6 * static_cast<size_t>(NO_));
-    for (int64_t ou = 0; ou < NO_; ++ou) std::memcpy(&b[6 * static_cast<size_t>(uo2q_[ou])], pd + 6 * ou, 48);
-    if (NO_ > 0) ck(cudaMemcpy(B_[0].p, b.data(), b.size() * sizeof(double), cudaMemcpyHostToDevice), "B");
-  }
+  rows_from_user(pd, 6, B_[0].p);
   if (F_ > 0) ck(cudaMemcpy(gf_[0].p, g, 6 * F_ * sizeof(double), cudaMemcpyHostToDevice), "g_f");
   upload_depths_user(gn_[0], g + 6 * F_);
   if (!factor_reduced(H_[0].p, B_[0].p, D_[0].p, lambda))

@@ -1,0 +1,38 @@
+"""Where does an end-to-end ic_solve spend its time (C4)?  Diagnostic only."""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_1704_06967_b200 import scenes, solver  # noqa: E402
+
+cfg = scenes.baseline_config(sys.argv[1] if len(sys.argv) > 1 else "C4")
+sc = scenes.make_scene(cfg, device="cuda")
+st = sc.state
+c = cfg.solver_config(threshold_px=0.0, max_iters=10)
+st_pin = st.copy()
+st_pin.ref = torch.from_numpy(np.ascontiguousarray(st.ref)).pin_memory().numpy()
+st_pin.targets = torch.from_numpy(np.ascontiguousarray(st.targets)).pin_memory().numpy()
+for rep in range(2):
+    t0 = time.perf_counter()
+    h = solver.Handle(st_pin, "gpu")
+    t1 = time.perf_counter()
+    h.ic_build(c)
+    t2 = time.perf_counter()
+    h.begin(True, None)
+    t3 = time.perf_counter()
+    n = 0
+    done = False
+    while not done:
+        _, done = h.iterate()
+        n += 1
+    t4 = time.perf_counter()
+    r = h.end(c)
+    t5 = time.perf_counter()
+    h.close()
+    t6 = time.perf_counter()
+    print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, ic_build {1e3*(t2-t1):.1f}, begin {1e3*(t3-t2):.1f}, "
+          f"{n} iters {1e3*(t4-t3):.1f}, end {1e3*(t5-t4):.1f}, destroy {1e3*(t6-t5):.1f}; warnings {len(h.warnings()) if h.h else 'n/a'}")

@@ -444,6 +444,8 @@ void Engine::ic_build(const pba_config* cfg) {
   launch_point(pa, stream_);
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, true);
+  Bpm_.alloc(6 * nO);
+  launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
   ic_.mcur = 0;

@@ -124,6 +124,7 @@ class Engine {
   DBuf<uint32_t> scratch_bits_;
   DBuf<double> J_;                // 7 planes, IC frozen rows
   DBuf<double> Bic_, Dic_, Hic_;  // IC frozen BlockHessian (solver.hpp:163)
+  DBuf<double> Bpm_;              // point-major copy of Bic_ for k_backsub
   DBuf<double> B_[2];             // frame-major pose-depth blocks (cur / cand)
   DBuf<double> D_[2];
   DBuf<double> H_[2];             // 21F

@@ -55,7 +55,8 @@ void need_built(bool built) {
 
 void Engine::backsub(bool ic, const double* B, const double* D, const double* g_n, double lambda,
                      const double* d_cur, double* d_cand, double* dx_out) {
-  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p};
+  BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p,
+                (ic && B == Bic_.p && Bpm_.p) ? Bpm_.p : nullptr};
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_backsub(a, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -129,6 +130,7 @@ void Engine::ic_refresh() {
   launch_point(pa, stream_);
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, false);
+  launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
 }
 
 // ---- FC pieces -------------------------------------------------------------------

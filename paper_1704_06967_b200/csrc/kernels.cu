@@ -76,7 +76,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // Shared-memory staging of one block step (OPS observations).
-constexpr int kStages = 3;
+#ifndef PBA_OBS_STAGES
+#define PBA_OBS_STAGES 2
+#endif
+constexpr int kStages = PBA_OBS_STAGES;
 constexpr int kJStage = 258;    // doubles per J plane per stage: OPS*G(<=256) + 2 alignment slack
 constexpr int kObsStage = 260;  // observation slots per stage: OPS (<=256) + 4 alignment slack
 struct StageSmem {
@@ -99,7 +102,7 @@ constexpr size_t obs_smem_bytes() {
 constexpr int NT_OBS = NT + 32;  // 8 consumer warps + 1 producer warp
 
 #ifndef PBA_OBS_MINB_IC
-#define PBA_OBS_MINB_IC 2
+#define PBA_OBS_MINB_IC 3
 #endif
 #ifndef PBA_OBS_MINB_OTHER
 #define PBA_OBS_MINB_OTHER 1
@@ -220,6 +223,10 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
       n = reinterpret_cast<const int32_t*>(tail + sizeof(double2) * kObsStage)[j + ioff];
       mbits = has_mask ? reinterpret_cast<const uint32_t*>(tail + (sizeof(double2) + sizeof(int32_t)) * kObsStage)[j + ioff]
                        : 0xffffffffu;
+#ifndef PBA_HOIST_J
+#define PBA_DEFER_J 1
+#endif
+#ifndef PBA_DEFER_J
       if constexpr (kLoadJ) {
         if (klive) {
           const int jj = j * P + k + static_cast<int>((qs * P) & 1);
@@ -228,9 +235,16 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
           for (int c = 0; c < 7; ++c) J[c] = sJ[c * kJStage + jj];
         }
       }
+#endif
     }
+#ifndef PBA_DEFER_J
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data now lives in registers
+#else
+    // J rows stay in shared memory until the residual is known (fewer live registers);
+    // the stage is released at the end of the step.
+    const double* sJrow = reinterpret_cast<const double*>(base) + (j * P + k + static_cast<int>((qs * P) & 1));
+#endif
     if (live) {
       dd.x = __ldg(&a.d_eval[n]);
       dd.y = want_upd ? __ldg(&a.d_old[n]) : dd.x;
@@ -313,12 +327,20 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
               dc = w * row[6] * row[6];
               gnc = row[6] * wr;
             } else if constexpr (MODE == OBS_IC) {
+#ifdef PBA_DEFER_J
+#pragma unroll
+              for (int c = 0; c < 7; ++c) J[c] = sJrow[c * kJStage];
+#endif
               // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
               const double wr = fabs(r) <= gam ? r : copysign(gam, r);
 #pragma unroll
               for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
               gnc = J[6] * wr;
             } else if constexpr (MODE == OBS_REFRESH) {
+#ifdef PBA_DEFER_J
+#pragma unroll
+              for (int c = 0; c < 7; ++c) J[c] = sJrow[c * kJStage];
+#endif
               const double w = huber_weight(r, gam);
               int h = 0;
 #pragma unroll
@@ -405,6 +427,10 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
       }
     }
+#ifdef PBA_DEFER_J
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+#endif
   }
 
   // ---- deterministic block reduction of the per-lane frame accumulators ----
@@ -516,8 +542,8 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
     double acc = 0.0;
     for (int64_t o = o0 + lane; o < o1; o += 32) {
       const int f = a.ov.pm_frame[o];
-      const int64_t q = a.ov.pm2fm[o];
-      const double* b = a.B + q * 6;
+      // frozen IC blocks have a point-major copy (coalesced); FC gathers the frame-major ones
+      const double* b = a.Bpm ? a.Bpm + o * 6 : a.B + static_cast<int64_t>(a.ov.pm2fm[o]) * 6;
       const double* x = a.xp + 6 * f;
       double dot = 0.0;
 #pragma unroll
@@ -553,6 +579,15 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
     double v = 0.0;
     for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
     a.partial[blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
+// Bpm[o] = B[pm2fm[o]] (point-major copy of the frozen IC pose-depth blocks)
+__global__ void k_b_to_pm(const ObsView ov, const double* __restrict__ B, double* __restrict__ Bpm) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ov.NO * 6;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = e / 6, c = e % 6;
+    Bpm[e] = B[static_cast<int64_t>(ov.pm2fm[o]) * 6 + c];
   }
 }
 
@@ -1220,6 +1255,13 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
     k_point<<<nb, NT, 0, s>>>(a);
     count_launches(1);
   }
+}
+
+void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s) {
+  if (ov.NO == 0) return;
+  const int g = static_cast<int>(std::min<int64_t>((ov.NO * 6 + 255) / 256, 148 * 32));
+  k_b_to_pm<<<g, 256, 0, s>>>(ov, B, Bpm);
+  count_launches(1);
 }
 
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s) {

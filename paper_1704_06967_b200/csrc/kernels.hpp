@@ -72,8 +72,10 @@ struct BacksubArgs {
   double* d_cand;         // N
   double* dx_out;         // N or null
   double* partial;        // nblocks * 4
+  const double* Bpm;      // NO*6 point-major copy of B, or null (gather through pm2fm)
 };
 int backsub_blocks(int N);
+void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s);
 void launch_backsub(const BacksubArgs& a, cudaStream_t s);
 
 // Point-major gather of the per-observation records.

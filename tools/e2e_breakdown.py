@@ -1,4 +1,4 @@
-"""Where does an end-to-end ic_solve spend its time (C4)?  Diagnostic only."""
+"""Where does an end-to-end ic_solve spend its time?  Diagnostic only."""
 import sys
 import time
 from pathlib import Path
@@ -16,23 +16,24 @@ c = cfg.solver_config(threshold_px=0.0, max_iters=10)
 st_pin = st.copy()
 st_pin.ref = torch.from_numpy(np.ascontiguousarray(st.ref)).pin_memory().numpy()
 st_pin.targets = torch.from_numpy(np.ascontiguousarray(st.targets)).pin_memory().numpy()
-for rep in range(2):
+for rep in range(3):
     t0 = time.perf_counter()
     h = solver.Handle(st_pin, "gpu")
     t1 = time.perf_counter()
-    h.ic_build(c)
+    h.begin(True, c)
     t2 = time.perf_counter()
-    h.begin(True, None)
-    t3 = time.perf_counter()
     n = 0
     done = False
     while not done:
         _, done = h.iterate()
         n += 1
-    t4 = time.perf_counter()
+    t3 = time.perf_counter()
     r = h.end(c)
-    t5 = time.perf_counter()
+    t4 = time.perf_counter()
     h.close()
+    t5 = time.perf_counter()
     t6 = time.perf_counter()
-    print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, ic_build {1e3*(t2-t1):.1f}, begin {1e3*(t3-t2):.1f}, "
-          f"{n} iters {1e3*(t4-t3):.1f}, end {1e3*(t5-t4):.1f}, destroy {1e3*(t6-t5):.1f}; warnings {len(h.warnings()) if h.h else 'n/a'}")
+    r2 = solver.ic_solve(st_pin, c)
+    t7 = time.perf_counter()
+    print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, build+first pass {1e3*(t2-t1):.1f}, {n} iters {1e3*(t3-t2):.1f}, "
+          f"end {1e3*(t4-t3):.1f}, destroy {1e3*(t5-t4):.1f} | ic_solve {1e3*(t7-t6):.1f} ms")

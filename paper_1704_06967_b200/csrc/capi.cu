@@ -23,6 +23,7 @@ template <typename Fn>
 int guarded(pba_handle* h, Fn&& fn) {
   if (!h || !h->e) return PBA_E_ARG;
   try {
+    h->e->bind();
     fn(*h->e);
     return PBA_OK;
   } catch (const PbaError& ex) {

@@ -11,9 +11,23 @@
 namespace pba_b200 {
 
 namespace {
-
+thread_local cudaStream_t t_alloc_stream = nullptr;
 
 }  // namespace
+
+cudaStream_t alloc_stream() { return t_alloc_stream; }
+void set_alloc_stream(cudaStream_t s) { t_alloc_stream = s; }
+void init_memory_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaMemPool_t pool;
+  ck(cudaDeviceGetDefaultMemPool(&pool, dev), "mempool");
+  uint64_t thr = ~uint64_t(0);
+  ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool threshold");
+  done = true;
+}
 
 // =====================================================================================
 // construction: upload the ProblemState (solver.hpp:33-43) into the device layout
@@ -35,6 +49,9 @@ Engine::Engine(const pba_problem* p) {
   if (F_ > 0 && (!p->targets || !p->pose_R || !p->pose_t)) throw PbaError(PBA_E_ARG, "missing frames");
   if (N_ > 0 && (!p->anchors_px || !p->inv_depths)) throw PbaError(PBA_E_ARG, "missing points");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  sh_.s = stream_;
+  init_memory_pool();
+  set_alloc_stream(stream_);
 
   // ---- images: one fp32 buffer, reference first ----
   std::vector<int64_t> off(F_ + 2, 0);
@@ -117,7 +134,7 @@ Engine::~Engine() {
   }
   if (status_h_) cudaFreeHost(status_h_);
   if (flags_h_) cudaFreeHost(flags_h_);
-  if (stream_) cudaStreamDestroy(stream_);
+  set_alloc_stream(stream_);  // members free stream-ordered; sh_ destroys the stream last
 }
 
 int64_t Engine::device_bytes() const {

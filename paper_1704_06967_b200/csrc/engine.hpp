@@ -28,10 +28,18 @@ inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw PbaError(PBA_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Device allocations are stream-ordered from the device's default memory pool, which is
+// configured to retain freed memory (release threshold = max): creating and destroying
+// handles for repeated solves then costs no cudaMalloc / cudaFree round trips.
+cudaStream_t alloc_stream();           // stream of the engine being constructed / used
+void set_alloc_stream(cudaStream_t s);
+void init_memory_pool();
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -40,11 +48,12 @@ struct DBuf {
     if (count == n && p) return;
     release();
     if (count == 0) return;
-    ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    s = alloc_stream();
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s), "cudaMallocAsync");
     n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
@@ -98,7 +107,20 @@ class Engine {
 
   std::string last_error;
 
+  // make this engine's stream the allocation stream of the calling thread (every C-ABI entry)
+  void bind() const { set_alloc_stream(stream_); }
+
  private:
+  // Declared first so it is destroyed last: device buffers free stream-ordered on it.
+  struct StreamHolder {
+    cudaStream_t s = nullptr;
+    ~StreamHolder() {
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    }
+  } sh_;
   // problem / layout
   int N_ = 0, F_ = 0, P_ = 0;
   int64_t NO_ = 0;

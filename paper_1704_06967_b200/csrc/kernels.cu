@@ -89,6 +89,41 @@ struct StageSmem {
   uint32_t msk[kObsStage];
 };
 
+// Butterfly reduce-scatter over the G lanes of an observation group: on entry each lane
+// holds NVP = S*G per-pixel contributions v[]; on exit lane r (group-relative) holds in
+// v[0..S) the group sums of the original entries [r*S, (r+1)*S).  log2(G) levels,
+// NVP/2 + NVP/4 + ... + S shuffles: ~2 per pixel instead of keeping NVP accumulators.
+template <int G, int NVP>
+__device__ __forceinline__ void group_reduce_scatter(double (&v)[NVP], int lane) {
+#pragma unroll
+  for (int o = G / 2, L = NVP; o > 0; o >>= 1, L >>= 1) {
+    const bool upper = (lane & o) != 0;
+    const int h = L / 2;
+#pragma unroll
+    for (int s = 0; s < NVP / 2; ++s) {
+      if (s < h) {
+        const double lo = v[s], hi = v[h + s];
+        const double recv = __shfl_xor_sync(0xffffffffu, upper ? lo : hi, o);
+        v[s] = (upper ? hi : lo) + recv;
+      }
+    }
+  }
+}
+
+// Sum a group-scattered accumulator (S slots per lane) over the groups of the warp and
+// store the warp totals of entries [0, NV) into dst[] (lanes r < G of the first group).
+template <int G, int S, int NV>
+__device__ __forceinline__ void warp_store_scattered(const double (&acc)[S], int lane, double* dst) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double v = acc[s];
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int c = lane * S + s;
+    if (lane < G && c < NV) dst[c] = v;
+  }
+}
+
 template <int MODE>
 constexpr bool obs_loads_J() {
   return MODE == OBS_IC || MODE == OBS_REFRESH;
@@ -105,7 +140,7 @@ constexpr int NT_OBS = NT + 32;  // 8 consumer warps + 1 producer warp
 #define PBA_OBS_MINB_IC 3
 #endif
 #ifndef PBA_OBS_MINB_OTHER
-#define PBA_OBS_MINB_OTHER 1
+#define PBA_OBS_MINB_OTHER 2
 #endif
 template <int MODE, int G>
 __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY) ? PBA_OBS_MINB_IC : PBA_OBS_MINB_OTHER)
@@ -199,10 +234,16 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   const bool klive = k < P;
   const double gam = a.gamma;
 
-  double gacc[6] = {0, 0, 0, 0, 0, 0};
-  double hacc[kHasH ? 21 : 1];
+  // per-frame sums, group-scattered: lane r of a group owns entries [r*S, (r+1)*S)
+  // IC keeps its 6 gradient sums per lane (cheaper than shuffling); H modes scatter all 27
+  constexpr int GS = kHasH ? G : 1;  // scatter width for the gradient sums
+  constexpr int SG = (6 + GS - 1) / GS, SH = (21 + G - 1) / G;
+  double gacc[SG];
+  double hacc[kHasH ? SH : 1];
 #pragma unroll
-  for (int i = 0; i < (kHasH ? 21 : 1); ++i) hacc[i] = 0.0;
+  for (int i = 0; i < SG; ++i) gacc[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < (kHasH ? SH : 1); ++i) hacc[i] = 0.0;
   double energy = 0.0, nact = 0.0, noob = 0.0, maxupd = 0.0;
 
   for (int s = 0; s < nsteps; ++s) {
@@ -254,6 +295,12 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
     bool keep = false;       // final mask bit (BUILD)
     double gnc = 0.0, dc = 0.0;
     double b6[6] = {0, 0, 0, 0, 0, 0};
+    double gv[SG * GS];                    // this pixel's J^T W r contribution (padded)
+    double hv[kHasH ? SH * G : 1];         // this pixel's J^T W J upper triangle (padded)
+#pragma unroll
+    for (int i = 0; i < SG * GS; ++i) gv[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < (kHasH ? SH * G : 1); ++i) hv[i] = 0.0;
     if (live) {
       // anchor reprojection update (solver.cpp:105-131): anchor = pattern offset 0
       if (want_upd && k == 0) {
@@ -320,9 +367,9 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
               for (int i2 = 0; i2 < 6; ++i2) {
                 const double wi = w * row[i2];
 #pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * row[j2];
                 b6[i2] = wi * row[6];
-                gacc[i2] += row[i2] * wr;
+                gv[i2] = row[i2] * wr;
               }
               dc = w * row[6] * row[6];
               gnc = row[6] * wr;
@@ -334,7 +381,7 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
               // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
               const double wr = fabs(r) <= gam ? r : copysign(gam, r);
 #pragma unroll
-              for (int c = 0; c < 6; ++c) gacc[c] += J[c] * wr;
+              for (int c = 0; c < 6; ++c) gv[c] = J[c] * wr;
               gnc = J[6] * wr;
             } else if constexpr (MODE == OBS_REFRESH) {
 #ifdef PBA_DEFER_J
@@ -347,7 +394,7 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
               for (int i2 = 0; i2 < 6; ++i2) {
                 const double wi = w * J[i2];
 #pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * J[j2];
+                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * J[j2];
                 b6[i2] = wi * J[6];
               }
               dc = w * J[6] * J[6];
@@ -397,7 +444,7 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
               for (int i2 = 0; i2 < 6; ++i2) {
                 const double wi = w * row[i2];
 #pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * row[j2];
                 b6[i2] = wi * row[6];
               }
               dc = w * row[6] * row[6];
@@ -407,6 +454,17 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
           for (int c = 0; c < 7; ++c) a.Jw[c * a.jstride + px] = row[c];
         }
       }
+    }
+    // per-frame sums: reduce-scatter this step's contributions over the group, accumulate
+    if constexpr (kHasG) {
+      if constexpr (GS > 1) group_reduce_scatter<GS, SG * GS>(gv, lane);
+#pragma unroll
+      for (int i = 0; i < SG; ++i) gacc[i] += gv[i];
+    }
+    if constexpr (kHasH) {
+      group_reduce_scatter<G, SH * G>(hv, lane);
+#pragma unroll
+      for (int i = 0; i < SH; ++i) hacc[i] += hv[i];
     }
     // per-observation records: reduce over the G lanes of the pattern
     if constexpr (kHasRec) {
@@ -438,14 +496,8 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
     v = warp_sum(v);
     if (lane == 0) red[warp][slot] = v;
   };
-  if constexpr (kHasG) {
-#pragma unroll
-    for (int i = 0; i < 6; ++i) put(PT_G + i, gacc[i]);
-  }
-  if constexpr (kHasH) {
-#pragma unroll
-    for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
-  }
+  if constexpr (kHasG) warp_store_scattered<GS, SG, 6>(gacc, lane, &red[warp][PT_G]);
+  if constexpr (kHasH) warp_store_scattered<G, SH, 21>(hacc, lane, &red[warp][PT_H]);
   put(PT_E, energy);
   put(PT_NACT, nact);
   put(PT_NOOB, noob);

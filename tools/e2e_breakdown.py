@@ -37,3 +37,22 @@ for rep in range(3):
     t7 = time.perf_counter()
     print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, build+first pass {1e3*(t2-t1):.1f}, {n} iters {1e3*(t3-t2):.1f}, "
           f"end {1e3*(t4-t3):.1f}, destroy {1e3*(t5-t4):.1f} | ic_solve {1e3*(t7-t6):.1f} ms")
+
+# per-iteration view with kernel times
+h = solver.Handle(st_pin, "gpu")
+h.set_profiling(True)
+t0 = time.perf_counter()
+h.begin(True, c)
+t1 = time.perf_counter()
+print("build+first pass %.1f ms" % (1e3 * (t1 - t0)), {k: round(v[1], 2) for k, v in h.kernel_times().items() if v[0]})
+h.set_profiling(True)
+done = False
+while not done:
+    t0 = time.perf_counter()
+    s, done = h.iterate()
+    t1 = time.perf_counter()
+    kt = h.kernel_times()
+    h.set_profiling(True)
+    print("iter %d %.2f ms acc=%d fact=%d E=%.6e maxupd=%.3g" % (s.iter, 1e3 * (t1 - t0), s.accepted, s.hessian_factorizations,
+                                                           s.energy, s.max_update_px),
+          {k: round(v[1], 2) for k, v in kt.items() if v[0]})

@@ -79,6 +79,8 @@ Engine::Engine(const pba_problem* p) {
 
   build_layout(p);
   const int ntiles = ov_.ntiles;
+  tval_.alloc(std::max<size_t>(static_cast<size_t>(N_) * P_, 1));
+  launch_template_values(N_, pat_, ref_, anchor_.p, tval_.p, stream_);
 
   const size_t nN = std::max(N_, 1), nF = std::max(F_, 1), nO = std::max<int64_t>(NO_, 1);
   pose_state_.alloc(nF);
@@ -278,6 +280,7 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.frames = frames_.p;
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
+  a.tval = tval_.p;
   a.jstride = jstride();
   a.gamma = gamma;
   a.partial = partial_.p;

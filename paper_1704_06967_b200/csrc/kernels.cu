@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
         const double pv = an.y + static_cast<double>(a.pat.dy[k]);
         const double x = (pu - rf.cx) * a.ref_ifx;
         const double y = (pv - rf.cy) * a.ref_ify;
-        const double tval = bilinear(rf.img, rf.W, pu, pv);
+        const double tval = __ldg(&a.tval[static_cast<int64_t>(n) * P + k]);  // template value (solver.cpp:49)
         double xn, yn, vx, vy, vz;
         double r = 0.0;
         if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
@@ -632,6 +632,18 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
     for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
     a.partial[blockIdx.x * 4 + threadIdx.x] = v;
   }
+}
+
+// Template values tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template,
+// solver.cpp:33-53): fixed for the whole solve, computed once per handle.
+__global__ void k_template_values(int N, PatternD pat, FrameD ref, const double2* __restrict__ anc,
+                                  double* __restrict__ tval) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= static_cast<int64_t>(N) * pat.P) return;
+  const int n = static_cast<int>(e / pat.P), k = static_cast<int>(e % pat.P);
+  const double pu = anc[n].x + static_cast<double>(pat.dx[k]);
+  const double pv = anc[n].y + static_cast<double>(pat.dy[k]);
+  tval[e] = bilinear(ref.img, ref.W, pu, pv);
 }
 
 // Bpm[o] = B[pm2fm[o]] (point-major copy of the frozen IC pose-depth blocks)
@@ -1307,6 +1319,14 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
     k_point<<<nb, NT, 0, s>>>(a);
     count_launches(1);
   }
+}
+
+void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const double2* anc, double* tval,
+                            cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(N) * pat.P;
+  if (n == 0) return;
+  k_template_values<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(N, pat, ref, anc, tval);
+  count_launches(1);
 }
 
 void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s) {

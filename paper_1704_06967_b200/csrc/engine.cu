@@ -271,6 +271,24 @@ int Engine::read_flag(int i) {
 }
 void Engine::clear_flags() { ck(cudaMemsetAsync(flags_.p, 0, 4 * sizeof(int), stream_), "memset flags"); }
 
+MaxUpdArgs Engine::maxupd_args(const PoseD* pose_old, const PoseD* pose_new, const double* d_old,
+                                const double* d_new) const {
+  MaxUpdArgs m{};
+  m.pose_cur = pose_old;
+  m.pose_cand = pose_new;
+  m.d_cur = d_old;
+  m.d_cand = d_new;
+  m.frames = frames_.p;
+  m.anchor_fm = anchor_fm_.p;
+  m.ref_cx = ref_.cx;
+  m.ref_cy = ref_.cy;
+  m.ref_ifx = 1.0 / ref_.fx;
+  m.ref_ify = 1.0 / ref_.fy;
+  m.dx0 = pat_.dx[0];
+  m.dy0 = pat_.dy[0];
+  return m;
+}
+
 ObsArgs Engine::obs_args(double gamma) const {
   ObsArgs a{};
   a.ov = ov_;
@@ -375,7 +393,8 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
-  launch_cf(ov_, Bic_.p, s_n_.p, partial_cf_.p, stream_);
+  const MaxUpdArgs mu = maxupd_args(pose_old, pose, d_old, d);
+  launch_cf(ov_, Bic_.p, s_n_.p, partial_cf_.p, stream_, pose_old ? &mu : nullptr);
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, partial_cf_.p, pose_old != nullptr, true, false, gf_[buf].p, rhs_[buf].p, nullptr, nullptr,
            true);
@@ -394,6 +413,10 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   const int n = 6 * F_;
   clear_flags();
   auto e = ev_begin(PBA_K_SCHUR);
+  if (schur_plan_.nblocks > 0 && !schur_plan_.dense) {  // dense chunk scratch, allocated on first use
+    schur_dense_.alloc(static_cast<size_t>(std::max<int64_t>(schur_dense_elems_, 1)));
+    schur_plan_.dense = schur_dense_.p;
+  }
   launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, stream_);
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);

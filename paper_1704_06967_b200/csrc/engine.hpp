@@ -159,7 +159,10 @@ class Engine {
   DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
   DBuf<int32_t> chunk_pts_;
-  DBuf<int4> schur_blocks_;
+  DBuf<int4> schur_blocks_, schur_chunks_;
+  DBuf<int64_t> schur_chunk_off_;
+  DBuf<double> schur_dense_;
+  int64_t schur_dense_elems_ = 0;
   SchurPlan schur_plan_{};
   DBuf<Status> status_;
   DBuf<int> flags_;
@@ -221,6 +224,7 @@ class Engine {
   int read_flag(int i);
   void clear_flags();
   ObsArgs obs_args(double gamma) const;
+  MaxUpdArgs maxupd_args(const PoseD* pose_old, const PoseD* pose_new, const double* d_old, const double* d_new) const;
   void finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
                 double* rhs, const double* g_f_in, double* H, bool status);
   // IC pieces

@@ -398,21 +398,38 @@ void Engine::build_layout(const pba_problem* p) {
       if (nchunks > 0)
         ck(cudaMemcpyAsync(w.data(), win.p, nchunks * sizeof(int2), cudaMemcpyDeviceToHost, s), "win");
       ck(cudaStreamSynchronize(s), "win sync");
+      std::vector<int4> chunks(nchunks);
+      std::vector<int64_t> off(nchunks);
+      int64_t total = 0;
       for (int c = 0; c < nchunks; ++c) {
         const int fmin = w[c].x, W = w[c].y - w[c].x + 1;
-        const int nb = (6 * W + 63) / 64;
-        if (fmin > 0xffff || W > 0x7fff || nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
+        const int LD = ((6 * W + 63) / 64) * 64;
+        const int nb = LD / 64;
+        if (nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
         const int c0 = c * kChunk, c1 = std::min(npts, c0 + kChunk);
+        chunks[c] = make_int4(c0, c1, fmin, LD);
+        off[c] = total;
+        total += static_cast<int64_t>(c1 - c0) * LD;
         for (int rb = 0; rb < nb; ++rb)
-          for (int cb = rb; cb < nb; ++cb) sblocks.push_back(make_int4(c0, c1, fmin | (W << 16), rb | (cb << 16)));
+          for (int cb = rb; cb < nb; ++cb) sblocks.push_back(make_int4(c, 0, 0, rb | (cb << 16)));
       }
+      schur_chunks_.alloc(std::max(nchunks, 1));
+      schur_chunk_off_.alloc(std::max(nchunks, 1));
+      if (nchunks > 0) {
+        ck(cudaMemcpyAsync(schur_chunks_.p, chunks.data(), nchunks * sizeof(int4), cudaMemcpyHostToDevice, s), "chunks");
+        ck(cudaMemcpyAsync(schur_chunk_off_.p, off.data(), nchunks * sizeof(int64_t), cudaMemcpyHostToDevice, s),
+           "chunk off");
+      }
+      schur_dense_elems_ = total;
+      ck(cudaStreamSynchronize(s), "chunks sync");
     }
     schur_blocks_.alloc(std::max<size_t>(sblocks.size(), 1));
     if (!sblocks.empty())
       ck(cudaMemcpyAsync(schur_blocks_.p, sblocks.data(), sblocks.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
          "blocks");
     ck(cudaStreamSynchronize(s), "plan sync");
-    schur_plan_ = SchurPlan{chunk_pts_.p, schur_blocks_.p, static_cast<int>(sblocks.size())};
+    schur_plan_ = SchurPlan{chunk_pts_.p, npts, schur_chunks_.p, schur_chunk_off_.p, nullptr, schur_blocks_.p,
+                            static_cast<int>(sblocks.size())};
   }
 
   ov_.N = N_;

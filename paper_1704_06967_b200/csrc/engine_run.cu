@@ -161,7 +161,8 @@ void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, 
   PointArgs pa{ov_, PT_FCH, rec_.p, gn_[buf].p, D_[buf].p, lambda_next, s_n_.p, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
-  launch_cf(ov_, B_[buf].p, s_n_.p, partial_cf_.p, stream_);
+  const MaxUpdArgs mu = maxupd_args(pose_old, pose, d_old, d);
+  launch_cf(ov_, B_[buf].p, s_n_.p, partial_cf_.p, stream_, pose_old ? &mu : nullptr);
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, partial_cf_.p, pose_old != nullptr, true, true, gf_[buf].p, rhs_[buf].p, nullptr, H_[buf].p,
            true);

@@ -155,10 +155,9 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   const int64_t q0 = a.ov.tile_q0[t];
   const int64_t q1 = a.ov.tile_q1[t];
   const int nsteps = static_cast<int>((q1 - q0 + OPS - 1) / OPS);
-  const bool want_upd = a.pose_old != nullptr;
   const bool has_mask = (MODE != OBS_BUILD) && a.mask_in != nullptr;
   // frame-uniform data in shared memory (one frame per tile): keeps registers for the pixel math
-  __shared__ PoseD s_pe, s_po, s_p0;
+  __shared__ PoseD s_pe, s_p0;
   __shared__ FrameD s_fr;
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -170,7 +169,6 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
-    if (want_upd) s_po = a.pose_old[f];
     if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -226,7 +224,6 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   // ---------------- consumer warps ----------------
   const FrameD& fr = s_fr;
   const PoseD& pe = s_pe;
-  const PoseD& po = s_po;
   const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
   const int k = threadIdx.x % G;
@@ -288,7 +285,6 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
 #endif
     if (live) {
       dd.x = __ldg(&a.d_eval[n]);
-      dd.y = want_upd ? __ldg(&a.d_old[n]) : dd.x;
     }
     const double dv = dd.x;  // depth at the evaluation parameters
     bool act = false;        // residual active at the evaluation parameters
@@ -302,21 +298,6 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
 #pragma unroll
     for (int i = 0; i < (kHasH ? SH * G : 1); ++i) hv[i] = 0.0;
     if (live) {
-      // anchor reprojection update (solver.cpp:105-131): anchor = pattern offset 0
-      if (want_upd && k == 0) {
-        const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
-        const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
-        double xo, yo, xn2, yn2, t0_, t1_, t2_;
-        const bool oka = warp_point(po, xa, ya, dd.y, xo, yo, t0_, t1_, t2_);
-        const bool okb = warp_point(pe, xa, ya, dv, xn2, yn2, t0_, t1_, t2_);
-        if (!oka || !okb) {
-          maxupd = INFINITY;
-        } else {
-          const double du = (fr.fx * xo + fr.cx) - (fr.fx * xn2 + fr.cx);
-          const double dvv = (fr.fy * yo + fr.cy) - (fr.fy * yn2 + fr.cy);
-          maxupd = fmax(maxupd, sqrt(du * du + dvv * dvv));
-        }
-      }
       if (klive && ((mbits >> k) & 1u)) {
         // template pixel (solver.cpp:42-49)
         const double pu = an.x + static_cast<double>(a.pat.dx[k]);
@@ -585,8 +566,8 @@ constexpr int kPointsPerWarp = 4;
 
 __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ double red[NT / 32][3];
-  double sum_d = 0.0, ninv = 0.0, nnf = 0.0;
+  __shared__ double red[NT / 32][4];
+  double sum_d = 0.0, ninv = 0.0, nnf = 0.0, mupd = 0.0;
   for (int i = 0; i < kPointsPerWarp; ++i) {
     const int n = (blockIdx.x * (NT / 32) + warp) * kPointsPerWarp + i;
     if (n >= a.ov.N) break;
@@ -621,15 +602,17 @@ __global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
       if (!isfinite(dx)) nnf += 1.0;
     }
   }
+  mupd = warp_max(mupd);
   if (lane == 0) {
     red[warp][0] = sum_d;
     red[warp][1] = ninv;
     red[warp][2] = nnf;
+    red[warp][3] = mupd;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 4) {
     double v = 0.0;
-    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < NT / 32; ++w) v = threadIdx.x == 3 ? fmax(v, red[w][3]) : v + red[w][threadIdx.x];
     a.partial[blockIdx.x * 4 + threadIdx.x] = v;
   }
 }
@@ -716,26 +699,59 @@ __global__ void __launch_bounds__(NT) k_point(const PointArgs a) {
 // k_cf: c_f partial per tile (solver.cpp:407-416 Schur right-hand-side term)
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_cf(const ObsView ov, const double* __restrict__ B,
-                                           const double* __restrict__ s_n, double* __restrict__ partial) {
+                                           const double* __restrict__ s_n, double* __restrict__ partial,
+                                           const MaxUpdArgs mu) {
   const int t = blockIdx.x;
   const int64_t q0 = ov.tile_q0[t], q1 = ov.tile_q1[t];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool want_upd = mu.pose_cand != nullptr;
+  // max_reprojection_update_px (solver.cpp:105-131): the tile's frame is uniform
+  __shared__ PoseD s_po, s_pn;
+  __shared__ FrameD s_fr;
+  if (want_upd && threadIdx.x == 0) {
+    const int f = ov.tile_frame[t];
+    s_po = mu.pose_cur[f];
+    s_pn = mu.pose_cand[f];
+    s_fr = mu.frames[f];
+  }
+  __syncthreads();
   double c[6] = {0, 0, 0, 0, 0, 0};
+  double mupd = 0.0;
   for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
-    const double s = __ldg(&s_n[ov.fm_point[q]]);
+    const int n = ov.fm_point[q];
+    const double s = __ldg(&s_n[n]);
 #pragma unroll
     for (int i = 0; i < 6; ++i) c[i] += B[q * 6 + i] * s;
+    if (want_upd) {
+      const double2 an = mu.anchor_fm[q];
+      const double xa = ((an.x + static_cast<double>(mu.dx0)) - mu.ref_cx) * mu.ref_ifx;
+      const double ya = ((an.y + static_cast<double>(mu.dy0)) - mu.ref_cy) * mu.ref_ify;
+      double xo, yo, xn2, yn2, t0_, t1_, t2_;
+      const bool oka = warp_point(s_po, xa, ya, __ldg(&mu.d_cur[n]), xo, yo, t0_, t1_, t2_);
+      const bool okb = warp_point(s_pn, xa, ya, __ldg(&mu.d_cand[n]), xn2, yn2, t0_, t1_, t2_);
+      if (!oka || !okb) {
+        mupd = INFINITY;
+      } else {
+        const double du = (s_fr.fx * xo + s_fr.cx) - (s_fr.fx * xn2 + s_fr.cx);
+        const double dv = (s_fr.fy * yo + s_fr.cy) - (s_fr.fy * yn2 + s_fr.cy);
+        mupd = fmax(mupd, sqrt(du * du + dv * dv));
+      }
+    }
   }
-  __shared__ double red[NT / 32][6];
+  __shared__ double red[NT / 32][7];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const double v = warp_sum(c[i]);
     if (lane == 0) red[warp][i] = v;
   }
+  {
+    const double v = warp_max(mupd);
+    if (lane == 0) red[warp][6] = v;
+  }
   __syncthreads();
-  if (threadIdx.x < 6) {
+  if (threadIdx.x < 7) {
     double v = 0.0;
-    for (int w = 0; w < NT / 32; ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < NT / 32; ++w) v = threadIdx.x == 6 ? fmax(v, red[w][6]) : v + red[w][threadIdx.x];
     partial[static_cast<int64_t>(t) * 8 + threadIdx.x] = v;
   }
 }
@@ -790,7 +806,7 @@ __global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
     case 0: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_E, 0, nt, lane, false) : 0.0; break;
     case 1: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NACT, 0, nt, lane, false) : 0.0; break;
     case 2: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NOOB, 0, nt, lane, false) : 0.0; break;
-    case 3: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_MAXUPD, 0, nt, lane, true) : 0.0; break;
+    case 3: v = a.partial_cf ? tile_sum(a.partial_cf, 8, 6, 0, nt, lane, true) : 0.0; break;
     case 4: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 0, 0, a.nbs, lane, false) : 0.0; break;
     case 5: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 1, 0, a.nbs, lane, false) : 0.0; break;
     case 6: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 2, 0, a.nbs, lane, false) : 0.0; break;
@@ -966,6 +982,7 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
 // Results enter S through the same deterministic fixed-point RED as k_schur_pts.
 constexpr int SCH_TB = 64;   // tile-block edge (window-local dimensions)
 constexpr int SCH_KB = 32;   // points staged per K sub-batch
+constexpr int SCH_CHUNK = 512;  // points per chunk (must match the host plan)
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -973,75 +990,124 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) k_schur_dense(const ObsView ov, const double* __restrict__ B,
-                                                     const double* __restrict__ D, double lambda,
-                                                     const int32_t* __restrict__ chunk_pts,
-                                                     const int4* __restrict__ blocks,
-                                                     const double* __restrict__ scale,
-                                                     unsigned long long* __restrict__ acc) {
-  // blocks[b] = {chunk point begin, chunk point end, fmin | (W << 16), rb | (cb << 16)}
+// Densify once per chunk: row p of chunk c = [b_n^T / sqrt(D_n + lambda)] over the chunk's
+// frame window (zero where the point does not observe a frame), LD_c = roundup(6 W_c, 64).
+__global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const double* __restrict__ B,
+                                                       const double* __restrict__ D, double lambda,
+                                                       const int32_t* __restrict__ chunk_pts, int npts,
+                                                       const int4* __restrict__ chunks,
+                                                       const int64_t* __restrict__ chunk_off, double* __restrict__ dense) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= npts) return;
+  const int c = warp / SCH_CHUNK;
+  const int4 ch = chunks[c];  // {begin, end, fmin, LD}
+  const int fmin = ch.z, LD = ch.w;
+  double* row = dense + chunk_off[c] + static_cast<int64_t>(warp - ch.x) * LD;
+  for (int d = lane; d < LD; d += 32) row[d] = 0.0;
+  __syncwarp();
+  const int n = chunk_pts[warp];
+  const double isq = 1.0 / sqrt(D[n] + lambda);
+  for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) {
+    const int lf = ov.pm_frame[o] - fmin;
+    const double* b = B + static_cast<int64_t>(ov.pm2fm[o]) * 6;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) row[6 * lf + i] = b[i] * isq;
+  }
+}
+
+// One 64x64 upper tile-block of a chunk's Gram matrix on DMMA; K-loop over the chunk's
+// points in sub-batches of SCH_KB, slices streamed from the dense rows (coalesced).
+__global__ void __launch_bounds__(256) k_schur_syrk(const ObsView ov, const int4* __restrict__ blocks,
+                                                    const int4* __restrict__ chunks,
+                                                    const int64_t* __restrict__ chunk_off,
+                                                    const double* __restrict__ dense, const double* __restrict__ scale,
+                                                    unsigned long long* __restrict__ acc) {
+  // blocks[b] = {chunk id, 0, 0, rb | cb << 16}
   const int4 blk = blocks[blockIdx.x];
-  const int p0 = blk.x, p1 = blk.y, fmin = blk.z & 0xffff, W = blk.z >> 16;
+  const int4 ch = chunks[blk.x];
+  const int p0 = ch.x, p1 = ch.y, fmin = ch.z, LD = ch.w;
   const int rb = blk.w & 0xffff, cb = blk.w >> 16;
-  const int dim = 6 * W;
   const int r0 = rb * SCH_TB, c0 = cb * SCH_TB;
   const bool diag = rb == cb;
+  const double* base = dense + chunk_off[blk.x];
   __shared__ double As[SCH_TB][SCH_KB + 1];
   __shared__ double Bs[SCH_TB][SCH_KB + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double accd[8][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) accd[i][0] = accd[i][1] = 0.0;
-  for (int pb = p0; pb < p1; pb += SCH_KB) {
+  // register prefetch of the next sub-batch overlaps its global (L2) loads with the DMMAs
+  constexpr int PPW = SCH_KB / 8;  // points per warp per sub-batch
+  double ra[PPW][2], rbv[PPW][2];
+  auto fetch = [&](int pb) {
     const int np = min(SCH_KB, p1 - pb);
-    for (int e = tid; e < SCH_TB * (SCH_KB + 1); e += 256) {
-      (&As[0][0])[e] = 0.0;
-      (&Bs[0][0])[e] = 0.0;
-    }
-    __syncthreads();
-    // densify: one warp per point, lanes over its observations
-    for (int pp = warp; pp < np; pp += 8) {
-      const int n = chunk_pts[pb + pp];
-      const double isq = 1.0 / sqrt(D[n] + lambda);
-      for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) {
-        const int lf = ov.pm_frame[o] - fmin;
-        const double* b = B + static_cast<int64_t>(ov.pm2fm[o]) * 6;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const int li = 6 * lf + i;
-          const double v = b[i] * isq;
-          if (li >= r0 && li < r0 + SCH_TB) As[li - r0][pp] = v;
-          if (li >= c0 && li < c0 + SCH_TB) Bs[li - c0][pp] = v;
-        }
+    for (int j = 0; j < PPW; ++j) {
+      const int pp = warp + 8 * j;
+      const bool live = pp < np;
+      const double* row = base + static_cast<int64_t>(pb - p0 + pp) * LD;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = lane + 32 * h;
+        ra[j][h] = live ? row[r0 + d] : 0.0;
+        rbv[j][h] = (live && !diag) ? row[c0 + d] : 0.0;
       }
     }
-    __syncthreads();
-    // C(64x64) += As * Bs^T; warp w owns tile row w, tile cols 0..7
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int j = 0; j < PPW; ++j) {
+      const int pp = warp + 8 * j;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = lane + 32 * h;
+        As[d][pp] = ra[j][h];
+        if (!diag) Bs[d][pp] = rbv[j][h];
+      }
+    }
+  };
+  if (p0 < p1) {
+    fetch(p0);
+    stash();
+  }
+  __syncthreads();
+  for (int pb = p0; pb < p1; pb += SCH_KB) {
+    const int np = min(SCH_KB, p1 - pb);
+    const bool more = pb + SCH_KB < p1;
+    if (more) fetch(pb + SCH_KB);
+    const double(*Bp)[SCH_KB + 1] = diag ? As : Bs;
     for (int k = 0; k < np; k += 4) {
       const double a = As[warp * 8 + (lane >> 2)][k + (lane & 3)];
 #pragma unroll
       for (int tc = 0; tc < 8; ++tc) {
-        const double b = Bs[tc * 8 + (lane >> 2)][k + (lane & 3)];
+        if (diag && tc < warp) continue;  // mirrored from the symmetric tile
+        const double b = Bp[tc * 8 + (lane >> 2)][k + (lane & 3)];
         dmma_8x8x4(accd[tc][0], accd[tc][1], a, b);
       }
     }
+    __syncthreads();
+    if (more) stash();
     __syncthreads();
   }
   // scatter into S (window-local -> global), fixed point
   const int ld = 6 * ov.F;
   const int gbase = 6 * fmin;
+  const int dim = LD;  // padded rows/cols are zero: their products vanish
 #pragma unroll
   for (int tc = 0; tc < 8; ++tc) {
+    if (diag && tc < warp) continue;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int lr = r0 + warp * 8 + (lane >> 2);
       const int lc = c0 + tc * 8 + (lane & 3) * 2 + i;
       if (lr >= dim || lc >= dim) continue;
       const int r = gbase + lr, c = gbase + lc;
+      if (r >= ld || c >= ld) continue;
       const long long qv = llrint(accd[tc][i] * scale[r] * scale[c]);
       if (qv == 0) continue;
       atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(qv));
-      if (!diag) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(qv));
+      // mirror: off-diagonal tile-blocks, and the strictly-upper tiles of diagonal tile-blocks
+      if (!diag || tc > warp) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(qv));
     }
   }
 }
@@ -1336,9 +1402,10 @@ void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_
   count_launches(1);
 }
 
-void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s) {
+void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf, cudaStream_t s,
+               const MaxUpdArgs* mu) {
   if (ov.ntiles > 0) {
-    k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf);
+    k_cf<<<ov.ntiles, NT, 0, s>>>(ov, B, s_n, partial_cf, mu ? *mu : MaxUpdArgs{});
     count_launches(1);
   }
 }
@@ -1378,8 +1445,10 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
   k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total);
   int launched = 2;
   if (plan && plan->nblocks > 0) {
-    k_schur_dense<<<plan->nblocks, 256, 0, s>>>(ov, B, D, lambda, plan->chunk_pts, plan->blocks, scale, acc);
-    ++launched;
+    k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, D, lambda, plan->chunk_pts, plan->npts,
+                                                                  plan->chunks, plan->chunk_off, plan->dense);
+    k_schur_syrk<<<plan->nblocks, 256, 0, s>>>(ov, plan->blocks, plan->chunks, plan->chunk_off, plan->dense, scale, acc);
+    launched += 2;
   } else {
     const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
     if (pb > 0) {

@@ -72,7 +72,7 @@ struct BacksubArgs {
   const double* d0;       // N (IC)
   double* d_cand;         // N
   double* dx_out;         // N or null
-  double* partial;        // nblocks * 4
+  double* partial;        // nblocks * 4: {sum d_cand, #invalid, #nonfinite, unused}
   const double* Bpm;      // NO*6 point-major copy of B, or null (gather through pm2fm)
 };
 int backsub_blocks(int N);
@@ -97,9 +97,22 @@ struct PointArgs {
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);
 
-// Frame-major  c_f = sum_n B_nf s_n  per tile.
+// max_reprojection_update_px (solver.cpp:105-131) between (pose_cur, d_cur) and
+// (pose_cand, d_cand) over every observed anchor, fused into k_cf (null pose_cand = skip).
+struct MaxUpdArgs {
+  const PoseD* pose_cur;
+  const PoseD* pose_cand;
+  const double* d_cur;
+  const double* d_cand;
+  const FrameD* frames;
+  const double2* anchor_fm;  // NO
+  double ref_cx, ref_cy, ref_ifx, ref_ify;
+  int dx0, dy0;              // pattern offset 0 (the anchor pixel)
+};
+
+// Frame-major  c_f = sum_n B_nf s_n  per tile (partial slots 0..5), max update (slot 6).
 void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* partial_cf,
-               cudaStream_t s);
+               cudaStream_t s, const MaxUpdArgs* mu = nullptr);
 
 // Reduction of tile partials.  Writes g_f (6F), rhs = -g_f + c_f (6F) when
 // partial_cf != null, H (21F upper) when want_h, and the scalar Status.
@@ -148,8 +161,12 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 // Chunk plan for the dense (DMMA) Schur path: points sorted by visibility window, cut into
 // chunks, one entry per 64x64 upper-triangle tile-block of each chunk's window Gram matrix.
 struct SchurPlan {
-  const int32_t* chunk_pts;  // N internal point ids in window order
-  const int4* blocks;        // {begin, end, fmin | W << 16, rb | cb << 16}
+  const int32_t* chunk_pts;  // internal point ids in window order (points with observations)
+  int npts;
+  const int4* chunks;        // per chunk {begin, end, fmin, LD = roundup(6 W, 64)}
+  const int64_t* chunk_off;  // per chunk offset (doubles) of its dense [points x LD] block
+  double* dense;             // densified scaled blocks (scratch)
+  const int4* blocks;        // per work item {chunk, 0, 0, rb | cb << 16}
   int nblocks;
 };
 // Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.

@@ -107,6 +107,9 @@ Engine::Engine(const pba_problem* p) {
   partial_.alloc(static_cast<size_t>(std::max(ntiles, 1)) * PT_STRIDE);
   partial_cf_.alloc(static_cast<size_t>(std::max(ntiles, 1)) * 8);
   partial_bs_.alloc(static_cast<size_t>(std::max(backsub_blocks(N_), 1)) * 4);
+  fscal_.alloc(4 * static_cast<size_t>(std::max(F_, 1)));
+  ticket_.alloc(4);
+  ck(cudaMemsetAsync(ticket_.p, 0, 4 * sizeof(unsigned int), ticket_.s), "ticket");
   partial_pt_.alloc(static_cast<size_t>(std::max(point_blocks(N_), 1)) * 2);
   partial_mr_.alloc(1024);
   S_.alloc(static_cast<size_t>(36) * nF * nF);
@@ -279,7 +282,7 @@ MaxUpdArgs Engine::maxupd_args(const PoseD* pose_old, const PoseD* pose_new, con
   m.d_cur = d_old;
   m.d_cand = d_new;
   m.frames = frames_.p;
-  m.anchor_fm = anchor_fm_.p;
+  m.anchor = anchor_.p;
   m.ref_cx = ref_.cx;
   m.ref_cy = ref_.cy;
   m.ref_ifx = 1.0 / ref_.fx;
@@ -322,6 +325,8 @@ void Engine::finalize(const double* partial, const double* partial_cf, bool bs, 
   f.g_f_in = g_f_in;
   f.H = H;
   f.status = status ? status_.p : nullptr;
+  f.fscal = fscal_.p;
+  f.ticket = ticket_.p + 1;
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_finalize(f, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -415,17 +420,18 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   auto e = ev_begin(PBA_K_SCHUR);
   if (schur_plan_.nblocks > 0 && !schur_plan_.dense) {  // dense chunk scratch, allocated on first use
     schur_dense_.alloc(static_cast<size_t>(std::max<int64_t>(schur_dense_elems_, 1)));
+    schur_wsort_.alloc(static_cast<size_t>(std::max(schur_plan_.npts, 1)));
     schur_plan_.dense = schur_dense_.p;
+    schur_plan_.wsort = schur_wsort_.p;
   }
-  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, stream_);
+  const bool densify = dense_B_ != B;  // the dense blocks depend on B only (not on D or lambda)
+  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_);
+  dense_B_ = B;
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);
-  launch_cholesky(S_.p, n, flags_.p, stream_);
+  launch_chol_inv(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, flags_.p, ticket_.p + 2, stream_);  // L, L^-1, L^-T
   ev_end(PBA_K_CHOLESKY, e);
   if (read_flag(0) != 0) return false;
-  e = ev_begin(PBA_K_CHOLESKY);
-  launch_tri_inverse(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, stream_);
-  ev_end(PBA_K_CHOLESKY, e);
   return true;
 }
 
@@ -479,6 +485,7 @@ void Engine::ic_build(const pba_config* cfg) {
   a.active_out = mask_[0].p;
   a.Jw = J_.p;
   a.B_out = Bic_.p;
+  dense_B_ = nullptr;  // the densified Schur blocks are stale
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_BUILD, a, stream_);
   ev_end(PBA_K_IC_BUILD, e);

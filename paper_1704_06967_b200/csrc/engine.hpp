@@ -156,12 +156,15 @@ class Engine {
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
+  DBuf<double> fscal_;            // per-frame scalar partials of k_finalize
+  DBuf<unsigned int> ticket_;     // grid tickets {k_backsub, k_finalize}, k_chol_inv barrier {count, generation}
   DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
   DBuf<int32_t> chunk_pts_;
   DBuf<int4> schur_blocks_, schur_chunks_;
   DBuf<int64_t> schur_chunk_off_;
-  DBuf<double> schur_dense_;
+  DBuf<double> schur_dense_, schur_wsort_;
+  const double* dense_B_ = nullptr;  // B whose blocks schur_dense_ holds (null = stale)
   int64_t schur_dense_elems_ = 0;
   SchurPlan schur_plan_{};
   DBuf<Status> status_;

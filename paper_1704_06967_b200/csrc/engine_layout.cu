@@ -428,7 +428,7 @@ void Engine::build_layout(const pba_problem* p) {
       ck(cudaMemcpyAsync(schur_blocks_.p, sblocks.data(), sblocks.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
          "blocks");
     ck(cudaStreamSynchronize(s), "plan sync");
-    schur_plan_ = SchurPlan{chunk_pts_.p, npts, schur_chunks_.p, schur_chunk_off_.p, nullptr, schur_blocks_.p,
+    schur_plan_ = SchurPlan{chunk_pts_.p, npts, schur_chunks_.p, schur_chunk_off_.p, nullptr, nullptr, schur_blocks_.p,
                             static_cast<int>(sblocks.size())};
   }
 

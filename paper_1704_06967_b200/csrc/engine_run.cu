@@ -57,6 +57,10 @@ void Engine::backsub(bool ic, const double* B, const double* D, const double* g_
                      const double* d_cur, double* d_cand, double* dx_out) {
   BacksubArgs a{ov_, ic ? 1 : 0, xp_.p, B, D, g_n, lambda, d_cur, d0_.p, d_cand, dx_out, partial_bs_.p,
                 (ic && B == Bic_.p && Bpm_.p) ? Bpm_.p : nullptr};
+  a.xp_smem = 6 * static_cast<size_t>(F_) * sizeof(double) <= 48 * 1024 ? 1 : 0;
+  a.ticket = ticket_.p;
+  a.gauge_scale = gauge_.p;
+  a.gauge_enabled = run_.cfg.normalize_depth_gauge ? 1 : 0;
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_backsub(a, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -122,6 +126,7 @@ void Engine::ic_refresh() {
   a.active_out = scratch_bits_.p;
   a.J = J_.p;
   a.B_out = Bic_.p;
+  dense_B_ = nullptr;
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_REFRESH, a, stream_);
   ev_end(PBA_K_IC_BUILD, e);
@@ -155,6 +160,7 @@ void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, 
   a.mask_in = nullptr;
   a.active_out = scratch_bits_.p;
   a.B_out = B_[buf].p;
+  dense_B_ = nullptr;
   auto e = ev_begin(PBA_K_OBS_PASS);
   launch_obs(OBS_FC, a, stream_);
   ev_end(PBA_K_OBS_PASS, e);
@@ -254,6 +260,7 @@ void Engine::solve_block_hessian(const double* pp, const double* dd, const doubl
   if (F_ > 0) ck(cudaMemcpy(H_[0].p, h21.data(), h21.size() * sizeof(double), cudaMemcpyHostToDevice), "H");
   upload_depths_user(D_[0], dd);
   rows_from_user(pd, 6, B_[0].p);
+  dense_B_ = nullptr;
   if (F_ > 0) ck(cudaMemcpy(gf_[0].p, g, 6 * F_ * sizeof(double), cudaMemcpyHostToDevice), "g_f");
   upload_depths_user(gn_[0], g + 6 * F_);
   if (!factor_reduced(H_[0].p, B_[0].p, D_[0].p, lambda))
@@ -384,8 +391,7 @@ bool Engine::grad_is_zero(int buf) {
 // normalize_depth_gauge of the candidate (solver.cpp:135-143), on the device, before the
 // candidate is evaluated (see k_gauge_mean); accepting is then a plain copy.
 void Engine::gauge_candidate() {
-  launch_gauge(N_, F_, partial_bs_.p, backsub_blocks(N_), run_.cfg.normalize_depth_gauge ? 1 : 0, gauge_.p,
-               d_cand_.p, pose_cand_.p, stream_);
+  launch_gauge(N_, F_, gauge_.p, d_cand_.p, pose_cand_.p, stream_);  // scale formed by k_backsub
 }
 
 void Engine::commit_candidate() {  // solver.cpp:611-620, 803-809

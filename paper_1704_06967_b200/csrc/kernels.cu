@@ -560,60 +560,185 @@ __global__ void k_pose_update(int ic, int F, const PoseD* __restrict__ cur, cons
 }
 
 // ---------------------------------------------------------------------------------
-// k_backsub: warp per point, lanes over the point's observations
+// Point-major reduction kernels (k_backsub, k_point).  A warp task is kPPW consecutive
+// internal points; their observations [pm_ptr[n0], pm_ptr[n0 + kPPW]) are contiguous in
+// point-major order, so the warp streams them flat (coalesced, kUnroll independent loads
+// in flight per lane) and keeps one register accumulator per point (the segment of an
+// observation is found from the kPPW - 1 inner boundaries).  Persistent grid of
+// reduce_blocks(N) blocks (a fixed function of N: the per-block partials and therefore
+// every reduction order are reproducible).
 // ---------------------------------------------------------------------------------
-constexpr int kPointsPerWarp = 4;
+constexpr int kPPW = 4;
+#ifndef PBA_BS_UNROLL
+#define PBA_BS_UNROLL 2
+#endif
+#ifndef PBA_BS_MINB
+#define PBA_BS_MINB 4
+#endif
+#ifndef PBA_PT_UNROLL
+#define PBA_PT_UNROLL 4
+#endif
+#ifndef PBA_PT_MINB
+#define PBA_PT_MINB 4
+#endif
+constexpr int kBsUnroll = PBA_BS_UNROLL, kBsMinB = PBA_BS_MINB;  // k_backsub: loads in flight per lane, blocks/SM
+constexpr int kPtUnroll = PBA_PT_UNROLL, kPtMinB = PBA_PT_MINB;  // k_point
 
-__global__ void __launch_bounds__(NT) k_backsub(const BacksubArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ double red[NT / 32][4];
-  double sum_d = 0.0, ninv = 0.0, nnf = 0.0, mupd = 0.0;
-  for (int i = 0; i < kPointsPerWarp; ++i) {
-    const int n = (blockIdx.x * (NT / 32) + warp) * kPointsPerWarp + i;
-    if (n >= a.ov.N) break;
-    const int64_t o0 = a.ov.pm_ptr[n], o1 = a.ov.pm_ptr[n + 1];
-    double acc = 0.0;
-    for (int64_t o = o0 + lane; o < o1; o += 32) {
-      const int f = a.ov.pm_frame[o];
-      // frozen IC blocks have a point-major copy (coalesced); FC gathers the frame-major ones
-      const double* b = a.Bpm ? a.Bpm + o * 6 : a.B + static_cast<int64_t>(a.ov.pm2fm[o]) * 6;
-      const double* x = a.xp + 6 * f;
-      double dot = 0.0;
+struct WarpTask {
+  int n0, np;              // first point, number of points (<= kPPW)
+  int64_t O0, Oe;          // observation range
+  int64_t b1, b2, b3;      // inner boundaries (points 1..3 start)
+};
+
+__device__ __forceinline__ WarpTask warp_task(const ObsView& ov, int task, int lane) {
+  WarpTask t;
+  t.n0 = task * kPPW;
+  t.np = min(kPPW, ov.N - t.n0);
+  const int64_t bj = ov.pm_ptr[t.n0 + min(lane, t.np)];
+  t.O0 = __shfl_sync(0xffffffffu, bj, 0);
+  t.b1 = __shfl_sync(0xffffffffu, bj, 1);
+  t.b2 = __shfl_sync(0xffffffffu, bj, 2);
+  t.b3 = __shfl_sync(0xffffffffu, bj, 3);
+  t.Oe = __shfl_sync(0xffffffffu, bj, kPPW);
+  return t;
+}
+
+__device__ __forceinline__ void seg_add(double (&acc)[kPPW], const WarpTask& t, int64_t o, double v) {
+  const int seg = (o >= t.b1) + (o >= t.b2) + (o >= t.b3);
 #pragma unroll
-      for (int c = 0; c < 6; ++c) dot += b[c] * x[c];
-      acc += dot;
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const double D = a.D[n] + a.lambda;
-      const double dx = (-a.g_n[n] - acc) / D;
-      const double dc = a.d_cur[n];
-      double dn;
-      if (a.ic) {
-        const double d0 = a.d0[n];
-        dn = ((d0 - dx) / d0) * dc;
-      } else {
-        dn = dc + dx;
-      }
-      a.d_cand[n] = dn;
-      if (a.dx_out) a.dx_out[n] = dx;
-      sum_d += dn;
-      if (dn <= 0.0) ninv += 1.0;
-      if (!isfinite(dx)) nnf += 1.0;
-    }
+  for (int p = 0; p < kPPW; ++p)
+    if (seg == p) acc[p] += v;
+}
+
+// lane p < kPPW receives the warp total of acc[p]
+__device__ __forceinline__ double seg_reduce(double (&acc)[kPPW], int lane) {
+  double mine = 0.0;
+#pragma unroll
+  for (int p = 0; p < kPPW; ++p) {
+    const double v = warp_sum(acc[p]);
+    if (lane == p) mine = v;
   }
-  mupd = warp_max(mupd);
-  if (lane == 0) {
-    red[warp][0] = sum_d;
-    red[warp][1] = ninv;
-    red[warp][2] = nnf;
-    red[warp][3] = mupd;
+  return mine;
+}
+
+// Block-level fixed-order reduction of NV per-thread values into partial[blockIdx.x * NV + i]
+// (slot NV-1 is a max when LAST_MAX).
+template <int NV, bool LAST_MAX>
+__device__ __forceinline__ void block_partial(double (&v)[NV], double* __restrict__ partial) {
+  __shared__ double red[NT / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const double x = (LAST_MAX && i == NV - 1) ? warp_max(v[i]) : warp_sum(v[i]);
+    if (lane == 0) red[warp][i] = x;
   }
   __syncthreads();
-  if (threadIdx.x < 4) {
+  if (threadIdx.x < NV) {
+    double x = 0.0;
+    for (int w = 0; w < NT / 32; ++w)
+      x = (LAST_MAX && threadIdx.x == NV - 1) ? fmax(x, red[w][threadIdx.x]) : x + red[w][threadIdx.x];
+    partial[blockIdx.x * NV + threadIdx.x] = x;
+  }
+}
+
+// Grid ticket: returns true in the last block to finish (after every block's partial is
+// visible); that block resets the counter for the next launch.
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) *ticket = 0u;
+  }
+  __syncthreads();
+  return s_last;
+}
+
+// k_backsub: dx_n = (-g_n - sum_f B_nf . xp_f) / (D_n + lambda) and the candidate depth
+// (solver.cpp:418-428, :553-560 / :747-750); the last block also forms the depth-gauge
+// scale of the candidate (mean of d_cand, normalize_depth_gauge solver.cpp:135-143).
+__global__ void __launch_bounds__(NT, kBsMinB) k_backsub(const BacksubArgs a) {
+  extern __shared__ double s_xp[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* __restrict__ xp = a.xp;
+  if (a.xp_smem) {
+    for (int i = threadIdx.x; i < 6 * a.ov.F; i += NT) s_xp[i] = a.xp[i];
+    __syncthreads();
+    xp = s_xp;
+  }
+  double st[3] = {0.0, 0.0, 0.0};  // sum d_cand, #invalid, #nonfinite
+  const int ntask = (a.ov.N + kPPW - 1) / kPPW;
+  for (int task = blockIdx.x * (NT / 32) + warp; task < ntask; task += gridDim.x * (NT / 32)) {
+    const WarpTask t = warp_task(a.ov, task, lane);
+    // per-point scalars, issued before the observation stream
+    const int np_ = lane < t.np ? t.n0 + lane : t.n0;
+    const double Dn = a.D[np_], gn = a.g_n[np_], dc = a.d_cur[np_];
+    const double d0n = a.ic ? a.d0[np_] : 0.0;
+    double acc[kPPW] = {0.0, 0.0, 0.0, 0.0};
+    if (a.Bpm) {  // frozen IC blocks: flat stream of the task's observations, 3 x 16 B per lane
+      const int ne = static_cast<int>(t.Oe - t.O0);
+      const int r1 = static_cast<int>(t.b1 - t.O0), r2 = static_cast<int>(t.b2 - t.O0),
+                r3 = static_cast<int>(t.b3 - t.O0);
+      const double2* __restrict__ bp = reinterpret_cast<const double2*>(a.Bpm) + 3 * t.O0;
+      const int32_t* __restrict__ fp = a.ov.pm_frame + t.O0;
+      for (int i0 = lane; i0 < ne; i0 += 32 * kBsUnroll) {
+        double2 bv[kBsUnroll][3];
+        int fr[kBsUnroll];
+#pragma unroll
+        for (int u = 0; u < kBsUnroll; ++u) {
+          const int i = i0 + 32 * u;
+          const bool ok = i < ne;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) bv[u][c] = ok ? __ldcs(bp + 3 * i + c) : make_double2(0.0, 0.0);
+          fr[u] = ok ? fp[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBsUnroll; ++u) {
+          const int i = i0 + 32 * u;
+          const double* x = xp + 6 * fr[u];
+          const double v = bv[u][0].x * x[0] + bv[u][0].y * x[1] + bv[u][1].x * x[2] + bv[u][1].y * x[3] +
+                           bv[u][2].x * x[4] + bv[u][2].y * x[5];
+          const int seg = (i >= r1) + (i >= r2) + (i >= r3);
+#pragma unroll
+          for (int p = 0; p < kPPW; ++p)
+            if (seg == p) acc[p] += v;
+        }
+      }
+    } else {  // FC: gather the frame-major blocks
+      for (int64_t o = t.O0 + lane; o < t.Oe; o += 32) {
+        const int f = a.ov.pm_frame[o];
+        const double* b = a.B + static_cast<int64_t>(a.ov.pm2fm[o]) * 6;
+        double dot = 0.0;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) dot += b[c] * xp[6 * f + c];
+        seg_add(acc, t, o, dot);
+      }
+    }
+    const double sum = seg_reduce(acc, lane);
+    if (lane < t.np) {
+      const int n = t.n0 + lane;
+      const double dx = (-gn - sum) / (Dn + a.lambda);
+      const double dn = a.ic ? ((d0n - dx) / d0n) * dc : dc + dx;
+      a.d_cand[n] = dn;
+      if (a.dx_out) a.dx_out[n] = dx;
+      st[0] += dn;
+      if (dn <= 0.0) st[1] += 1.0;
+      if (!isfinite(dx)) st[2] += 1.0;
+    }
+  }
+  double v4[4] = {st[0], st[1], st[2], 0.0};
+  block_partial<4, false>(v4, a.partial);
+  if (!last_block(a.ticket)) return;
+  if (warp == 0) {  // same fixed order as k_finalize's sum of slot 0
     double v = 0.0;
-    for (int w = 0; w < NT / 32; ++w) v = threadIdx.x == 3 ? fmax(v, red[w][3]) : v + red[w][threadIdx.x];
-    a.partial[blockIdx.x * 4 + threadIdx.x] = v;
+    for (int b = lane; b < gridDim.x; b += 32) v += __ldcg(a.partial + 4 * b);
+    v = warp_sum(v);
+    if (lane == 0) {
+      const double mean = v / static_cast<double>(a.ov.N);
+      *a.gauge_scale = (a.gauge_enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
+    }
   }
 }
 
@@ -639,60 +764,52 @@ __global__ void k_b_to_pm(const ObsView ov, const double* __restrict__ B, double
 }
 
 // ---------------------------------------------------------------------------------
-// k_point: warp per point gather of per-observation records
+// k_point: point-major gather of the per-observation records (flat warp tasks)
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_point(const PointArgs a) {
+__global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ double red[NT / 32];
   double g2 = 0.0;
-  for (int i = 0; i < kPointsPerWarp; ++i) {
-    const int n = (blockIdx.x * (NT / 32) + warp) * kPointsPerWarp + i;
-    if (n >= a.ov.N) break;
-    double gs = 0.0, ds = 0.0;
+  const int ntask = (a.ov.N + kPPW - 1) / kPPW;
+  for (int task = blockIdx.x * (NT / 32) + warp; task < ntask; task += gridDim.x * (NT / 32)) {
+    const WarpTask t = warp_task(a.ov, task, lane);
+    const int np_ = lane < t.np ? t.n0 + lane : t.n0;
+    double gs = 0.0, ds = 0.0, Dn = 0.0;
+    if (a.mode == PT_GRAD || a.mode == PT_RESCALE) Dn = a.D[np_];
+    if (a.mode == PT_RESCALE) gs = a.g_n[np_];
     if (a.mode != PT_RESCALE) {
-      const int64_t o0 = a.ov.pm_ptr[n], o1 = a.ov.pm_ptr[n + 1];
-      for (int64_t o = o0 + lane; o < o1; o += 32) {
-        const double2 rc = a.rec[a.ov.pm2fm[o]];
-        gs += rc.x;
-        ds += rc.y;
+      double ag[kPPW] = {0.0, 0.0, 0.0, 0.0}, ad[kPPW] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t o0 = t.O0 + lane; o0 < t.Oe; o0 += 32 * kPtUnroll) {
+        double2 rc[kPtUnroll];
+#pragma unroll
+        for (int u = 0; u < kPtUnroll; ++u) {
+          const int64_t o = o0 + 32 * u;
+          rc[u] = o < t.Oe ? a.rec[a.ov.pm2fm[o]] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kPtUnroll; ++u) {
+          const int64_t o = o0 + 32 * u;
+          seg_add(ag, t, o, rc[u].x);
+          seg_add(ad, t, o, rc[u].y);
+        }
       }
-      gs = warp_sum(gs);
-      ds = warp_sum(ds);
+      gs = seg_reduce(ag, lane);
+      ds = seg_reduce(ad, lane);
     }
-    if (lane == 0) {
-      double g = gs, D;
+    if (lane < t.np) {
+      const int n = t.n0 + lane;
+      double g = gs, D = Dn;
       switch (a.mode) {
-        case PT_GRAD:
-          a.g_n[n] = g;
-          D = a.D[n];
-          break;
-        case PT_FCH:
-          a.g_n[n] = g;
-          a.D[n] = ds;
-          D = ds;
-          break;
-        case PT_DONLY:
-          a.D[n] = ds;
-          D = ds;
-          g = 0.0;
-          break;
-        default:  // PT_RESCALE
-          g = a.g_n[n];
-          D = a.D[n];
-          break;
+        case PT_GRAD: a.g_n[n] = g; break;
+        case PT_FCH: a.g_n[n] = g; a.D[n] = ds; D = ds; break;
+        case PT_DONLY: a.D[n] = ds; D = ds; g = 0.0; break;
+        default: break;  // PT_RESCALE
       }
       if (a.s_n && a.mode != PT_DONLY) a.s_n[n] = g / (D + a.lambda);
       g2 += g * g;
     }
   }
-  if (lane == 0) red[warp] = g2;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double v = 0.0;
-    for (int w = 0; w < NT / 32; ++w) v += red[w];
-    a.partial[blockIdx.x * 2] = v;
-    a.partial[blockIdx.x * 2 + 1] = 0.0;
-  }
+  double v2[2] = {g2, 0.0};
+  block_partial<2, false>(v2, a.partial);
 }
 
 // ---------------------------------------------------------------------------------
@@ -717,13 +834,19 @@ __global__ void __launch_bounds__(NT) k_cf(const ObsView ov, const double* __res
   __syncthreads();
   double c[6] = {0, 0, 0, 0, 0, 0};
   double mupd = 0.0;
+  const double2* __restrict__ B2 = reinterpret_cast<const double2*>(B);
   for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
     const int n = ov.fm_point[q];
     const double s = __ldg(&s_n[n]);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) c[i] += B[q * 6 + i] * s;
+    const double2 b0 = __ldcs(B2 + 3 * q), b1 = __ldcs(B2 + 3 * q + 1), b2 = __ldcs(B2 + 3 * q + 2);
+    c[0] += b0.x * s;
+    c[1] += b0.y * s;
+    c[2] += b1.x * s;
+    c[3] += b1.y * s;
+    c[4] += b2.x * s;
+    c[5] += b2.y * s;
     if (want_upd) {
-      const double2 an = mu.anchor_fm[q];
+      const double2 an = __ldg(&mu.anchor[n]);
       const double xa = ((an.x + static_cast<double>(mu.dx0)) - mu.ref_cx) * mu.ref_ifx;
       const double ya = ((an.y + static_cast<double>(mu.dy0)) - mu.ref_cy) * mu.ref_ify;
       double xo, yo, xn2, yn2, t0_, t1_, t2_;
@@ -734,10 +857,11 @@ __global__ void __launch_bounds__(NT) k_cf(const ObsView ov, const double* __res
       } else {
         const double du = (s_fr.fx * xo + s_fr.cx) - (s_fr.fx * xn2 + s_fr.cx);
         const double dv = (s_fr.fy * yo + s_fr.cy) - (s_fr.fy * yn2 + s_fr.cy);
-        mupd = fmax(mupd, sqrt(du * du + dv * dv));
+        mupd = fmax(mupd, du * du + dv * dv);  // squared: sqrt is monotone, taken once per tile
       }
     }
   }
+  mupd = sqrt(mupd);
   __shared__ double red[NT / 32][7];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -775,17 +899,21 @@ __global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
   if (blockIdx.x < F) {
     const int f = blockIdx.x;
     const int t0 = a.ov.ftile_ptr[f], t1 = a.ov.ftile_ptr[f + 1];
-    __shared__ double vals[6 + 6 + 21];
-    // components: 0..5 g, 6..11 cf, 12..32 H
-    for (int c = warp; c < 33; c += NT / 32) {
+    __shared__ double vals[6 + 6 + 21 + 4];
+    // components: 0..5 g, 6..11 cf, 12..32 H, 33 energy, 34 #active, 35 #oob, 36 max update
+    for (int c = warp; c < 37; c += NT / 32) {
       double v = 0.0;
       if (c < 6) {
         v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_G + c, t0, t1, lane, false)
                       : (a.g_f_in ? a.g_f_in[6 * f + c] : 0.0);
       } else if (c < 12) {
         if (a.partial_cf) v = tile_sum(a.partial_cf, 8, c - 6, t0, t1, lane, false);
-      } else if (a.want_h && a.partial) {
-        v = tile_sum(a.partial, PT_STRIDE, PT_H + (c - 12), t0, t1, lane, false);
+      } else if (c < 33) {
+        if (a.want_h && a.partial) v = tile_sum(a.partial, PT_STRIDE, PT_H + (c - 12), t0, t1, lane, false);
+      } else if (c < 36) {
+        if (a.partial) v = tile_sum(a.partial, PT_STRIDE, PT_E + (c - 33), t0, t1, lane, false);
+      } else {
+        if (a.partial_cf) v = tile_sum(a.partial_cf, 8, 6, t0, t1, lane, true);
       }
       if (lane == 0) vals[c] = v;
     }
@@ -796,25 +924,31 @@ __global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
       if (a.rhs) a.rhs[6 * f + threadIdx.x] = -g + vals[6 + threadIdx.x];
     }
     if (a.want_h && a.H && threadIdx.x < 21) a.H[21 * f + threadIdx.x] = vals[12 + threadIdx.x];
-    return;
+    if (threadIdx.x < 4) a.fscal[4 * f + threadIdx.x] = vals[33 + threadIdx.x];
   }
-  // scalar block
+  // the last block to finish reduces the per-frame scalars and the point-kernel partials
+  if (!last_block(a.ticket) || !a.status) return;
   __shared__ double sc[8];
-  const int nt = a.ov.ntiles;
   double v = 0.0;
-  switch (warp) {
-    case 0: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_E, 0, nt, lane, false) : 0.0; break;
-    case 1: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NACT, 0, nt, lane, false) : 0.0; break;
-    case 2: v = a.partial ? tile_sum(a.partial, PT_STRIDE, PT_NOOB, 0, nt, lane, false) : 0.0; break;
-    case 3: v = a.partial_cf ? tile_sum(a.partial_cf, 8, 6, 0, nt, lane, true) : 0.0; break;
-    case 4: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 0, 0, a.nbs, lane, false) : 0.0; break;
-    case 5: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 1, 0, a.nbs, lane, false) : 0.0; break;
-    case 6: v = a.partial_bs ? tile_sum(a.partial_bs, 4, 2, 0, a.nbs, lane, false) : 0.0; break;
-    default: v = a.partial_pt ? tile_sum(a.partial_pt, 2, 0, 0, a.npt, lane, false) : 0.0; break;
+  if (warp < 4) {
+    const bool mx = warp == 3;
+    for (int f = lane; f < F; f += 32) {
+      const double x = __ldcg(a.fscal + 4 * f + warp);
+      v = mx ? fmax(v, x) : v + x;
+    }
+    v = mx ? warp_max(v) : warp_sum(v);
+  } else if (warp < 7) {
+    if (a.partial_bs) {
+      for (int b = lane; b < a.nbs; b += 32) v += a.partial_bs[4 * b + (warp - 4)];
+      v = warp_sum(v);
+    }
+  } else if (a.partial_pt) {
+    for (int b = lane; b < a.npt; b += 32) v += a.partial_pt[2 * b];
+    v = warp_sum(v);
   }
   if (lane == 0) sc[warp] = v;
   __syncthreads();
-  if (threadIdx.x == 0 && a.status) {
+  if (threadIdx.x == 0) {
     Status s;
     s.energy = sc[0];
     s.num_active = sc[1];
@@ -849,18 +983,6 @@ __global__ void k_commit(int N, int F, const double* __restrict__ d_cand, const 
 // the FC Jacobian/Hessian built in the same pass then sits in the normalized
 // parametrization exactly like the reference's next-iteration build (:688-724).
 // ---------------------------------------------------------------------------------
-__global__ void k_gauge_mean(const double* __restrict__ partial_bs, int nbs, int N, int enabled,
-                             double* __restrict__ scale) {
-  const int lane = threadIdx.x & 31;
-  double v = 0.0;
-  for (int b = lane; b < nbs; b += 32) v += partial_bs[b * 4];  // same fixed order as k_finalize
-  v = warp_sum(v);
-  if (threadIdx.x == 0) {
-    const double mean = v / static_cast<double>(N);
-    *scale = (enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
-  }
-}
-
 __global__ void k_gauge_apply(int N, int F, const double* __restrict__ scale, double* __restrict__ d,
                               PoseD* __restrict__ pose) {
   const double m = *scale;
@@ -930,9 +1052,12 @@ __device__ __forceinline__ int h21_index(int i, int j) {
 }
 
 __global__ void k_schur_scale(int F, const double* __restrict__ H21, double* __restrict__ scale,
-                              unsigned long long* __restrict__ acc, int64_t nacc) {
+                              unsigned long long* __restrict__ acc, int64_t nacc, const int32_t* __restrict__ chunk_pts,
+                              int npts, const double* __restrict__ D, double lambda, double* __restrict__ wsort) {
   const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   for (int64_t e = e0; e < nacc; e += static_cast<int64_t>(gridDim.x) * blockDim.x) acc[e] = 0ull;
+  for (int64_t p = e0; p < npts; p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    wsort[p] = 1.0 / (D[chunk_pts[p]] + lambda);  // Schur weight of the p-th window-sorted point
   if (e0 < 6 * F) {
     const int r = static_cast<int>(e0);
     const double h = H21[21 * (r / 6) + h21_index(r % 6, r % 6)];
@@ -965,11 +1090,11 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
       bool zb = true;
       for (int c = 0; c < 6; ++c) zb = zb && (Bb[c] == 0.0);
       if (zb) continue;
+      if (b == a && i > jj) continue;  // upper triangle only (k_schur_final mirrors)
       const int r = 6 * fa + i, c = 6 * fb + jj;
       const double v = Ba[i] * Bb[jj] / Dn;
       const long long q = llrint(v * scale[r] * scale[c]);
       atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(q));
-      if (b != a) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(q));
     }
   }
 }
@@ -981,7 +1106,6 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
 // K-looping over the chunk's points through shared memory.  8 warps x 8 DMMA 8x8 tiles.
 // Results enter S through the same deterministic fixed-point RED as k_schur_pts.
 constexpr int SCH_TB = 64;   // tile-block edge (window-local dimensions)
-constexpr int SCH_KB = 32;   // points staged per K sub-batch
 constexpr int SCH_CHUNK = 512;  // points per chunk (must match the host plan)
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -990,10 +1114,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// Densify once per chunk: row p of chunk c = [b_n^T / sqrt(D_n + lambda)] over the chunk's
+// Densify once per B (independent of D and lambda): row p of chunk c = b_n^T over the chunk's
 // frame window (zero where the point does not observe a frame), LD_c = roundup(6 W_c, 64).
 __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const double* __restrict__ B,
-                                                       const double* __restrict__ D, double lambda,
                                                        const int32_t* __restrict__ chunk_pts, int npts,
                                                        const int4* __restrict__ chunks,
                                                        const int64_t* __restrict__ chunk_off, double* __restrict__ dense) {
@@ -1006,22 +1129,44 @@ __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const d
   for (int d = lane; d < LD; d += 32) row[d] = 0.0;
   __syncwarp();
   const int n = chunk_pts[warp];
-  const double isq = 1.0 / sqrt(D[n] + lambda);
   for (int64_t o = ov.pm_ptr[n] + lane; o < ov.pm_ptr[n + 1]; o += 32) {
     const int lf = ov.pm_frame[o] - fmin;
     const double* b = B + static_cast<int64_t>(ov.pm2fm[o]) * 6;
 #pragma unroll
-    for (int i = 0; i < 6; ++i) row[6 * lf + i] = b[i] * isq;
+    for (int i = 0; i < 6; ++i) row[6 * lf + i] = b[i];
   }
 }
 
-// One 64x64 upper tile-block of a chunk's Gram matrix on DMMA; K-loop over the chunk's
-// points in sub-batches of SCH_KB, slices streamed from the dense rows (coalesced).
-__global__ void __launch_bounds__(256) k_schur_syrk(const ObsView ov, const int4* __restrict__ blocks,
-                                                    const int4* __restrict__ chunks,
-                                                    const int64_t* __restrict__ chunk_off,
-                                                    const double* __restrict__ dense, const double* __restrict__ scale,
-                                                    unsigned long long* __restrict__ acc) {
+// One 64x64 upper tile-block of a chunk's weighted Gram matrix  sum_p w_p a_p a_p^T  on DMMA.
+// 4 warps, each a 32x32 quadrant (4x4 DMMA 8x8 tiles, 32 fp64 accumulators per lane); the
+// K loop streams SY_KB points per stage into shared memory with cp.async (2 stages,
+// zero-filled past the chunk end); the weight w_p = 1/(D_n + lambda) scales the A fragment.
+constexpr int SY_KB = 32;      // points per stage
+constexpr int SY_LDS = 72;     // smem row stride (doubles): fragment loads are 2 wavefronts
+constexpr int SY_STAGES = 2;
+constexpr int SY_THREADS = 128;
+constexpr size_t SY_SMEM = static_cast<size_t>(SY_STAGES) * (2 * SY_KB * SY_LDS + SY_KB) * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, const int4* __restrict__ blocks,
+                                                           const int4* __restrict__ chunks,
+                                                           const int64_t* __restrict__ chunk_off,
+                                                           const double* __restrict__ dense,
+                                                           const double* __restrict__ wsort,
+                                                           const double* __restrict__ scale,
+                                                           unsigned long long* __restrict__ acc) {
+  extern __shared__ __align__(16) double sy_smem[];
   // blocks[b] = {chunk id, 0, 0, rb | cb << 16}
   const int4 blk = blocks[blockIdx.x];
   const int4 ch = chunks[blk.x];
@@ -1030,86 +1175,84 @@ __global__ void __launch_bounds__(256) k_schur_syrk(const ObsView ov, const int4
   const int r0 = rb * SCH_TB, c0 = cb * SCH_TB;
   const bool diag = rb == cb;
   const double* base = dense + chunk_off[blk.x];
-  __shared__ double As[SCH_TB][SCH_KB + 1];
-  __shared__ double Bs[SCH_TB][SCH_KB + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double accd[8][2];
+  const int wr = warp >> 1, wc = warp & 1;
+  const bool active = !(diag && wr > wc);  // strictly-lower quadrant of a diagonal block: mirrored
+  double* As = sy_smem;                                   // [stage][KB][LDS]
+  double* Bs = As + SY_STAGES * SY_KB * SY_LDS;           // [stage][KB][LDS]
+  double* Ws = Bs + SY_STAGES * SY_KB * SY_LDS;           // [stage][KB]
+  auto issue = [&](int stage, int pb) {
+    double* as = As + stage * SY_KB * SY_LDS;
+    double* bs = Bs + stage * SY_KB * SY_LDS;
+    // KB rows x 32 16-byte pieces for each of A and B
 #pragma unroll
-  for (int i = 0; i < 8; ++i) accd[i][0] = accd[i][1] = 0.0;
-  // register prefetch of the next sub-batch overlaps its global (L2) loads with the DMMAs
-  constexpr int PPW = SCH_KB / 8;  // points per warp per sub-batch
-  double ra[PPW][2], rbv[PPW][2];
-  auto fetch = [&](int pb) {
-    const int np = min(SCH_KB, p1 - pb);
-#pragma unroll
-    for (int j = 0; j < PPW; ++j) {
-      const int pp = warp + 8 * j;
-      const bool live = pp < np;
-      const double* row = base + static_cast<int64_t>(pb - p0 + pp) * LD;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int d = lane + 32 * h;
-        ra[j][h] = live ? row[r0 + d] : 0.0;
-        rbv[j][h] = (live && !diag) ? row[c0 + d] : 0.0;
-      }
+    for (int it = 0; it < (2 * SY_KB * 32) / SY_THREADS; ++it) {
+      const int idx = tid + it * SY_THREADS;
+      const int isb = idx >= SY_KB * 32;
+      const int j = idx - isb * SY_KB * 32;
+      const int pp = j >> 5, piece = j & 31;
+      const bool valid = pb + pp < p1;
+      const double* src = base + static_cast<int64_t>(valid ? pb - p0 + pp : 0) * LD + (isb ? c0 : r0) + 2 * piece;
+      cp_async16((isb ? bs : as) + pp * SY_LDS + 2 * piece, src, valid);
     }
+    if (tid < SY_KB) cp_async8(Ws + stage * SY_KB + tid, wsort + min(pb + tid, p1 - 1), pb + tid < p1);
+    cp_async_commit();
   };
-  auto stash = [&]() {
+  double accd[4][4][2];
 #pragma unroll
-    for (int j = 0; j < PPW; ++j) {
-      const int pp = warp + 8 * j;
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int d = lane + 32 * h;
-        As[d][pp] = ra[j][h];
-        if (!diag) Bs[d][pp] = rbv[j][h];
-      }
-    }
-  };
-  if (p0 < p1) {
-    fetch(p0);
-    stash();
-  }
-  __syncthreads();
-  for (int pb = p0; pb < p1; pb += SCH_KB) {
-    const int np = min(SCH_KB, p1 - pb);
-    const bool more = pb + SCH_KB < p1;
-    if (more) fetch(pb + SCH_KB);
-    const double(*Bp)[SCH_KB + 1] = diag ? As : Bs;
-    for (int k = 0; k < np; k += 4) {
-      const double a = As[warp * 8 + (lane >> 2)][k + (lane & 3)];
-#pragma unroll
-      for (int tc = 0; tc < 8; ++tc) {
-        if (diag && tc < warp) continue;  // mirrored from the symmetric tile
-        const double b = Bp[tc * 8 + (lane >> 2)][k + (lane & 3)];
-        dmma_8x8x4(accd[tc][0], accd[tc][1], a, b);
-      }
+    for (int j = 0; j < 4; ++j) accd[i][j][0] = accd[i][j][1] = 0.0;
+  const int nsb = (p1 - p0 + SY_KB - 1) / SY_KB;
+  if (nsb > 0) issue(0, p0);
+  for (int sb = 0; sb < nsb; ++sb) {
+    const int stage = sb & 1;
+    if (sb + 1 < nsb) {
+      issue(stage ^ 1, p0 + (sb + 1) * SY_KB);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (more) stash();
-    __syncthreads();
+    if (active) {
+      const double* as = As + stage * SY_KB * SY_LDS + wr * 32 + (lane >> 2);
+      const double* bs = Bs + stage * SY_KB * SY_LDS + wc * 32 + (lane >> 2);
+      const double* ws = Ws + stage * SY_KB;
+#pragma unroll
+      for (int kk = 0; kk < SY_KB; kk += 4) {
+        const int k = kk + (lane & 3);
+        const double w = ws[k];
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = as[k * SY_LDS + 8 * i] * w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = bs[k * SY_LDS + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(accd[i][j][0], accd[i][j][1], a[i], b[j]);
+      }
+    }
+    __syncthreads();  // the stage is overwritten by the next issue
   }
-  // scatter into S (window-local -> global), fixed point
+  if (!active) return;
+  // fold into the upper triangle of S (window-local -> global), fixed point
   const int ld = 6 * ov.F;
   const int gbase = 6 * fmin;
-  const int dim = LD;  // padded rows/cols are zero: their products vanish
 #pragma unroll
-  for (int tc = 0; tc < 8; ++tc) {
-    if (diag && tc < warp) continue;
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int lr = r0 + warp * 8 + (lane >> 2);
-      const int lc = c0 + tc * 8 + (lane & 3) * 2 + i;
-      if (lr >= dim || lc >= dim) continue;
-      const int r = gbase + lr, c = gbase + lc;
-      if (r >= ld || c >= ld) continue;
-      const long long qv = llrint(accd[tc][i] * scale[r] * scale[c]);
-      if (qv == 0) continue;
-      atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(qv));
-      // mirror: off-diagonal tile-blocks, and the strictly-upper tiles of diagonal tile-blocks
-      if (!diag || tc > warp) atomicAdd(&acc[static_cast<int64_t>(c) * ld + r], static_cast<unsigned long long>(qv));
-    }
-  }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lr = r0 + wr * 32 + 8 * i + (lane >> 2);
+        const int lc = c0 + wc * 32 + 8 * j + (lane & 3) * 2 + h;
+        if (lr > lc || lc >= LD) continue;  // padded rows/cols are zero
+        const int r = gbase + lr, c = gbase + lc;
+        if (c >= ld) continue;
+        const long long qv = llrint(accd[i][j][h] * scale[r] * scale[c]);
+        if (qv != 0) atomicAdd(&acc[static_cast<int64_t>(r) * ld + c], static_cast<unsigned long long>(qv));
+      }
 }
 
 __global__ void k_schur_final(int F, const double* __restrict__ H21, double lambda, const double* __restrict__ scale,
@@ -1121,7 +1264,8 @@ __global__ void k_schur_final(int F, const double* __restrict__ H21, double lamb
     const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
     double v = 0.0;
     if (r / 6 == c / 6) v = H21[21 * (r / 6) + h21_index(r % 6, c % 6)] + (r == c ? lambda : 0.0);
-    const double upd = static_cast<double>(static_cast<long long>(acc[e])) / (scale[r] * scale[c]);
+    const int64_t eu = r <= c ? e : static_cast<int64_t>(c) * n + r;  // upper-triangle accumulator
+    const double upd = static_cast<double>(static_cast<long long>(acc[eu])) / (scale[r] * scale[c]);
     S[e] = v - upd;
   }
 }
@@ -1312,6 +1456,243 @@ __global__ void __launch_bounds__(256) k_tri_inv_col(const double* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------------
+// k_chol_inv: the whole factorization in ONE persistent cooperative kernel.
+// Right-looking blocked Cholesky (NB = 32) of the lower triangle of S in place, fused with
+// the explicit inverse X = L^-1 (block rows X_k. = Dinv_k (I - sum_{m<k} L_km X_m.), the sum
+// accumulated right-looking in the not-yet-final block rows of X) and X^T.  Per block step k:
+//   phase A (all CTAs): panel L_ik = A_ik Dinv_k^T (i > k); X_kj = -Dinv_k R_kj (j < k), X_kk
+//   phase B (all CTAs): trailing A_ij -= L_ik L_jk^T (k < j <= i); R_ij += L_ik X_kj (j <= k);
+//                       CTA 0 updates A_{k+1,k+1} first and factors it (look-ahead) -> L, Dinv
+// with a software grid barrier between phases (co-residency from the cooperative launch).
+// Replaces ~3 launches per block column + the per-column inverse CTAs of the earlier path.
+// ---------------------------------------------------------------------------------
+constexpr int CI_THREADS = 256;
+
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int g = gen;
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicExch(&bar[1], g + 1u);
+    } else {
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+      } while (v == g);
+    }
+    gen = g + 1u;
+  }
+  __syncthreads();
+}
+
+struct CiSmem {
+  double a[NB][NB + 1];
+  double b[NB][NB + 1];
+  double d[NB][NB + 1];
+};
+
+// load a 32x32 block (rows r0.., cols c0..) of an n x n row-major matrix; out of range -> 0.
+// trans: t[c][r] = M[r0 + r][c0 + c]
+__device__ __forceinline__ void ci_load(double (*t)[NB + 1], const double* __restrict__ M, int n, int r0, int c0,
+                                        bool trans) {
+  for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
+    const int r = e / NB, c = e % NB;
+    const int gr = r0 + r, gc = c0 + c;
+    const double v = (gr < n && gc < n) ? __ldcg(M + static_cast<int64_t>(gr) * n + gc) : 0.0;
+    if (trans) t[c][r] = v; else t[r][c] = v;
+  }
+}
+// acc[q] (element e = tid + 256 q, r = e / 32, c = e % 32) = sum_p x[r][p] * y[p][c]
+__device__ __forceinline__ void ci_mm(const double (*x)[NB + 1], const double (*y)[NB + 1], double (&acc)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
+    double v = 0.0;
+#pragma unroll 8
+    for (int p = 0; p < NB; ++p) v += x[r][p] * y[p][c];
+    acc[q] = v;
+  }
+}
+__device__ __forceinline__ void ci_store(double* __restrict__ M, int n, int r0, int c0, const double (&acc)[4],
+                                         double sign, double* __restrict__ MT) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
+    const int gr = r0 + r, gc = c0 + c;
+    if (gr < n && gc < n) {
+      M[static_cast<int64_t>(gr) * n + gc] = sign * acc[q];
+      if (MT) MT[static_cast<int64_t>(gc) * n + gr] = sign * acc[q];
+    }
+  }
+}
+
+// Factor the diagonal block k in shared memory: L_kk into A, Dinv_k = L_kk^-1 into Dinv.
+__device__ void ci_diag(CiSmem& sm, double* __restrict__ A, int n, int k, double* __restrict__ Dinv, int* fail) {
+  const int k0 = k * NB, kb = min(NB, n - k0);
+  double (*a)[NB + 1] = sm.a;
+  for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
+    const int r = e / NB, c = e % NB;
+    a[r][c] = (r < kb && c < kb && c <= r) ? __ldcg(A + static_cast<int64_t>(k0 + r) * n + k0 + c)
+                                           : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < NB; ++j) {
+    if (threadIdx.x == 0) {
+      const double dj = a[j][j];
+      if (!(dj > 0.0) || !isfinite(dj)) {
+        *fail = 1;
+        a[j][j] = 1.0;
+      } else {
+        a[j][j] = sqrt(dj);
+      }
+    }
+    __syncthreads();
+    const double piv = a[j][j];
+    for (int r = j + 1 + threadIdx.x; r < NB; r += CI_THREADS) a[r][j] = a[r][j] / piv;
+    __syncthreads();
+    for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
+      const int r = e / NB, c = e % NB;
+      if (c > j && r >= c) a[r][c] -= a[r][j] * a[c][j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
+    const int r = e / NB, c = e % NB;
+    if (r < kb && c <= r) A[static_cast<int64_t>(k0 + r) * n + k0 + c] = a[r][c];
+  }
+  // Dinv_k: forward substitution, one column per thread
+  if (threadIdx.x < NB) {
+    const int c = threadIdx.x;
+    double x[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int p = 0; p < r; ++p) v -= a[r][p] * x[p];
+      x[r] = (r < c) ? 0.0 : v / a[r][r];
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) Dinv[(static_cast<int64_t>(k) * NB + r) * NB + c] = x[r];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(CI_THREADS) k_chol_inv(double* __restrict__ A, int n, double* __restrict__ X,
+                                                         double* __restrict__ XT, double* __restrict__ Dinv,
+                                                         int* __restrict__ fail, unsigned int* __restrict__ bar) {
+  __shared__ CiSmem sm;
+  unsigned int gen = 0;
+  if (threadIdx.x == 0) gen = *reinterpret_cast<volatile unsigned int*>(bar + 1);
+  const int nblk = (n + NB - 1) / NB;
+  const int G = gridDim.x, cta = blockIdx.x;
+  if (cta == 0) ci_diag(sm, A, n, 0, Dinv, fail);
+  grid_barrier(bar, gen);
+  for (int k = 0; k < nblk; ++k) {
+    const int k0 = k * NB;
+    // ---- phase A: panel + block row k of X ----
+    const int npanel = nblk - k - 1;
+    const int itemsA = npanel + k + 1;
+    bool dl = false;
+    for (int it = cta; it < itemsA; it += G) {
+      if (!dl) {  // Dinv_k^T (panel) -- loaded once per CTA and step
+        for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
+          const int r = e / NB, c = e % NB;
+          sm.d[r][c] = __ldcg(Dinv + (static_cast<int64_t>(k) * NB + r) * NB + c);
+        }
+        dl = true;
+      }
+      __syncthreads();
+      double acc[4];
+      if (it < npanel) {  // L_ik = A_ik Dinv_k^T
+        const int i0 = (k + 1 + it) * NB;
+        ci_load(sm.a, A, n, i0, k0, false);
+        for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) sm.b[e % NB][e / NB] = sm.d[e / NB][e % NB];
+        __syncthreads();
+        ci_mm(sm.a, sm.b, acc);
+        ci_store(A, n, i0, k0, acc, 1.0, nullptr);
+      } else {
+        const int j = it - npanel;  // 0..k
+        if (j == k) {               // X_kk = Dinv_k
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + q * CI_THREADS;
+            acc[q] = sm.d[e / NB][e % NB];
+          }
+          ci_store(X, n, k0, k0, acc, 1.0, XT);
+        } else {  // X_kj = -Dinv_k R_kj
+          ci_load(sm.b, X, n, k0, j * NB, false);
+          __syncthreads();
+          ci_mm(sm.d, sm.b, acc);
+          ci_store(X, n, k0, j * NB, acc, -1.0, XT);
+        }
+      }
+      __syncthreads();
+    }
+    grid_barrier(bar, gen);
+    if (k + 1 >= nblk) break;
+    // ---- phase B: trailing update of A, right-looking accumulation of R; look-ahead on CTA 0 ----
+    const int m = nblk - k - 1;                 // trailing block rows k+1 .. nblk-1
+    const int ntrail = m * (m + 1) / 2;         // tiles (i, j), k < j <= i
+    const int nr = m * (k + 1);                 // tiles (i, j), i > k, j <= k
+    const int items = ntrail + nr;
+    auto do_item = [&](int it) {
+      double acc[4];
+      if (it < ntrail) {
+        int t = it, ti = 0;
+        while (t > ti) {
+          t -= ti + 1;
+          ++ti;
+        }
+        const int i0 = (k + 1 + ti) * NB, j0 = (k + 1 + t) * NB;
+        ci_load(sm.a, A, n, i0, k0, false);     // L_ik
+        ci_load(sm.b, A, n, j0, k0, true);      // L_jk^T
+        __syncthreads();
+        ci_mm(sm.a, sm.b, acc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
+          const int gr = i0 + r, gc = j0 + c;
+          if (gr < n && gc < n && gc <= gr) A[static_cast<int64_t>(gr) * n + gc] -= acc[q];
+        }
+      } else {
+        const int u = it - ntrail;
+        const int ti = u / (k + 1), j = u % (k + 1);
+        const int i0 = (k + 1 + ti) * NB, j0 = j * NB;
+        ci_load(sm.a, A, n, i0, k0, false);     // L_ik
+        ci_load(sm.b, X, n, k0, j0, false);     // X_kj
+        __syncthreads();
+        ci_mm(sm.a, sm.b, acc);
+        const bool first = j == k;              // R_ij starts at step k = j
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
+          const int gr = i0 + r, gc = j0 + c;
+          if (gr < n && gc < n) {
+            double* dst = X + static_cast<int64_t>(gr) * n + gc;
+            *dst = first ? acc[q] : *dst + acc[q];
+          }
+        }
+      }
+      __syncthreads();
+    };
+    if (cta == 0) {
+      do_item(0);                               // tile (k+1, k+1)
+      ci_diag(sm, A, n, k + 1, Dinv, fail);     // look-ahead factorization of the next diagonal block
+    }
+    if (G > 1) {
+      for (int it = 1 + (cta + G - 1) % G; it < items; it += G - 1)
+        if (cta != 0) do_item(it);
+    } else {
+      for (int it = 1; it < items; ++it) do_item(it);
+    }
+    grid_barrier(bar, gen);
+  }
+}
+
 // y = M b for a triangular row-major M (lower: columns <= row; upper: columns >= row).
 __global__ void __launch_bounds__(256) k_tri_gemv(const double* __restrict__ M, int n, int lower,
                                                   const double* __restrict__ b, double* __restrict__ y,
@@ -1365,16 +1746,19 @@ void launch_pose_update(int ic, int F, const PoseD* cur, const PoseD* pose0, con
   count_launches(1);
 }
 
-int backsub_blocks(int N) {
-  const int per_block = (NT / 32) * kPointsPerWarp;
-  return (N + per_block - 1) / per_block;
+static int reduce_blocks(int N, int minb) {
+  const int ntask = (N + kPPW - 1) / kPPW;
+  const int nb = (ntask + NT / 32 - 1) / (NT / 32);
+  return std::max(1, std::min(nb, 148 * minb));
 }
-int point_blocks(int N) { return backsub_blocks(N); }
+int backsub_blocks(int N) { return reduce_blocks(N, kBsMinB); }
+int point_blocks(int N) { return reduce_blocks(N, kPtMinB); }
 
 void launch_backsub(const BacksubArgs& a, cudaStream_t s) {
   const int nb = backsub_blocks(a.ov.N);
   if (nb > 0) {
-    k_backsub<<<nb, NT, 0, s>>>(a);
+    const size_t smem = a.xp_smem ? 6 * static_cast<size_t>(a.ov.F) * sizeof(double) : 0;
+    k_backsub<<<nb, NT, smem, s>>>(a);
     count_launches(1);
   }
 }
@@ -1411,7 +1795,7 @@ void launch_cf(const ObsView& ov, const double* B, const double* s_n, double* pa
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
-  k_finalize<<<a.ov.F + 1, NT, 0, s>>>(a);
+  k_finalize<<<std::max(a.ov.F, 1), NT, 0, s>>>(a);
   count_launches(1);
 }
 
@@ -1422,12 +1806,11 @@ void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, d
   count_launches(1);
 }
 
-void launch_gauge(int N, int F, const double* partial_bs, int nbs, int enabled, double* scale, double* d,
-                  PoseD* pose, cudaStream_t s) {
-  k_gauge_mean<<<1, 32, 0, s>>>(partial_bs, nbs, N, enabled, scale);
+void launch_gauge(int N, int F, const double* scale, double* d, PoseD* pose, cudaStream_t s) {
   const int m = N > F ? N : F;
+  if (m == 0) return;
   k_gauge_apply<<<(m + 255) / 256, 256, 0, s>>>(N, F, scale, d, pose);
-  count_launches(2);
+  count_launches(1);
 }
 
 void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref, const double2* anchor, int dx0,
@@ -1438,17 +1821,28 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 }
 
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
-                  double* scale, unsigned long long* acc, const SchurPlan* plan, cudaStream_t s) {
+                  double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s) {
   const int n = 6 * ov.F;
   const int64_t total = static_cast<int64_t>(n) * n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
-  k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total);
+  const bool dense = plan && plan->nblocks > 0;
+  k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total, dense ? plan->chunk_pts : nullptr,
+                                       dense ? plan->npts : 0, D, lambda, dense ? plan->wsort : nullptr);
   int launched = 2;
-  if (plan && plan->nblocks > 0) {
-    k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, D, lambda, plan->chunk_pts, plan->npts,
-                                                                  plan->chunks, plan->chunk_off, plan->dense);
-    k_schur_syrk<<<plan->nblocks, 256, 0, s>>>(ov, plan->blocks, plan->chunks, plan->chunk_off, plan->dense, scale, acc);
-    launched += 2;
+  if (dense) {
+    if (densify) {
+      k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, plan->chunk_pts, plan->npts, plan->chunks,
+                                                                    plan->chunk_off, plan->dense);
+      ++launched;
+    }
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_schur_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SY_SMEM));
+      return true;
+    }();
+    (void)attr;
+    k_schur_syrk<<<plan->nblocks, SY_THREADS, SY_SMEM, s>>>(ov, plan->blocks, plan->chunks, plan->chunk_off,
+                                                            plan->dense, plan->wsort, scale, acc);
+    ++launched;
   } else {
     const int pb = (ov.N + (NT / 32) - 1) / (NT / 32);
     if (pb > 0) {
@@ -1481,6 +1875,30 @@ void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double*
   k_tri_diag_inv<<<nblk, 256, 0, s>>>(L, n, Dinv);
   k_tri_inv_col<<<nblk, 256, 0, s>>>(L, n, Dinv, X, XT);
   count_launches(2);
+}
+
+int chol_inv_grid() {
+  static int g = [] {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_inv, CI_THREADS, 0);
+    return std::max(1, sms * std::max(1, std::min(per, 1)));
+  }();
+  return g;
+}
+
+void launch_chol_inv(double* S, int n, double* Dinv, double* X, double* XT, int* fail, unsigned int* bar,
+                     cudaStream_t s) {
+  if (n == 0) return;
+  const int nblk = (n + NB - 1) / NB;
+  const int items = std::max(nblk * (nblk + 1) / 2, 1);
+  int grid = std::min(chol_inv_grid(), items);
+  void* args[] = {&S, &n, &X, &XT, &Dinv, &fail, &bar};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_chol_inv), dim3(grid),
+                                                    dim3(CI_THREADS), args, 0, s);
+  if (e != cudaSuccess) std::fprintf(stderr, "k_chol_inv launch: %s\n", cudaGetErrorString(e));
+  count_launches(1);
 }
 
 void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x, int* nonfinite,

@@ -74,6 +74,10 @@ struct BacksubArgs {
   double* dx_out;         // N or null
   double* partial;        // nblocks * 4: {sum d_cand, #invalid, #nonfinite, unused}
   const double* Bpm;      // NO*6 point-major copy of B, or null (gather through pm2fm)
+  int xp_smem;            // stage xp in shared memory (6F doubles <= 48 KB)
+  unsigned int* ticket;   // grid ticket (zero between launches)
+  double* gauge_scale;    // out: mean of d_cand (1 when disabled / not positive-finite)
+  int gauge_enabled;
 };
 int backsub_blocks(int N);
 // tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template, solver.cpp:33-53)
@@ -105,7 +109,7 @@ struct MaxUpdArgs {
   const double* d_cur;
   const double* d_cand;
   const FrameD* frames;
-  const double2* anchor_fm;  // NO
+  const double2* anchor;     // N: anchor pixel (internal point order, L2-resident)
   double ref_cx, ref_cy, ref_ifx, ref_ify;
   int dx0, dy0;              // pattern offset 0 (the anchor pixel)
 };
@@ -140,6 +144,8 @@ struct FinalizeArgs {
   const double* g_f_in;       // 6F: gradient when the obs partial is absent (rescale)
   double* H;                  // 21F or null
   Status* status;             // or null
+  double* fscal;              // F*4 scratch: per-frame {energy, #active, #oob, max update}
+  unsigned int* ticket;       // grid ticket (zero between launches)
 };
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 
@@ -147,9 +153,8 @@ void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 void launch_commit(int N, int F, const double* d_cand, const PoseD* pose_cand, double scale_d,
                    double scale_t, double* d_cur, PoseD* pose_cur, cudaStream_t s);
 
-// Depth-gauge normalization of a candidate from k_backsub's partial sums (solver.cpp:135-143).
-void launch_gauge(int N, int F, const double* partial_bs, int nbs, int enabled, double* scale, double* d,
-                  PoseD* pose, cudaStream_t s);
+// Depth-gauge normalization of a candidate with the scale formed by k_backsub (solver.cpp:135-143).
+void launch_gauge(int N, int F, const double* scale, double* d, PoseD* pose, cudaStream_t s);
 
 // Max reprojection update between two parameter sets (solver.cpp:105-131).
 void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& ref,
@@ -165,19 +170,27 @@ struct SchurPlan {
   int npts;
   const int4* chunks;        // per chunk {begin, end, fmin, LD = roundup(6 W, 64)}
   const int64_t* chunk_off;  // per chunk offset (doubles) of its dense [points x LD] block
-  double* dense;             // densified scaled blocks (scratch)
+  double* dense;             // densified blocks b_n (scratch; valid while B is unchanged)
+  double* wsort;             // npts: 1 / (D_n + lambda) of the window-sorted points (scratch)
   const int4* blocks;        // per work item {chunk, 0, 0, rb | cb << 16}
   int nblocks;
 };
 // Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.
 // plan == nullptr selects the per-point pair kernel.
+// densify = false reuses plan->dense from the previous call with the same B.
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D,
                   double lambda, double* S, double* scale, unsigned long long* acc, const SchurPlan* plan,
-                  cudaStream_t s);
+                  bool densify, cudaStream_t s);
 
 // In-place dense Cholesky (lower) of the n x n row-major S; *fail set on a
 // non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s);
+
+// Fused factorization (one cooperative launch): lower Cholesky of S in place, X = L^-1
+// (row-major lower), XT = X^T, Dinv = inverses of the 32x32 diagonal blocks; *fail set on a
+// non-positive / non-finite pivot.  bar: 2 zero-initialised grid-barrier words (reusable).
+void launch_chol_inv(double* S, int n, double* Dinv, double* X, double* XT, int* fail, unsigned int* bar,
+                     cudaStream_t s);
 
 // X = L^-1 (row-major lower) and XT = X^T, from the Cholesky factor in L (lower).
 // Dinv: ceil(n/32) * 32 * 32 scratch.

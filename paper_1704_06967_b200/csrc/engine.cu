@@ -414,16 +414,21 @@ void Engine::ic_rescale_rhs(int buf, double lambda) {
   finalize(nullptr, partial_cf_.p, false, false, false, nullptr, rhs_[buf].p, gf_[buf].p, nullptr, false);
 }
 
-bool Engine::factor_reduced(const double* H, const double* B, const double* D, double lambda) {
-  const int n = 6 * F_;
-  clear_flags();
-  auto e = ev_begin(PBA_K_SCHUR);
-  if (schur_plan_.nblocks > 0 && !schur_plan_.dense) {  // dense chunk scratch, allocated on first use
+// Dense Schur chunk scratch: allocated when a solver is built (not inside a timed factorization).
+void Engine::alloc_schur() {
+  if (schur_plan_.nblocks > 0 && !schur_plan_.dense) {
     schur_dense_.alloc(static_cast<size_t>(std::max<int64_t>(schur_dense_elems_, 1)));
     schur_wsort_.alloc(static_cast<size_t>(std::max(schur_plan_.npts, 1)));
     schur_plan_.dense = schur_dense_.p;
     schur_plan_.wsort = schur_wsort_.p;
   }
+}
+
+bool Engine::factor_reduced(const double* H, const double* B, const double* D, double lambda) {
+  const int n = 6 * F_;
+  clear_flags();
+  auto e = ev_begin(PBA_K_SCHUR);
+  alloc_schur();
   const bool densify = dense_B_ != B;  // the dense blocks depend on B only (not on D or lambda)
   launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_);
   dense_B_ = B;
@@ -495,6 +500,7 @@ void Engine::ic_build(const pba_config* cfg) {
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, true);
   Bpm_.alloc(6 * nO);
+  alloc_schur();
   launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275

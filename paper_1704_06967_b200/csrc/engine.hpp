@@ -234,6 +234,7 @@ class Engine {
   void ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
                double lambda, const PoseD* pose_old, const double* d_old);
   void ic_rescale_rhs(int buf, double lambda);
+  void alloc_schur();
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
   void ic_factorize_loop(double lambda);
   void ic_refresh();

@@ -146,6 +146,7 @@ void Engine::alloc_fc() {
     D_[b].alloc(std::max(N_, 1));
     H_[b].alloc(21 * std::max(F_, 1));
   }
+  alloc_schur();
 }
 
 // Residual pass + FC J^T W J / J^T W r build at (pose, d) (solver.cpp:63-103, 688-724)

@@ -502,6 +502,196 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// k_obs_lane: the Hessian-building passes (FC build at the candidate, IC build at p0) with
+// ONE LANE PER OBSERVATION looping over the P pattern pixels.  These passes are instruction
+// bound (fp64 Jacobian rows, 21 J^T W J products per pixel): keeping the per-observation
+// sums (B_nf, D, g_n, active bits) and the per-frame sums (J^T W J, J^T W r) in the lane's
+// registers removes every per-pixel shuffle reduction and the TMA pipeline of k_obs (whose
+// inputs here are only 24 bytes per observation).  Same formulas, same frame-major tiles.
+// ---------------------------------------------------------------------------------
+#ifndef PBA_LANE_MINB
+#define PBA_LANE_MINB 2
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
+  static_assert(MODE == OBS_FC || MODE == OBS_BUILD, "lane kernel: H-building modes");
+  const int t = blockIdx.x;
+  const int f = a.ov.tile_frame[t];
+  const int64_t q0 = a.ov.tile_q0[t], q1 = a.ov.tile_q1[t];
+  __shared__ PoseD s_pe, s_p0;
+  __shared__ FrameD s_fr;
+  __shared__ double red[NT / 32][PT_STRIDE];
+  if (threadIdx.x == 0) {
+    s_fr = a.frames[f];
+    s_pe = a.pose_eval[f];
+    if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
+  }
+  __syncthreads();
+  const FrameD& fr = s_fr;
+  const PoseD& pe = s_pe;
+  const PoseD& p0 = s_p0;
+  const FrameD& rf = a.ref;
+  const int P = a.pat.P;
+  const double gam = a.gamma;
+  double hacc[21], gacc[6];
+#pragma unroll
+  for (int i = 0; i < 21; ++i) hacc[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) gacc[i] = 0.0;
+  double energy = 0.0, nact = 0.0, noob = 0.0;
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
+    const double2 an = a.anchor_fm[q];
+    const int n = a.ov.fm_point[q];
+    const double dv = __ldg(&a.d_eval[n]);
+    const double* tv = a.tval + static_cast<int64_t>(n) * P;
+    double b6[6] = {0, 0, 0, 0, 0, 0};
+    double dc = 0.0, gnc = 0.0;
+    uint32_t bits = 0u;
+    bool obs_ok = true;
+    if constexpr (MODE == OBS_BUILD) {
+      // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
+      const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
+      const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
+      const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + dv * p0.t[2];
+      obs_ok = (dv > 0.0) && !(vza < kDegenerateDepthEps);
+    }
+    for (int k = 0; k < P; ++k) {
+      // template pixel (solver.cpp:42-49)
+      const double pu = an.x + static_cast<double>(a.pat.dx[k]);
+      const double pv = an.y + static_cast<double>(a.pat.dy[k]);
+      const double x = (pu - rf.cx) * a.ref_ifx;
+      const double y = (pv - rf.cy) * a.ref_ify;
+      double row[7] = {0, 0, 0, 0, 0, 0, 0};
+      double xn, yn, vx, vy, vz, r = 0.0;
+      bool act = false;
+      if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
+        noob += 1.0;
+      } else {
+        const double u = fr.fx * xn + fr.cx;
+        const double v = fr.fy * yn + fr.cy;
+        if (!in_margin(u, v, fr.W, fr.H)) {
+          noob += 1.0;
+        } else {
+          r = __ldg(tv + k) - bilinear(fr.img, fr.W, u, v);
+          act = true;
+          energy += huber_loss(r, gam);
+          nact += 1.0;
+          if (a.r_out) a.r_out[q * P + k] = r;
+          if constexpr (MODE == OBS_FC) {
+            // image_gradient on the target at the warped point (image.cpp:36-49)
+            const double du = bilinear(fr.img, fr.W, u + 0.5, v) - bilinear(fr.img, fr.W, u - 0.5, v);
+            const double dvv = bilinear(fr.img, fr.W, u, v + 0.5) - bilinear(fr.img, fr.W, u, v - 0.5);
+            const double gx = du * fr.fx, gy = dvv * fr.fy;
+            // fc_warp_jacobian (geometry.cpp:129-139); row = -(grad^T J_img)
+            const double Rx0 = pe.R[0] * x + pe.R[1] * y + pe.R[2];
+            const double Rx1 = pe.R[3] * x + pe.R[4] * y + pe.R[5];
+            const double Rx2 = pe.R[6] * x + pe.R[7] * y + pe.R[8];
+            const double iz = 1.0 / vz;
+            const double P02 = -vx * iz * iz, P12 = -vy * iz * iz;
+            row[0] = -(gx * (P02 * Rx1) + gy * (iz * -Rx2 + P12 * Rx1));
+            row[1] = -(gx * (iz * Rx2 + P02 * -Rx0) + gy * (P12 * -Rx0));
+            row[2] = -(gx * (iz * -Rx1) + gy * (iz * Rx0));
+            row[3] = -(gx * (iz * dv));
+            row[4] = -(gy * (iz * dv));
+            row[5] = -(gx * (P02 * dv) + gy * (P12 * dv));
+            row[6] = -(gx * (iz * pe.t[0] + P02 * pe.t[2]) + gy * (iz * pe.t[1] + P12 * pe.t[2]));
+            const double w = huber_weight(r, gam);
+            const double wr = w * r;
+            int h = 0;
+#pragma unroll
+            for (int i2 = 0; i2 < 6; ++i2) {
+              const double wi = w * row[i2];
+#pragma unroll
+              for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+              b6[i2] += wi * row[6];
+              gacc[i2] += row[i2] * wr;
+            }
+            dc += w * row[6] * row[6];
+            gnc += row[6] * wr;
+            bits |= 1u << k;
+          }
+        }
+      }
+      if constexpr (MODE == OBS_BUILD) {
+        // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
+        bool keep = false;
+        if (act && obs_ok) {
+          // template gradient image_gradient(ref, x) (image.cpp:36-49)
+          const double gu = rf.fx * x + rf.cx, gvp = rf.fy * y + rf.cy;
+          const bool grad_ok = in_bounds_px(gu - 0.5, gvp, rf.W, rf.H) && in_bounds_px(gu + 0.5, gvp, rf.W, rf.H) &&
+                               in_bounds_px(gu, gvp - 0.5, rf.W, rf.H) && in_bounds_px(gu, gvp + 0.5, rf.W, rf.H);
+          const double R0x0 = p0.R[0] * x + p0.R[1] * y + p0.R[2];
+          const double R0x1 = p0.R[3] * x + p0.R[4] * y + p0.R[5];
+          const double R0x2 = p0.R[6] * x + p0.R[7] * y + p0.R[8];
+          const double vz0 = R0x2 + dv * p0.t[2];
+          if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
+            keep = true;
+            const double gxi = (bilinear(rf.img, rf.W, gu + 0.5, gvp) - bilinear(rf.img, rf.W, gu - 0.5, gvp)) * rf.fx;
+            const double gyi = (bilinear(rf.img, rf.W, gu, gvp + 0.5) - bilinear(rf.img, rf.W, gu, gvp - 0.5)) * rf.fy;
+            const double zbar0 = vz0 / dv;
+            const double g30 = gxi / zbar0, g31 = gyi / zbar0, g32 = -(gxi * x + gyi * y) / zbar0;
+            const double a0 = p0.R[0] * g30 + p0.R[1] * g31 + p0.R[2] * g32;
+            const double a1 = p0.R[3] * g30 + p0.R[4] * g31 + p0.R[5] * g32;
+            const double a2 = p0.R[6] * g30 + p0.R[7] * g31 + p0.R[8] * g32;
+            const double adt = a0 * p0.t[0] + a1 * p0.t[1] + a2 * p0.t[2];
+            const double m0 = zbar0 * a0, m1 = zbar0 * a1, m2 = zbar0 * a2 - adt;
+            row[0] = R0x1 * m2 - R0x2 * m1;
+            row[1] = R0x2 * m0 - R0x0 * m2;
+            row[2] = R0x0 * m1 - R0x1 * m0;
+            row[3] = dv * m0;
+            row[4] = dv * m1;
+            row[5] = dv * m2;
+            row[6] = m0 * p0.t[0] + m1 * p0.t[1] + m2 * p0.t[2];
+            const double w = huber_weight(r, gam);  // W0 (solver.cpp:279)
+            int h = 0;
+#pragma unroll
+            for (int i2 = 0; i2 < 6; ++i2) {
+              const double wi = w * row[i2];
+#pragma unroll
+              for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+              b6[i2] += wi * row[6];
+            }
+            dc += w * row[6] * row[6];
+          }
+        }
+        if (keep) bits |= 1u << k;
+        const int64_t px = q * P + k;
+#pragma unroll
+        for (int c = 0; c < 7; ++c) a.Jw[c * a.jstride + px] = row[c];
+      }
+    }
+    a.active_out[q] = bits;
+    a.rec[q] = make_double2(gnc, dc);
+#pragma unroll
+    for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+  }
+  // ---- deterministic block reduction of the per-lane frame accumulators ----
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto put = [&](int slot, double v) {
+    v = warp_sum(v);
+    if (lane == 0) red[warp][slot] = v;
+  };
+  if constexpr (MODE == OBS_FC) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) put(PT_G + i, gacc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
+  put(PT_E, energy);
+  put(PT_NACT, nact);
+  put(PT_NOOB, noob);
+  __syncthreads();
+  if (warp == 0) {
+    const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (MODE == OBS_FC && lane < 6) ||
+                      (lane >= PT_H && lane < PT_H + 21);
+    double v = 0.0;
+    if (used)
+      for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
+    a.partial[static_cast<int64_t>(t) * PT_STRIDE + lane] = v;
+  }
+}
+
 template <int MODE, int G>
 void launch_obs_g(const ObsArgs& a, cudaStream_t s) {
   constexpr size_t smem = obs_smem_bytes<MODE>();
@@ -1734,8 +1924,11 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
   switch (mode) {
     case OBS_ENERGY: launch_obs_mode<OBS_ENERGY>(a, G, s); break;
     case OBS_IC: launch_obs_mode<OBS_IC>(a, G, s); break;
-    case OBS_FC: launch_obs_mode<OBS_FC>(a, G, s); break;
-    case OBS_BUILD: launch_obs_mode<OBS_BUILD>(a, G, s); break;
+    case OBS_FC:
+      if (a.mask_in) launch_obs_mode<OBS_FC>(a, G, s);
+      else k_obs_lane<OBS_FC><<<a.ov.ntiles, NT, 0, s>>>(a);
+      break;
+    case OBS_BUILD: k_obs_lane<OBS_BUILD><<<a.ov.ntiles, NT, 0, s>>>(a); break;
     default: launch_obs_mode<OBS_REFRESH>(a, G, s); break;
   }
 }

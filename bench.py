@@ -266,13 +266,14 @@ def run_ours(args, rank, world):
     if not args.no_e2e:
         pin = {}
         # pinned host copies of the inputs (the user's buffers)
-        for name in ("ref", "targets"):
+        st_pin = st.copy()
+        for name in ("ref", "targets", "anchors_px", "inv_depths", "R", "t", "obs_ptr", "obs_frame"):
             a = getattr(st, name)
+            if a is None:
+                continue
             t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
             pin[name] = t
-        st_pin = st.copy()
-        st_pin.ref = pin["ref"].numpy()
-        st_pin.targets = pin["targets"].numpy()
+            setattr(st_pin, name, t.numpy())
         c2 = sc_cfg.solver_config(threshold_px=0.0, max_iters=args.e2e_iters, max_bad_steps=8)
         h2d = (st.ref.nbytes + st.targets.nbytes + st.anchors_px.nbytes + st.inv_depths.nbytes + st.R.nbytes
                + st.t.nbytes + (0 if st.obs_ptr is None else st.obs_ptr.nbytes + st.obs_frame.nbytes))

@@ -153,6 +153,9 @@ int pba_gpu_ic_hessian(pba_handle* h, double* pose_pose, double* depth_depth,
                        double* pose_depth, double* lambda);
 int pba_gpu_warning_count(const pba_handle* h);                   /* IcSolver::warnings() solver.hpp:130 */
 int pba_gpu_warning(const pba_handle* h, int i, char* buf, int len);
+/* All warnings at once, '\n'-separated and NUL-terminated (truncated to len - 1 bytes);
+   returns the full length excluding the NUL.  Bulk form of warnings() for large problems. */
+int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len);
 int pba_gpu_ic_run(pba_handle* h, const pba_config* cfg, pba_report* rep); /* IcSolver::run / ic_solve solver.cpp:481-654,845-847 */
 
 /* ---- FcSolver (solver.hpp:172-182) ------------------------------------------- */

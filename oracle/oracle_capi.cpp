@@ -281,6 +281,20 @@ int pba_oracle_warning_count(const pba_oracle_handle* h) {
   return h->ic ? static_cast<int>(h->ic->warnings().size()) : 0;
 }
 
+int64_t pba_oracle_warnings_text(const pba_oracle_handle* h, char* buf, int64_t len) {
+  std::string all;
+  if (h->ic)
+    for (const auto& w : h->ic->warnings()) {
+      if (!all.empty()) all += '\n';
+      all += w;
+    }
+  if (buf && len > 0) {
+    const size_t n = std::min<size_t>(all.size(), static_cast<size_t>(len - 1));
+    std::memcpy(buf, all.data(), n);
+    buf[n] = '\0';
+  }
+  return static_cast<int64_t>(all.size());
+}
 int pba_oracle_warning(const pba_oracle_handle* h, int i, char* buf, int len) {
   if (!h->ic || i < 0 || i >= static_cast<int>(h->ic->warnings().size())) return PBA_E_ARG;
   std::snprintf(buf, len, "%s", h->ic->warnings()[i].c_str());

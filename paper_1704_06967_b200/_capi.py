@@ -97,6 +97,7 @@ _COMMON = {
     "ic_hessian": (C.c_int, [VP, P(f64), P(f64), P(f64), P(f64)]),
     "warning_count": (C.c_int, [VP]),
     "warning": (C.c_int, [VP, C.c_int, C.c_char_p, C.c_int]),
+    "warnings_text": (C.c_int64, [VP, C.c_char_p, C.c_int64]),
     "ic_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),
     "fc_build": (C.c_int, [VP, f64, P(f64), P(f64), P(f64), P(f64)]),
     "fc_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),

@@ -120,6 +120,20 @@ int pba_gpu_ic_hessian(pba_handle* h, double* pp, double* dd, double* pd, double
 int pba_gpu_warning_count(const pba_handle* h) {
   return (h && h->e) ? static_cast<int>(h->e->warnings().size()) : 0;
 }
+int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len) {
+  if (!h || !h->e) return 0;
+  std::string all;
+  for (const auto& w : h->e->warnings()) {
+    if (!all.empty()) all += '\n';
+    all += w;
+  }
+  if (buf && len > 0) {
+    const size_t n = std::min<size_t>(all.size(), static_cast<size_t>(len - 1));
+    std::memcpy(buf, all.data(), n);
+    buf[n] = '\0';
+  }
+  return static_cast<int64_t>(all.size());
+}
 int pba_gpu_warning(const pba_handle* h, int i, char* buf, int len) {
   if (!h || !h->e || i < 0 || i >= static_cast<int>(h->e->warnings().size()) || !buf || len <= 0) return PBA_E_ARG;
   std::snprintf(buf, len, "%s", h->e->warnings()[i].c_str());

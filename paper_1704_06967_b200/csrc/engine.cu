@@ -2,6 +2,9 @@
 // Control flow mirrors /root/reference/proj/src/solver.cpp line by line (cited);
 // every per-pixel / per-point / per-frame computation is a kernel in kernels.cu.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -9,6 +12,20 @@
 #include "engine.hpp"
 
 namespace pba_b200 {
+
+void trace_mark(cudaStream_t s, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("PBA_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  if (s) cudaStreamSynchronize(s);
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[pba trace] %-28s %8.2f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 
 namespace {
 thread_local cudaStream_t t_alloc_stream = nullptr;
@@ -61,12 +78,19 @@ Engine::Engine(const pba_problem* p) {
     if (!im.data || im.width < 4 || im.height < 4) throw PbaError(PBA_E_ARG, "bad target image");
     off[f + 2] = off[f + 1] + static_cast<int64_t>(im.width) * im.height;
   }
+  trace_mark(nullptr, "create: start");
   images_.alloc(off[F_ + 1]);
   ck(cudaMemcpyAsync(images_.p, p->ref.data, off[1] * sizeof(float), cudaMemcpyHostToDevice, stream_), "upload ref");
+  // target images go up on a second stream, overlapped with the layout build on stream_
+  cudaStream_t up = nullptr;
+  cudaEvent_t up_done = nullptr;
+  ck(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "upload stream");
+  ck(cudaEventCreateWithFlags(&up_done, cudaEventDisableTiming), "upload event");
   for (int f = 0; f < F_; ++f)
     ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
-                       cudaMemcpyHostToDevice, stream_),
+                       cudaMemcpyHostToDevice, up),
        "upload target");
+  ck(cudaEventRecord(up_done, up), "upload record");
   ref_ = FrameD{images_.p, p->ref.width, p->ref.height, p->ref.fx, p->ref.fy, p->ref.cx, p->ref.cy};
   frames_h_.resize(F_);
   for (int f = 0; f < F_; ++f) {
@@ -78,6 +102,7 @@ Engine::Engine(const pba_problem* p) {
     ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, stream_), "frames");
 
   build_layout(p);
+  trace_mark(stream_, "create: layout");
   const int ntiles = ov_.ntiles;
   tval_.alloc(std::max<size_t>(static_cast<size_t>(N_) * P_, 1));
   launch_template_values(N_, pat_, ref_, anchor_.p, tval_.p, stream_);
@@ -128,6 +153,13 @@ Engine::Engine(const pba_problem* p) {
   R_state_.assign(p->pose_R, p->pose_R + 9 * F_);
   t_state_.assign(p->pose_t, p->pose_t + 3 * F_);
   set_params(p->pose_R, p->pose_t, p->inv_depths);
+  trace_mark(stream_, "create: buffers+tval+params");
+  // the caller's image buffers are free once create returns: finish the upload here
+  ck(cudaStreamWaitEvent(stream_, up_done, 0), "upload wait");
+  ck(cudaEventSynchronize(up_done), "upload sync");
+  cudaEventDestroy(up_done);
+  cudaStreamDestroy(up);
+  trace_mark(stream_, "create: image upload tail");
 }
 
 Engine::~Engine() {
@@ -161,9 +193,11 @@ void Engine::upload_poses(DBuf<PoseD>& dst, const double* R, const double* t) {
   ck(cudaStreamSynchronize(stream_), "sync");
 }
 void Engine::upload_depths_user(DBuf<double>& dst, const double* d_user) {
-  std::vector<double> h(N_);
-  for (int i = 0; i < N_; ++i) h[i] = d_user[perm_[i]];
-  if (N_ > 0) ck(cudaMemcpyAsync(dst.p, h.data(), N_ * sizeof(double), cudaMemcpyHostToDevice, stream_), "depths");
+  if (N_ > 0) {  // user order -> internal order on the device
+    perm_tmp_.alloc(N_);
+    ck(cudaMemcpyAsync(perm_tmp_.p, d_user, N_ * sizeof(double), cudaMemcpyHostToDevice, stream_), "depths");
+    launch_permute(N_, perm_d_.p, perm_tmp_.p, dst.p, false, stream_);
+  }
   ck(cudaStreamSynchronize(stream_), "sync");
 }
 void Engine::download_poses(const DBuf<PoseD>& src, double* R, double* t) {
@@ -176,10 +210,12 @@ void Engine::download_poses(const DBuf<PoseD>& src, double* R, double* t) {
   }
 }
 void Engine::download_depths_user(const DBuf<double>& src, double* d_user) {
-  std::vector<double> h(N_);
-  if (N_ > 0) ck(cudaMemcpyAsync(h.data(), src.p, N_ * sizeof(double), cudaMemcpyDeviceToHost, stream_), "depths");
+  if (N_ > 0) {  // internal order -> user order on the device
+    perm_tmp_.alloc(N_);
+    launch_permute(N_, perm_d_.p, src.p, perm_tmp_.p, true, stream_);
+    ck(cudaMemcpyAsync(d_user, perm_tmp_.p, N_ * sizeof(double), cudaMemcpyDeviceToHost, stream_), "depths");
+  }
   ck(cudaStreamSynchronize(stream_), "sync");
-  for (int i = 0; i < N_; ++i) d_user[perm_[i]] = h[i];
 }
 
 void Engine::set_params(const double* R, const double* t, const double* d) {
@@ -414,6 +450,18 @@ void Engine::ic_rescale_rhs(int buf, double lambda) {
   finalize(nullptr, partial_cf_.p, false, false, false, nullptr, rhs_[buf].p, gf_[buf].p, nullptr, false);
 }
 
+// User indices (ascending) of the points with D_n == 0.
+std::vector<int32_t> Engine::zero_depth_points(const double* D) {
+  std::vector<int32_t> out;
+  if (N_ == 0) return out;
+  const int64_t cnt = launch_zero_d(N_, D, perm_d_.p, zero_idx_.p, stream_);
+  out.resize(static_cast<size_t>(cnt));
+  if (cnt > 0)
+    ck(cudaMemcpy(out.data(), zero_idx_.p, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost), "zero-D list");
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
 // Dense Schur chunk scratch: allocated when a solver is built (not inside a timed factorization).
 void Engine::alloc_schur() {
   if (schur_plan_.nblocks > 0 && !schur_plan_.dense) {
@@ -491,30 +539,34 @@ void Engine::ic_build(const pba_config* cfg) {
   a.Jw = J_.p;
   a.B_out = Bic_.p;
   dense_B_ = nullptr;  // the densified Schur blocks are stale
+  trace_mark(stream_, "ic_build: setup+alloc");
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_BUILD, a, stream_);
   ev_end(PBA_K_IC_BUILD, e);
+  trace_mark(stream_, "ic_build: build pass");
   PointArgs pa{ov_, PT_DONLY, rec_.p, nullptr, Dic_.p, 0.0, nullptr, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, true);
+  trace_mark(stream_, "ic_build: D pass");
   Bpm_.alloc(6 * nO);
   alloc_schur();
+  trace_mark(stream_, "ic_build: Bpm+schur alloc");
   launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
   ic_.mcur = 0;
-  {  // :359-364 zero depth Hessian warnings, in user point order
-    std::vector<double> D(N_);
-    if (N_ > 0) ck(cudaMemcpy(D.data(), Dic_.p, N_ * sizeof(double), cudaMemcpyDeviceToHost), "D");
-    for (int u = 0; u < N_; ++u)
-      if (D[iperm_[u]] == 0.0)
-        ic_.warnings.push_back("point " + std::to_string(u) + ": zero depth Hessian entry (unobservable depth)");
+  {  // :359-364 zero depth Hessian warnings, in user point order (compacted on the device)
+    const std::vector<int32_t> zu = zero_depth_points(Dic_.p);
+    for (const int32_t u : zu)
+      ic_.warnings.push_back("point " + std::to_string(u) + ": zero depth Hessian entry (unobservable depth)");
   }
   ic_.builds = 1;
+  trace_mark(stream_, "ic_build: D, B copy, warnings");
   ic_factorize_loop(ic_.lambda);
   ic_.built = true;
+  trace_mark(stream_, "ic_build: factorize");
 }
 
 // =====================================================================================

@@ -32,6 +32,8 @@ inline void ck(cudaError_t e, const char* what) {
 // configured to retain freed memory (release threshold = max): creating and destroying
 // handles for repeated solves then costs no cudaMalloc / cudaFree round trips.
 cudaStream_t alloc_stream();           // stream of the engine being constructed / used
+// Host-side phase tracer (env PBA_TRACE=1): synchronizes s and prints the ms since the last mark.
+void trace_mark(cudaStream_t s, const char* what);
 void set_alloc_stream(cudaStream_t s);
 void init_memory_pool();
 
@@ -141,6 +143,9 @@ class Engine {
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
   DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
   DBuf<int32_t> uo2q_d_;         // caller obs -> frame-major obs q
+  DBuf<int32_t> perm_d_;         // internal point -> user point (device copy)
+  DBuf<int32_t> zero_idx_;       // scratch: compacted user indices (+1 counter slot)
+  DBuf<double> perm_tmp_;        // scratch: per-point values in user order
   DBuf<PoseD> pose_state_, pose_cur_, pose_cand_, pose0_;
   DBuf<double> d_state_, d_cur_, d_cand_, d0_;
   DBuf<uint32_t> mask_[2];        // IC sticky mask / candidate active bits
@@ -235,6 +240,7 @@ class Engine {
                double lambda, const PoseD* pose_old, const double* d_old);
   void ic_rescale_rhs(int buf, double lambda);
   void alloc_schur();
+  std::vector<int32_t> zero_depth_points(const double* D);
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
   void ic_factorize_loop(double lambda);
   void ic_refresh();

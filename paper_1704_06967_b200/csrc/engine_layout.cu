@@ -244,6 +244,7 @@ void Engine::build_layout(const pba_problem* p) {
   }
   count_launches(1);
 
+  trace_mark(s, "layout: obs upload+validate");
   // ---- internal point order: Morton order of the anchor pixel (texture locality) ----
   DBuf<double2> anc_user;
   anc_user.alloc(std::max(N_, 1));
@@ -263,6 +264,7 @@ void Engine::build_layout(const pba_problem* p) {
     radix_sort_pairs(key.p, key_sorted.p, idx.p, perm_d.p, N_, 32, s);
   }
 
+  trace_mark(s, "layout: morton sort");
   // ---- point-major list ----
   DBuf<int64_t> cnt;
   cnt.alloc(static_cast<size_t>(N_) + 1);
@@ -288,6 +290,7 @@ void Engine::build_layout(const pba_problem* p) {
     count_launches(1);
   }
 
+  trace_mark(s, "layout: point-major list");
   // ---- frame-major list (stable radix sort of observations by frame) ----
   DBuf<int32_t> frames_sorted, iota_o, fm2pm;
   frames_sorted.alloc(nO);
@@ -311,6 +314,7 @@ void Engine::build_layout(const pba_problem* p) {
                                                uo2q_d_.p, anchor_fm_.p);
     count_launches(1);
   }
+  trace_mark(s, "layout: frame-major sort+scatter");
   fm_ptr_.alloc(static_cast<size_t>(F_) + 1);
   k_fm_ptr<<<(F_ + 1 + 255) / 256, 256, 0, s>>>(F_, NO_, frames_sorted.p, fm_ptr_.p);
   count_launches(1);
@@ -326,12 +330,16 @@ void Engine::build_layout(const pba_problem* p) {
     ck(cudaMemcpyAsync(perm_.data(), perm_d.p, N_ * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "perm");
     ck(cudaMemcpyAsync(iperm_.data(), iperm_d.p, N_ * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "iperm");
   }
+  perm_d_.alloc(std::max(N_, 1));
+  zero_idx_.alloc(static_cast<size_t>(N_) + 1);
+  if (N_ > 0) ck(cudaMemcpyAsync(perm_d_.p, perm_d.p, N_ * sizeof(int32_t), cudaMemcpyDeviceToDevice, s), "perm copy");
   ck(cudaStreamSynchronize(s), "layout sync");
   if (fl[0] & 1) throw PbaError(PBA_E_ARG, "obs_ptr must be non-decreasing");
   if (fl[0] & 2) throw PbaError(PBA_E_ARG, "obs_frame out of range");
   if (fl[0] & 4) throw PbaError(PBA_E_ARG, "obs_frame must be strictly increasing per point");
   template_ok_ = fl[1] == 0;
 
+  trace_mark(s, "layout: host results");
   // ---- frame-major tiles (a tile never crosses a frame) ----
   {
     const int G = [this] {
@@ -366,6 +374,7 @@ void Engine::build_layout(const pba_problem* p) {
     ck(cudaStreamSynchronize(s), "tiles sync");
   }
 
+  trace_mark(s, "layout: tiles");
   // ---- Schur chunk plan: points sorted by visibility window (first, last frame), chunks of
   //      kChunk points; one work item per 64x64 upper tile-block of each chunk's window ----
   {
@@ -432,6 +441,7 @@ void Engine::build_layout(const pba_problem* p) {
                             static_cast<int>(sblocks.size())};
   }
 
+  trace_mark(s, "layout: schur plan");
   ov_.N = N_;
   ov_.F = F_;
   ov_.P = P_;

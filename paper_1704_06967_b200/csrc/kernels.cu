@@ -2094,6 +2094,44 @@ void launch_chol_inv(double* S, int n, double* Dinv, double* X, double* XT, int*
   count_launches(1);
 }
 
+// internal <-> user point order: to_user ? dst[perm[i]] = src[i] : dst[i] = src[perm[i]]
+__global__ void k_permute(int N, const int32_t* __restrict__ perm, const double* __restrict__ src,
+                          double* __restrict__ dst, int to_user) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  if (to_user) dst[perm[i]] = src[i]; else dst[i] = src[perm[i]];
+}
+void launch_permute(int N, const int32_t* perm, const double* src, double* dst, bool to_user, cudaStream_t s) {
+  if (N == 0) return;
+  k_permute<<<(N + 255) / 256, 256, 0, s>>>(N, perm, src, dst, to_user ? 1 : 0);
+  count_launches(1);
+}
+
+// Compact the user indices of the points with D == 0 (order fixed afterwards on the host).
+__global__ void k_zero_d(int N, const double* __restrict__ D, const int32_t* __restrict__ perm,
+                         int32_t* __restrict__ out, unsigned int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool z = i < N && D[i] == 0.0;
+  const unsigned m = __ballot_sync(0xffffffffu, z);
+  if (m == 0u) return;
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(cnt, static_cast<unsigned>(__popc(m)));
+  base = __shfl_sync(m, base, __ffs(m) - 1);
+  if (z) out[base + __popc(m & ((1u << lane) - 1u))] = perm[i];
+}
+
+int64_t launch_zero_d(int N, const double* D, const int32_t* perm, int32_t* out, cudaStream_t s) {
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(out + N);
+  cudaMemsetAsync(cnt, 0, sizeof(unsigned int), s);
+  k_zero_d<<<(N + 255) / 256, 256, 0, s>>>(N, D, perm, out, cnt);
+  count_launches(1);
+  unsigned int h = 0;
+  cudaMemcpyAsync(&h, cnt, sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return static_cast<int64_t>(h);
+}
+
 void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x, int* nonfinite,
                      cudaStream_t s) {
   const int nb = (n + 7) / 8;

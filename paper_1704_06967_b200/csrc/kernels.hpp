@@ -201,6 +201,13 @@ void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double*
 void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x,
                      int* nonfinite, cudaStream_t s);
 
+// Per-point values between internal and user point order (perm: internal -> user).
+void launch_permute(int N, const int32_t* perm, const double* src, double* dst, bool to_user, cudaStream_t s);
+
+// User indices of the points with D == 0 into out[0..count) (out holds N + 1 int32: the last
+// slot is the counter); returns count (synchronizes s).
+int64_t launch_zero_d(int N, const double* D, const int32_t* perm, int32_t* out, cudaStream_t s);
+
 // Process-wide count of kernel launches issued by this library.
 void count_launches(int64_t n);
 int64_t launch_count();

@@ -334,12 +334,12 @@ class Handle:
         return BlockHessian(pp, dd, pd, lam.value)
 
     def warnings(self) -> List[str]:
-        out = []
-        buf = C.create_string_buffer(512)
-        for i in range(self.b.warning_count(self.h)):
-            self.b.warning(self.h, i, buf, 512)
-            out.append(buf.value.decode())
-        return out
+        if self.b.warning_count(self.h) == 0:
+            return []
+        n = int(self.b.warnings_text(self.h, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        self.b.warnings_text(self.h, buf, n + 1)
+        return buf.value.decode().split("\n")
 
     def _report(self, fn, cfg: SolverConfig, capacity: Optional[int] = None) -> SolveReport:
         cap = int(capacity if capacity is not None else max(cfg.max_iters, 1))

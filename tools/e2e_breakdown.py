@@ -14,8 +14,9 @@ sc = scenes.make_scene(cfg, device="cuda")
 st = sc.state
 c = cfg.solver_config(threshold_px=0.0, max_iters=10)
 st_pin = st.copy()
-st_pin.ref = torch.from_numpy(np.ascontiguousarray(st.ref)).pin_memory().numpy()
-st_pin.targets = torch.from_numpy(np.ascontiguousarray(st.targets)).pin_memory().numpy()
+for name in ("ref", "targets", "anchors_px", "inv_depths", "R", "t", "obs_ptr", "obs_frame"):
+    if getattr(st, name) is not None:
+        setattr(st_pin, name, torch.from_numpy(np.ascontiguousarray(getattr(st, name))).pin_memory().numpy())
 for rep in range(3):
     t0 = time.perf_counter()
     h = solver.Handle(st_pin, "gpu")
@@ -37,6 +38,17 @@ for rep in range(3):
     t7 = time.perf_counter()
     print(f"rep {rep}: create {1e3*(t1-t0):.1f} ms, build+first pass {1e3*(t2-t1):.1f}, {n} iters {1e3*(t3-t2):.1f}, "
           f"end {1e3*(t4-t3):.1f}, destroy {1e3*(t5-t4):.1f} | ic_solve {1e3*(t7-t6):.1f} ms")
+
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = solver.Handle(st_pin, "gpu")
+    t1 = time.perf_counter()
+    r = h.ic_run(c)
+    t2 = time.perf_counter()
+    h.close()
+    t3 = time.perf_counter()
+    print(f"ic_run path {rep}: create {1e3*(t1-t0):.1f} ms, ic_run {1e3*(t2-t1):.1f}, close {1e3*(t3-t2):.1f}")
 
 # per-iteration view with kernel times
 h = solver.Handle(st_pin, "gpu")

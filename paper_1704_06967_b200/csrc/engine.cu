@@ -338,7 +338,8 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
   a.tval = tval_.p;
-  a.jstride = jstride();
+  a.d0 = d0_.p;
+  a.pose0 = pose0_.p;  // frozen IC poses (rows of the factored IC Jacobian)
   a.gamma = gamma;
   a.partial = partial_.p;
   a.rec = rec_.p;
@@ -427,7 +428,7 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.d_old = d_old;
   a.mask_in = mask_in;
   a.active_out = active_out;
-  a.J = J_.p;
+  a.Jm = J_.p;
   auto e = ev_begin(PBA_K_OBS_PASS);
   launch_obs(OBS_IC, a, stream_);
   ev_end(PBA_K_OBS_PASS, e);
@@ -526,7 +527,7 @@ void Engine::ic_build(const pba_config* cfg) {
                              ": zero initial translation, inverse depth unobservable from this frame");
   }
   const size_t nO = std::max<int64_t>(NO_, 1);
-  J_.alloc(static_cast<size_t>(7) * jstride() + 2);  // +2: aligned TMA windows may overrun by one
+  J_.alloc(static_cast<size_t>(std::max<int64_t>(jm_doubles(NO_, P_), 1)));  // factored rows m (k_obs_lane)
   Bic_.alloc(6 * nO);
   Dic_.alloc(std::max(N_, 1));
   Hic_.alloc(21 * std::max(F_, 1));
@@ -536,7 +537,7 @@ void Engine::ic_build(const pba_config* cfg) {
   a.pose0 = pose0_.p;
   a.d_eval = d0_.p;
   a.active_out = mask_[0].p;
-  a.Jw = J_.p;
+  a.Jmw = J_.p;
   a.B_out = Bic_.p;
   dense_B_ = nullptr;  // the densified Schur blocks are stale
   trace_mark(stream_, "ic_build: setup+alloc");

@@ -100,7 +100,6 @@ class Engine {
                                double lambda, double* dx);
 
   int64_t num_obs() const { return NO_; }
-  int64_t jstride() const { return ((NO_ * P_ + 1) / 2) * 2; }
   int64_t device_bytes() const;
   cudaStream_t stream() const { return stream_; }
   void set_profiling(bool on);

@@ -124,7 +124,7 @@ void Engine::ic_refresh() {
   a.d_eval = d_cur_.p;
   a.mask_in = mask_[ic_.mcur].p;
   a.active_out = scratch_bits_.p;
-  a.J = J_.p;
+  a.Jm = J_.p;
   a.B_out = Bic_.p;
   dense_B_ = nullptr;
   auto e = ev_begin(PBA_K_IC_BUILD);

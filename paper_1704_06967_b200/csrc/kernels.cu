@@ -59,19 +59,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                                     uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
@@ -80,96 +67,42 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 #define PBA_OBS_STAGES 2
 #endif
 constexpr int kStages = PBA_OBS_STAGES;
-constexpr int kJStage = 258;    // doubles per J plane per stage: OPS*G(<=256) + 2 alignment slack
 constexpr int kObsStage = 260;  // observation slots per stage: OPS (<=256) + 4 alignment slack
 struct StageSmem {
-  double J[7][kJStage];
   double2 anc[kObsStage];
   int32_t fmp[kObsStage];
   uint32_t msk[kObsStage];
 };
 
-// Butterfly reduce-scatter over the G lanes of an observation group: on entry each lane
-// holds NVP = S*G per-pixel contributions v[]; on exit lane r (group-relative) holds in
-// v[0..S) the group sums of the original entries [r*S, (r+1)*S).  log2(G) levels,
-// NVP/2 + NVP/4 + ... + S shuffles: ~2 per pixel instead of keeping NVP accumulators.
-template <int G, int NVP>
-__device__ __forceinline__ void group_reduce_scatter(double (&v)[NVP], int lane) {
-#pragma unroll
-  for (int o = G / 2, L = NVP; o > 0; o >>= 1, L >>= 1) {
-    const bool upper = (lane & o) != 0;
-    const int h = L / 2;
-#pragma unroll
-    for (int s = 0; s < NVP / 2; ++s) {
-      if (s < h) {
-        const double lo = v[s], hi = v[h + s];
-        const double recv = __shfl_xor_sync(0xffffffffu, upper ? lo : hi, o);
-        v[s] = (upper ? hi : lo) + recv;
-      }
-    }
-  }
-}
-
-// Sum a group-scattered accumulator (S slots per lane) over the groups of the warp and
-// store the warp totals of entries [0, NV) into dst[] (lanes r < G of the first group).
-template <int G, int S, int NV>
-__device__ __forceinline__ void warp_store_scattered(const double (&acc)[S], int lane, double* dst) {
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    double v = acc[s];
-#pragma unroll
-    for (int o = G; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int c = lane * S + s;
-    if (lane < G && c < NV) dst[c] = v;
-  }
-}
-
-template <int MODE>
-constexpr bool obs_loads_J() {
-  return MODE == OBS_IC || MODE == OBS_REFRESH;
-}
-template <int MODE>
-constexpr size_t obs_smem_bytes() {
-  return obs_loads_J<MODE>() ? kStages * sizeof(StageSmem)
-                             : kStages * (sizeof(StageSmem) - sizeof(double) * 7 * kJStage);
-}
-
 constexpr int NT_OBS = NT + 32;  // 8 consumer warps + 1 producer warp
+constexpr size_t kEnergyStageBytes = sizeof(StageSmem);
+constexpr size_t kEnergySmem = kStages * kEnergyStageBytes;
 
 #ifndef PBA_OBS_MINB_IC
 #define PBA_OBS_MINB_IC 3
 #endif
-#ifndef PBA_OBS_MINB_OTHER
-#define PBA_OBS_MINB_OTHER 2
-#endif
-template <int MODE, int G>
-__global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY) ? PBA_OBS_MINB_IC : PBA_OBS_MINB_OTHER)
-    k_obs(const ObsArgs a) {
+// k_obs_energy: residual / Huber pass (energy_eval, solver.cpp:229-244) with the G lanes of
+// an observation over its pattern pixels; a producer warp streams each step's anchors,
+// point ids and mask words into shared memory with cp.async.bulk + mbarrier (kStages deep).
+template <int G>
+__global__ void __launch_bounds__(NT_OBS, PBA_OBS_MINB_IC) k_obs_energy(const ObsArgs a) {
   constexpr int OPS = NT / G;  // observations per block step
-  constexpr bool kHasH = (MODE == OBS_FC || MODE == OBS_BUILD || MODE == OBS_REFRESH);
-  constexpr bool kHasG = (MODE == OBS_IC || MODE == OBS_FC);
-  constexpr bool kHasRec = (MODE != OBS_ENERGY);
-  constexpr bool kLoadJ = obs_loads_J<MODE>();
   const int t = blockIdx.x;
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t];
   const int64_t q1 = a.ov.tile_q1[t];
   const int nsteps = static_cast<int>((q1 - q0 + OPS - 1) / OPS);
-  const bool has_mask = (MODE != OBS_BUILD) && a.mask_in != nullptr;
-  // frame-uniform data in shared memory (one frame per tile): keeps registers for the pixel math
-  __shared__ PoseD s_pe, s_p0;
+  const bool has_mask = a.mask_in != nullptr;
+  __shared__ PoseD s_pe;
   __shared__ FrameD s_fr;
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
   __shared__ double red[NT / 32][PT_STRIDE];
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  constexpr size_t kStageBytes = kLoadJ ? sizeof(StageSmem) : sizeof(StageSmem) - sizeof(double) * 7 * kJStage;
-  constexpr size_t kTail = kLoadJ ? sizeof(double) * 7 * kJStage : 0;
   const int P = a.pat.P;
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
-    if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], NT / 32);
@@ -183,37 +116,23 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   if (warp == NT / 32) {
     // ---------------- producer warp: TMA bulk copies, kStages steps ahead ----------------
     if (lane == 0) {
-      const uint64_t pol = kLoadJ ? evict_first_policy() : 0;
       for (int s = 0; s < nsteps; ++s) {
         const int st = s % kStages;
         const int round = s / kStages;
         if (round > 0) mbar_wait(&empty_bar[st], static_cast<uint32_t>((round - 1) & 1));
         fence_proxy_async_smem();
-        unsigned char* base = dyn_smem + static_cast<size_t>(st) * kStageBytes;
+        unsigned char* base = dyn_smem + static_cast<size_t>(st) * kEnergyStageBytes;
         const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
         const int64_t qe = qs + OPS < q1 ? qs + OPS : q1;
         const int64_t i0 = qs & ~int64_t(3), i1 = (qe + 3) & ~int64_t(3);  // 16-byte aligned int32 windows
-        uint32_t tx = static_cast<uint32_t>((qe - qs) * sizeof(double2) + (i1 - i0) * sizeof(int32_t) *
-                                            (has_mask ? 2 : 1));
-        int64_t j0 = 0, j1 = 0;
-        if (kLoadJ) {
-          j0 = (qs * P) & ~int64_t(1);
-          j1 = (qe * P + 1) & ~int64_t(1);
-          tx += static_cast<uint32_t>(7 * (j1 - j0) * sizeof(double));
-        }
+        const uint32_t tx = static_cast<uint32_t>((qe - qs) * sizeof(double2) + (i1 - i0) * sizeof(int32_t) *
+                                                  (has_mask ? 2 : 1));
         mbar_expect_tx(&full_bar[st], tx);
-        if (kLoadJ) {
-          double* sJ = reinterpret_cast<double*>(base);
-          for (int c = 0; c < 7; ++c)
-            bulk_g2s_evict_first(sJ + c * kJStage, a.J + c * a.jstride + j0,
-                                 static_cast<uint32_t>((j1 - j0) * sizeof(double)), &full_bar[st], pol);
-        }
-        unsigned char* tail = base + kTail;
-        bulk_g2s(tail, a.anchor_fm + qs, static_cast<uint32_t>((qe - qs) * sizeof(double2)), &full_bar[st]);
-        bulk_g2s(tail + sizeof(double2) * kObsStage, a.ov.fm_point + i0,
+        bulk_g2s(base, a.anchor_fm + qs, static_cast<uint32_t>((qe - qs) * sizeof(double2)), &full_bar[st]);
+        bulk_g2s(base + sizeof(double2) * kObsStage, a.ov.fm_point + i0,
                  static_cast<uint32_t>((i1 - i0) * sizeof(int32_t)), &full_bar[st]);
         if (has_mask)
-          bulk_g2s(tail + (sizeof(double2) + sizeof(int32_t)) * kObsStage, a.mask_in + i0,
+          bulk_g2s(base + (sizeof(double2) + sizeof(int32_t)) * kObsStage, a.mask_in + i0,
                    static_cast<uint32_t>((i1 - i0) * sizeof(uint32_t)), &full_bar[st]);
       }
     }
@@ -224,298 +143,142 @@ __global__ void __launch_bounds__(NT_OBS, (MODE == OBS_IC || MODE == OBS_ENERGY)
   // ---------------- consumer warps ----------------
   const FrameD& fr = s_fr;
   const PoseD& pe = s_pe;
-  const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
   const int k = threadIdx.x % G;
   const int j = threadIdx.x / G;
   const bool klive = k < P;
   const double gam = a.gamma;
-
-  // per-frame sums, group-scattered: lane r of a group owns entries [r*S, (r+1)*S)
-  // IC keeps its 6 gradient sums per lane (cheaper than shuffling); H modes scatter all 27
-  constexpr int GS = kHasH ? G : 1;  // scatter width for the gradient sums
-  constexpr int SG = (6 + GS - 1) / GS, SH = (21 + G - 1) / G;
-  double gacc[SG];
-  double hacc[kHasH ? SH : 1];
-#pragma unroll
-  for (int i = 0; i < SG; ++i) gacc[i] = 0.0;
-#pragma unroll
-  for (int i = 0; i < (kHasH ? SH : 1); ++i) hacc[i] = 0.0;
-  double energy = 0.0, nact = 0.0, noob = 0.0, maxupd = 0.0;
-
+  double energy = 0.0, nact = 0.0, noob = 0.0;
   for (int s = 0; s < nsteps; ++s) {
     const int st = s % kStages;
     mbar_wait(&full_bar[st], static_cast<uint32_t>((s / kStages) & 1));
-    const unsigned char* base = dyn_smem + static_cast<size_t>(st) * kStageBytes;
-    const unsigned char* tail = base + kTail;
+    const unsigned char* base = dyn_smem + static_cast<size_t>(st) * kEnergyStageBytes;
     const int64_t qs = q0 + static_cast<int64_t>(s) * OPS;
     const int64_t q = qs + j;
     const bool live = q < q1;
-    double2 an = make_double2(0.0, 0.0), dd = make_double2(1.0, 1.0);
+    double2 an = make_double2(0.0, 0.0);
     uint32_t mbits = 0u;
     int n = 0;
-    double J[kLoadJ ? 7 : 1];
     if (live) {
       const int ioff = static_cast<int>(qs & 3);  // skew of the aligned int32 window
-      an = reinterpret_cast<const double2*>(tail)[j];
-      n = reinterpret_cast<const int32_t*>(tail + sizeof(double2) * kObsStage)[j + ioff];
-      mbits = has_mask ? reinterpret_cast<const uint32_t*>(tail + (sizeof(double2) + sizeof(int32_t)) * kObsStage)[j + ioff]
+      an = reinterpret_cast<const double2*>(base)[j];
+      n = reinterpret_cast<const int32_t*>(base + sizeof(double2) * kObsStage)[j + ioff];
+      mbits = has_mask ? reinterpret_cast<const uint32_t*>(base + (sizeof(double2) + sizeof(int32_t)) * kObsStage)[j + ioff]
                        : 0xffffffffu;
-#ifndef PBA_HOIST_J
-#define PBA_DEFER_J 1
-#endif
-#ifndef PBA_DEFER_J
-      if constexpr (kLoadJ) {
-        if (klive) {
-          const int jj = j * P + k + static_cast<int>((qs * P) & 1);
-          const double* sJ = reinterpret_cast<const double*>(base);
-#pragma unroll
-          for (int c = 0; c < 7; ++c) J[c] = sJ[c * kJStage + jj];
-        }
-      }
-#endif
     }
-#ifndef PBA_DEFER_J
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage data now lives in registers
-#else
-    // J rows stay in shared memory until the residual is known (fewer live registers);
-    // the stage is released at the end of the step.
-    const double* sJrow = reinterpret_cast<const double*>(base) + (j * P + k + static_cast<int>((qs * P) & 1));
-#endif
-    if (live) {
-      dd.x = __ldg(&a.d_eval[n]);
-    }
-    const double dv = dd.x;  // depth at the evaluation parameters
-    bool act = false;        // residual active at the evaluation parameters
-    bool keep = false;       // final mask bit (BUILD)
-    double gnc = 0.0, dc = 0.0;
-    double b6[6] = {0, 0, 0, 0, 0, 0};
-    double gv[SG * GS];                    // this pixel's J^T W r contribution (padded)
-    double hv[kHasH ? SH * G : 1];         // this pixel's J^T W J upper triangle (padded)
-#pragma unroll
-    for (int i = 0; i < SG * GS; ++i) gv[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < (kHasH ? SH * G : 1); ++i) hv[i] = 0.0;
-    if (live) {
-      if (klive && ((mbits >> k) & 1u)) {
-        // template pixel (solver.cpp:42-49)
-        const double pu = an.x + static_cast<double>(a.pat.dx[k]);
-        const double pv = an.y + static_cast<double>(a.pat.dy[k]);
-        const double x = (pu - rf.cx) * a.ref_ifx;
-        const double y = (pv - rf.cy) * a.ref_ify;
-        const double tval = __ldg(&a.tval[static_cast<int64_t>(n) * P + k]);  // template value (solver.cpp:49)
-        double xn, yn, vx, vy, vz;
-        double r = 0.0;
-        if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
+    bool act = false;
+    if (live && klive && ((mbits >> k) & 1u)) {
+      const double dv = __ldg(&a.d_eval[n]);
+      // template pixel (solver.cpp:42-49)
+      const double pu = an.x + static_cast<double>(a.pat.dx[k]);
+      const double pv = an.y + static_cast<double>(a.pat.dy[k]);
+      const double x = (pu - rf.cx) * a.ref_ifx;
+      const double y = (pv - rf.cy) * a.ref_ify;
+      double xn, yn, vx, vy, vz;
+      if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
+        noob += 1.0;
+      } else {
+        const double u = fr.fx * xn + fr.cx;
+        const double v = fr.fy * yn + fr.cy;
+        if (!in_margin(u, v, fr.W, fr.H)) {
           noob += 1.0;
         } else {
-          const double u = fr.fx * xn + fr.cx;
-          const double v = fr.fy * yn + fr.cy;
-          if (!in_margin(u, v, fr.W, fr.H)) {
-            noob += 1.0;
-          } else {
-            r = tval - bilinear(fr.img, fr.W, u, v);
-            act = true;
-            energy += huber_loss(r, gam);
-            nact += 1.0;
-            if (a.r_out) a.r_out[q * P + k] = r;
-            if constexpr (MODE == OBS_FC) {
-              // image_gradient on the target at the warped point (image.cpp:36-49)
-              const double du = bilinear(fr.img, fr.W, u + 0.5, v) - bilinear(fr.img, fr.W, u - 0.5, v);
-              const double dvv = bilinear(fr.img, fr.W, u, v + 0.5) - bilinear(fr.img, fr.W, u, v - 0.5);
-              const double gx = du * fr.fx, gy = dvv * fr.fy;
-              // fc_warp_jacobian (geometry.cpp:129-139); row = -(grad^T J_img)
-              const double Rx0 = pe.R[0] * x + pe.R[1] * y + pe.R[2];
-              const double Rx1 = pe.R[3] * x + pe.R[4] * y + pe.R[5];
-              const double Rx2 = pe.R[6] * x + pe.R[7] * y + pe.R[8];
-              const double iz = 1.0 / vz;
-              const double P02 = -vx * iz * iz, P12 = -vy * iz * iz;
-              // pre columns: c0 = (0,-Rx2,Rx1), c1 = (Rx2,0,-Rx0), c2 = (-Rx1,Rx0,0),
-              // c3..5 = d e_i, c6 = t
-              double row[7];
-              row[0] = -(gx * (P02 * Rx1) + gy * (iz * -Rx2 + P12 * Rx1));
-              row[1] = -(gx * (iz * Rx2 + P02 * -Rx0) + gy * (P12 * -Rx0));
-              row[2] = -(gx * (iz * -Rx1) + gy * (iz * Rx0));
-              row[3] = -(gx * (iz * dv));
-              row[4] = -(gy * (iz * dv));
-              row[5] = -(gx * (P02 * dv) + gy * (P12 * dv));
-              row[6] = -(gx * (iz * pe.t[0] + P02 * pe.t[2]) + gy * (iz * pe.t[1] + P12 * pe.t[2]));
-              const double w = huber_weight(r, gam);
-              const double wr = w * r;
-              int h = 0;
-#pragma unroll
-              for (int i2 = 0; i2 < 6; ++i2) {
-                const double wi = w * row[i2];
-#pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * row[j2];
-                b6[i2] = wi * row[6];
-                gv[i2] = row[i2] * wr;
-              }
-              dc = w * row[6] * row[6];
-              gnc = row[6] * wr;
-            } else if constexpr (MODE == OBS_IC) {
-#ifdef PBA_DEFER_J
-#pragma unroll
-              for (int c = 0; c < 7; ++c) J[c] = sJrow[c * kJStage];
-#endif
-              // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
-              const double wr = fabs(r) <= gam ? r : copysign(gam, r);
-#pragma unroll
-              for (int c = 0; c < 6; ++c) gv[c] = J[c] * wr;
-              gnc = J[6] * wr;
-            } else if constexpr (MODE == OBS_REFRESH) {
-#ifdef PBA_DEFER_J
-#pragma unroll
-              for (int c = 0; c < 7; ++c) J[c] = sJrow[c * kJStage];
-#endif
-              const double w = huber_weight(r, gam);
-              int h = 0;
-#pragma unroll
-              for (int i2 = 0; i2 < 6; ++i2) {
-                const double wi = w * J[i2];
-#pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * J[j2];
-                b6[i2] = wi * J[6];
-              }
-              dc = w * J[6] * J[6];
-            }
-          }
-        }
-        if constexpr (MODE == OBS_BUILD) {
-          // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
-          const int64_t px = q * P + k;
-          double row[7] = {0, 0, 0, 0, 0, 0, 0};
-          const double d0 = dv;
-          // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
-          const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
-          const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
-          const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + d0 * p0.t[2];
-          const bool obs_ok = (d0 > 0.0) && !(vza < kDegenerateDepthEps);
-          if (act && obs_ok) {
-            // template gradient image_gradient(ref, x) (image.cpp:36-49)
-            const double gu = rf.fx * x + rf.cx, gv = rf.fy * y + rf.cy;
-            const bool grad_ok = in_bounds_px(gu - 0.5, gv, rf.W, rf.H) && in_bounds_px(gu + 0.5, gv, rf.W, rf.H) &&
-                                 in_bounds_px(gu, gv - 0.5, rf.W, rf.H) && in_bounds_px(gu, gv + 0.5, rf.W, rf.H);
-            const double R0x0 = p0.R[0] * x + p0.R[1] * y + p0.R[2];
-            const double R0x1 = p0.R[3] * x + p0.R[4] * y + p0.R[5];
-            const double R0x2 = p0.R[6] * x + p0.R[7] * y + p0.R[8];
-            const double vz0 = R0x2 + d0 * p0.t[2];
-            if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
-              keep = true;
-              const double gxi = (bilinear(rf.img, rf.W, gu + 0.5, gv) - bilinear(rf.img, rf.W, gu - 0.5, gv)) * rf.fx;
-              const double gyi = (bilinear(rf.img, rf.W, gu, gv + 0.5) - bilinear(rf.img, rf.W, gu, gv - 0.5)) * rf.fy;
-              const double zbar0 = vz0 / d0;
-              const double g30 = gxi / zbar0, g31 = gyi / zbar0, g32 = -(gxi * x + gyi * y) / zbar0;
-              const double a0 = p0.R[0] * g30 + p0.R[1] * g31 + p0.R[2] * g32;
-              const double a1 = p0.R[3] * g30 + p0.R[4] * g31 + p0.R[5] * g32;
-              const double a2 = p0.R[6] * g30 + p0.R[7] * g31 + p0.R[8] * g32;
-              const double adt = a0 * p0.t[0] + a1 * p0.t[1] + a2 * p0.t[2];
-              const double m0 = zbar0 * a0, m1 = zbar0 * a1, m2 = zbar0 * a2 - adt;
-              row[0] = R0x1 * m2 - R0x2 * m1;
-              row[1] = R0x2 * m0 - R0x0 * m2;
-              row[2] = R0x0 * m1 - R0x1 * m0;
-              row[3] = d0 * m0;
-              row[4] = d0 * m1;
-              row[5] = d0 * m2;
-              row[6] = m0 * p0.t[0] + m1 * p0.t[1] + m2 * p0.t[2];
-              const double w = huber_weight(r, gam);  // W0 (solver.cpp:279)
-              int h = 0;
-#pragma unroll
-              for (int i2 = 0; i2 < 6; ++i2) {
-                const double wi = w * row[i2];
-#pragma unroll
-                for (int j2 = i2; j2 < 6; ++j2) hv[h++] = wi * row[j2];
-                b6[i2] = wi * row[6];
-              }
-              dc = w * row[6] * row[6];
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < 7; ++c) a.Jw[c * a.jstride + px] = row[c];
+          const double r = __ldg(&a.tval[static_cast<int64_t>(n) * P + k]) - bilinear(fr.img, fr.W, u, v);
+          act = true;
+          energy += huber_loss(r, gam);
+          nact += 1.0;
+          if (a.r_out) a.r_out[q * P + k] = r;
         }
       }
     }
-    // per-frame sums: reduce-scatter this step's contributions over the group, accumulate
-    if constexpr (kHasG) {
-      if constexpr (GS > 1) group_reduce_scatter<GS, SG * GS>(gv, lane);
-#pragma unroll
-      for (int i = 0; i < SG; ++i) gacc[i] += gv[i];
-    }
-    if constexpr (kHasH) {
-      group_reduce_scatter<G, SH * G>(hv, lane);
-#pragma unroll
-      for (int i = 0; i < SH; ++i) hacc[i] += hv[i];
-    }
-    // per-observation records: reduce over the G lanes of the pattern
-    if constexpr (kHasRec) {
-      gnc = group_sum<G>(gnc);
-      dc = group_sum<G>(dc);
-      if constexpr (kHasH) {
-#pragma unroll
-        for (int i2 = 0; i2 < 6; ++i2) b6[i2] = group_sum<G>(b6[i2]);
-      }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, MODE == OBS_BUILD ? keep : act);
-    if (live && k == 0) {
-      const unsigned bits = (G == 32) ? bal : ((bal >> ((lane / G) * G)) & ((1u << G) - 1u));
-      a.active_out[q] = bits;
-      if constexpr (kHasRec) a.rec[q] = make_double2(gnc, dc);
-      if constexpr (kHasH) {
-#pragma unroll
-        for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
-      }
-    }
-#ifdef PBA_DEFER_J
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);
-#endif
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (live && k == 0) a.active_out[q] = (G == 32) ? bal : ((bal >> ((lane / G) * G)) & ((1u << G) - 1u));
   }
-
-  // ---- deterministic block reduction of the per-lane frame accumulators ----
+  // ---- deterministic block reduction ----
   auto put = [&](int slot, double v) {
     v = warp_sum(v);
     if (lane == 0) red[warp][slot] = v;
   };
-  if constexpr (kHasG) warp_store_scattered<GS, SG, 6>(gacc, lane, &red[warp][PT_G]);
-  if constexpr (kHasH) warp_store_scattered<G, SH, 21>(hacc, lane, &red[warp][PT_H]);
   put(PT_E, energy);
   put(PT_NACT, nact);
   put(PT_NOOB, noob);
-  {
-    const double m = warp_max(maxupd);
-    if (lane == 0) red[warp][PT_MAXUPD] = m;
-  }
   __syncthreads();
   if (warp == 0 && lane < PT_STRIDE) {
-    const bool used = (lane >= PT_E && lane <= PT_MAXUPD) || (kHasG && lane < 6) ||
-                      (kHasH && lane >= PT_H && lane < PT_H + 21);
     double v = 0.0;
-    if (used) {
-      if (lane == PT_MAXUPD) {
-        for (int w = 0; w < NT / 32; ++w) v = fmax(v, red[w][lane]);
-      } else {
-        for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
-      }
-    }
+    if (lane >= PT_E && lane < PT_MAXUPD)
+      for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
     a.partial[static_cast<int64_t>(t) * PT_STRIDE + lane] = v;
   }
 }
 
+template <int G>
+void launch_energy_g(const ObsArgs& a, cudaStream_t s) {
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_obs_energy<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kEnergySmem));
+    return true;
+  }();
+  (void)attr;
+  k_obs_energy<G><<<a.ov.ntiles, NT_OBS, kEnergySmem, s>>>(a);
+}
+
+void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
+  switch (G) {
+    case 1: launch_energy_g<1>(a, s); break;
+    case 2: launch_energy_g<2>(a, s); break;
+    case 4: launch_energy_g<4>(a, s); break;
+    case 8: launch_energy_g<8>(a, s); break;
+    case 16: launch_energy_g<16>(a, s); break;
+    default: launch_energy_g<32>(a, s); break;
+  }
+}
+
 // ---------------------------------------------------------------------------------
-// k_obs_lane: the Hessian-building passes (FC build at the candidate, IC build at p0) with
-// ONE LANE PER OBSERVATION looping over the P pattern pixels.  These passes are instruction
-// bound (fp64 Jacobian rows, 21 J^T W J products per pixel): keeping the per-observation
-// sums (B_nf, D, g_n, active bits) and the per-frame sums (J^T W J, J^T W r) in the lane's
-// registers removes every per-pixel shuffle reduction and the TMA pipeline of k_obs (whose
-// inputs here are only 24 bytes per observation).  Same formulas, same frame-major tiles.
+// k_obs_lane: ONE LANE PER OBSERVATION looping over the P pattern pixels; used for every
+// pass that touches Jacobian rows (IC candidate pass, IC build, IC refresh, FC build).
+// Per-observation sums (B_nf, D, g_n, active bits) and per-frame sums (J^T W r, J^T W J)
+// live in the lane's registers: no per-pixel shuffle reductions.
+//
+// Factored IC Jacobian.  The IC proxy row of pixel k of observation (n, f) at p0 is
+// (solver.cpp:331-349)   row = [ R0 x_k  x  m ,  d0 m ,  m . t0 ],   m = zbar0 (a - adt e_z / zbar0)
+// where R0 x_k and t0 come from the frozen frame pose p0_f and the pixel ray, d0 from the
+// frozen depth of the point, and m (3 doubles) carries the template gradient.  The build
+// pass stores m only (24 B instead of 56 B per pixel) and every consumer rebuilds the row
+// with the same fused operations (ic_row), so the rows are bitwise the rows the build used
+// for H and B.  Layout: blocks of 32 frame-major observations, [block][c][k][lane]
+// (coalesced for a warp of consecutive observations, written and read by lane).
 // ---------------------------------------------------------------------------------
 #ifndef PBA_LANE_MINB
 #define PBA_LANE_MINB 2
 #endif
-template <int MODE>
-__global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
-  static_assert(MODE == OBS_FC || MODE == OBS_BUILD, "lane kernel: H-building modes");
+#ifndef PBA_IC_MINB
+#define PBA_IC_MINB 3
+#endif
+
+__device__ __forceinline__ int64_t jm_index(int64_t q, int c, int k, int P) {
+  return ((q >> 5) * 3 + c) * (static_cast<int64_t>(P) * 32) + k * 32 + (q & 31);
+}
+// R0 x_k for the pixel ray (x, y, 1), explicit fused order shared by build and consumers
+__device__ __forceinline__ void rot_ray(const PoseD& p0, double x, double y, double (&R0x)[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) R0x[i] = fma(p0.R[3 * i], x, fma(p0.R[3 * i + 1], y, p0.R[3 * i + 2]));
+}
+__device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], double d0, double m0, double m1,
+                                       double m2, double (&row)[7]) {
+  row[0] = fma(R0x[1], m2, -(R0x[2] * m1));
+  row[1] = fma(R0x[2], m0, -(R0x[0] * m2));
+  row[2] = fma(R0x[0], m1, -(R0x[1] * m0));
+  row[3] = d0 * m0;
+  row[4] = d0 * m1;
+  row[5] = d0 * m2;
+  row[6] = fma(m0, p0.t[0], fma(m1, p0.t[1], m2 * p0.t[2]));
+}
+
+template <int MODE, int PT>
+__global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
+  constexpr bool kH = (MODE != OBS_IC);         // builds J^T W J, B, D
+  constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC);
   const int t = blockIdx.x;
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t], q1 = a.ov.tile_q1[t];
@@ -525,18 +288,18 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
-    if (MODE == OBS_BUILD) s_p0 = a.pose0[f];
+    if (MODE != OBS_FC) s_p0 = a.pose0[f];
   }
   __syncthreads();
   const FrameD& fr = s_fr;
   const PoseD& pe = s_pe;
   const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
-  const int P = a.pat.P;
+  const int P = PT > 0 ? PT : a.pat.P;
   const double gam = a.gamma;
-  double hacc[21], gacc[6];
+  double hacc[kH ? 21 : 1], gacc[6];
 #pragma unroll
-  for (int i = 0; i < 21; ++i) hacc[i] = 0.0;
+  for (int i = 0; i < (kH ? 21 : 1); ++i) hacc[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) gacc[i] = 0.0;
   double energy = 0.0, nact = 0.0, noob = 0.0;
@@ -545,6 +308,9 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
     const int n = a.ov.fm_point[q];
     const double dv = __ldg(&a.d_eval[n]);
     const double* tv = a.tval + static_cast<int64_t>(n) * P;
+    const uint32_t mbits = (MODE == OBS_IC || MODE == OBS_REFRESH) && a.mask_in ? a.mask_in[q] : 0xffffffffu;
+    const double d0n = (MODE == OBS_IC || MODE == OBS_REFRESH) ? __ldg(&a.d0[n]) : dv;
+    const double* jm = (MODE == OBS_FC) ? nullptr : a.Jm + jm_index(q, 0, 0, P);
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
     uint32_t bits = 0u;
@@ -556,13 +322,14 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
       const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + dv * p0.t[2];
       obs_ok = (dv > 0.0) && !(vza < kDegenerateDepthEps);
     }
+#pragma unroll (PT > 0 ? PT : 1)
     for (int k = 0; k < P; ++k) {
+      if (!((mbits >> k) & 1u)) continue;
       // template pixel (solver.cpp:42-49)
       const double pu = an.x + static_cast<double>(a.pat.dx[k]);
       const double pv = an.y + static_cast<double>(a.pat.dy[k]);
       const double x = (pu - rf.cx) * a.ref_ifx;
       const double y = (pv - rf.cy) * a.ref_ify;
-      double row[7] = {0, 0, 0, 0, 0, 0, 0};
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
       if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
@@ -578,7 +345,32 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
           energy += huber_loss(r, gam);
           nact += 1.0;
           if (a.r_out) a.r_out[q * P + k] = r;
-          if constexpr (MODE == OBS_FC) {
+          if constexpr (MODE == OBS_IC) {
+            // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
+            const double wr = fabs(r) <= gam ? r : copysign(gam, r);
+            double R0x[3], row[7];
+            rot_ray(p0, x, y, R0x);
+            ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) gacc[c] += row[c] * wr;
+            gnc += row[6] * wr;
+            bits |= 1u << k;
+          } else if constexpr (MODE == OBS_REFRESH) {
+            double R0x[3], row[7];
+            rot_ray(p0, x, y, R0x);
+            ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
+            const double w = huber_weight(r, gam);
+            int h = 0;
+#pragma unroll
+            for (int i2 = 0; i2 < 6; ++i2) {
+              const double wi = w * row[i2];
+#pragma unroll
+              for (int j2 = i2; j2 < 6; ++j2) hacc[h++] += wi * row[j2];
+              b6[i2] += wi * row[6];
+            }
+            dc += w * row[6] * row[6];
+            bits |= 1u << k;
+          } else if constexpr (MODE == OBS_FC) {
             // image_gradient on the target at the warped point (image.cpp:36-49)
             const double du = bilinear(fr.img, fr.W, u + 0.5, v) - bilinear(fr.img, fr.W, u - 0.5, v);
             const double dvv = bilinear(fr.img, fr.W, u, v + 0.5) - bilinear(fr.img, fr.W, u, v - 0.5);
@@ -589,6 +381,7 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
             const double Rx2 = pe.R[6] * x + pe.R[7] * y + pe.R[8];
             const double iz = 1.0 / vz;
             const double P02 = -vx * iz * iz, P12 = -vy * iz * iz;
+            double row[7];
             row[0] = -(gx * (P02 * Rx1) + gy * (iz * -Rx2 + P12 * Rx1));
             row[1] = -(gx * (iz * Rx2 + P02 * -Rx0) + gy * (P12 * -Rx0));
             row[2] = -(gx * (iz * -Rx1) + gy * (iz * Rx0));
@@ -615,18 +408,17 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
       }
       if constexpr (MODE == OBS_BUILD) {
         // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
-        bool keep = false;
+        double m0 = 0.0, m1 = 0.0, m2 = 0.0;
         if (act && obs_ok) {
           // template gradient image_gradient(ref, x) (image.cpp:36-49)
           const double gu = rf.fx * x + rf.cx, gvp = rf.fy * y + rf.cy;
           const bool grad_ok = in_bounds_px(gu - 0.5, gvp, rf.W, rf.H) && in_bounds_px(gu + 0.5, gvp, rf.W, rf.H) &&
                                in_bounds_px(gu, gvp - 0.5, rf.W, rf.H) && in_bounds_px(gu, gvp + 0.5, rf.W, rf.H);
-          const double R0x0 = p0.R[0] * x + p0.R[1] * y + p0.R[2];
-          const double R0x1 = p0.R[3] * x + p0.R[4] * y + p0.R[5];
-          const double R0x2 = p0.R[6] * x + p0.R[7] * y + p0.R[8];
-          const double vz0 = R0x2 + dv * p0.t[2];
+          double R0x[3];
+          rot_ray(p0, x, y, R0x);
+          const double vz0 = R0x[2] + dv * p0.t[2];
           if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
-            keep = true;
+            bits |= 1u << k;
             const double gxi = (bilinear(rf.img, rf.W, gu + 0.5, gvp) - bilinear(rf.img, rf.W, gu - 0.5, gvp)) * rf.fx;
             const double gyi = (bilinear(rf.img, rf.W, gu, gvp + 0.5) - bilinear(rf.img, rf.W, gu, gvp - 0.5)) * rf.fy;
             const double zbar0 = vz0 / dv;
@@ -635,14 +427,11 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
             const double a1 = p0.R[3] * g30 + p0.R[4] * g31 + p0.R[5] * g32;
             const double a2 = p0.R[6] * g30 + p0.R[7] * g31 + p0.R[8] * g32;
             const double adt = a0 * p0.t[0] + a1 * p0.t[1] + a2 * p0.t[2];
-            const double m0 = zbar0 * a0, m1 = zbar0 * a1, m2 = zbar0 * a2 - adt;
-            row[0] = R0x1 * m2 - R0x2 * m1;
-            row[1] = R0x2 * m0 - R0x0 * m2;
-            row[2] = R0x0 * m1 - R0x1 * m0;
-            row[3] = dv * m0;
-            row[4] = dv * m1;
-            row[5] = dv * m2;
-            row[6] = m0 * p0.t[0] + m1 * p0.t[1] + m2 * p0.t[2];
+            m0 = zbar0 * a0;
+            m1 = zbar0 * a1;
+            m2 = zbar0 * a2 - adt;
+            double row[7];
+            ic_row(p0, R0x, dv, m0, m1, m2, row);
             const double w = huber_weight(r, gam);  // W0 (solver.cpp:279)
             int h = 0;
 #pragma unroll
@@ -655,16 +444,18 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
             dc += w * row[6] * row[6];
           }
         }
-        if (keep) bits |= 1u << k;
-        const int64_t px = q * P + k;
-#pragma unroll
-        for (int c = 0; c < 7; ++c) a.Jw[c * a.jstride + px] = row[c];
+        double* jw = a.Jmw + jm_index(q, 0, k, P);
+        jw[0] = m0;
+        jw[P * 32] = m1;
+        jw[2 * P * 32] = m2;
       }
     }
     a.active_out[q] = bits;
     a.rec[q] = make_double2(gnc, dc);
+    if constexpr (kH) {
 #pragma unroll
-    for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+      for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+    }
   }
   // ---- deterministic block reduction of the per-lane frame accumulators ----
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -672,46 +463,24 @@ __global__ void __launch_bounds__(NT, PBA_LANE_MINB) k_obs_lane(const ObsArgs a)
     v = warp_sum(v);
     if (lane == 0) red[warp][slot] = v;
   };
-  if constexpr (MODE == OBS_FC) {
+  if constexpr (kG) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) put(PT_G + i, gacc[i]);
   }
+  if constexpr (kH) {
 #pragma unroll
-  for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
+    for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
+  }
   put(PT_E, energy);
   put(PT_NACT, nact);
   put(PT_NOOB, noob);
   __syncthreads();
   if (warp == 0) {
-    const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (MODE == OBS_FC && lane < 6) ||
-                      (lane >= PT_H && lane < PT_H + 21);
+    const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (kG && lane < 6) || (kH && lane >= PT_H && lane < PT_H + 21);
     double v = 0.0;
     if (used)
       for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
     a.partial[static_cast<int64_t>(t) * PT_STRIDE + lane] = v;
-  }
-}
-
-template <int MODE, int G>
-void launch_obs_g(const ObsArgs& a, cudaStream_t s) {
-  constexpr size_t smem = obs_smem_bytes<MODE>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_obs<MODE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr_set = true;
-  }
-  k_obs<MODE, G><<<a.ov.ntiles, NT_OBS, smem, s>>>(a);
-}
-
-template <int MODE>
-void launch_obs_mode(const ObsArgs& a, int G, cudaStream_t s) {
-  switch (G) {
-    case 1: launch_obs_g<MODE, 1>(a, s); break;
-    case 2: launch_obs_g<MODE, 2>(a, s); break;
-    case 4: launch_obs_g<MODE, 4>(a, s); break;
-    case 8: launch_obs_g<MODE, 8>(a, s); break;
-    case 16: launch_obs_g<MODE, 16>(a, s); break;
-    default: launch_obs_g<MODE, 32>(a, s); break;
   }
 }
 
@@ -1917,19 +1686,22 @@ std::atomic<int64_t> g_launches{0};
 void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+template <int MODE>
+void launch_lane(const ObsArgs& a, cudaStream_t s) {
+  if (a.pat.P == 8) k_obs_lane<MODE, 8><<<a.ov.ntiles, NT, 0, s>>>(a);
+  else k_obs_lane<MODE, 0><<<a.ov.ntiles, NT, 0, s>>>(a);
+}
+
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
   if (a.ov.ntiles == 0) return;
   const int G = next_pow2(a.pat.P);
   count_launches(1);
   switch (mode) {
-    case OBS_ENERGY: launch_obs_mode<OBS_ENERGY>(a, G, s); break;
-    case OBS_IC: launch_obs_mode<OBS_IC>(a, G, s); break;
-    case OBS_FC:
-      if (a.mask_in) launch_obs_mode<OBS_FC>(a, G, s);
-      else k_obs_lane<OBS_FC><<<a.ov.ntiles, NT, 0, s>>>(a);
-      break;
-    case OBS_BUILD: k_obs_lane<OBS_BUILD><<<a.ov.ntiles, NT, 0, s>>>(a); break;
-    default: launch_obs_mode<OBS_REFRESH>(a, G, s); break;
+    case OBS_ENERGY: launch_energy(a, G, s); break;
+    case OBS_IC: launch_lane<OBS_IC>(a, s); break;
+    case OBS_FC: k_obs_lane<OBS_FC, 0><<<a.ov.ntiles, NT, 0, s>>>(a); break;
+    case OBS_BUILD: launch_lane<OBS_BUILD>(a, s); break;
+    default: launch_lane<OBS_REFRESH>(a, s); break;
   }
 }
 

@@ -43,15 +43,17 @@ struct ObsArgs {
   const uint32_t* mask_in;     // NO bit words or null (= all pixels)
   uint32_t* active_out;        // NO bit words
   double* r_out;               // NO*P or null
-  const double* J;             // 7 planes of NO*P (IC / REFRESH read, BUILD write)
-  int64_t jstride;             // plane stride in doubles (even: 16-byte aligned TMA sources)
-  double* Jw;                  // BUILD output planes
+  const double* Jm;            // factored IC Jacobian m (3 per pixel, see k_obs_lane), IC / REFRESH read
+  double* Jmw;                 // BUILD output of m
+  const double* d0;            // N: frozen depths of the IC build (IC / REFRESH)
   double* B_out;               // NO*6 (FC/BUILD/REFRESH)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
   double* partial;             // ntiles * PT_STRIDE
 };
 
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
+// doubles of the factored IC Jacobian store for NO observations of P pixels
+inline int64_t jm_doubles(int64_t NO, int P) { return ((NO + 31) / 32) * 3 * static_cast<int64_t>(P) * 32; }
 
 // Candidate poses (IC: apply_ic_update geometry.cpp:197-209 with pc.d0 = 1;
 // FC: pose_boxplus geometry.cpp:93-98) from the pose step xp (6F).

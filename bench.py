@@ -127,14 +127,16 @@ def ncu_traffic():
 
 def obs_pass_bytes(st, n_px_active):
     """Algorithmic DRAM bytes of one IC obs-pass launch:
-    56 B per active pixel (frozen fp64 J row, 7 doubles) + per observation 44 B
-    (fm_point 4, mask 4, active 4, record 16, candidate depth 8, old depth 8) +
-    per point 16 B anchor (read once per observing frame is L2 traffic, counted once) +
-    the fp32 target images once + the reference image once."""
+    24 B per active pixel (factored frozen IC Jacobian m, 3 doubles; the row is rebuilt from m
+    and the frozen pose / depth) + per observation 44 B (anchor 16, point id 4, mask 4,
+    active bits 4, record 16) + per point 80 B (candidate depth 8, frozen depth 8, template
+    values 8P with P = 8; gathers counted once per point) + the fp32 target images once +
+    the reference image once."""
     H, W = st.ref.shape
     F = st.num_frames
     NO = st.num_observations
-    return 56 * n_px_active + 44 * NO + 16 * st.num_points + 4 * F * H * W + 4 * H * W
+    P = st.pattern.shape[0]
+    return 24 * n_px_active + 44 * NO + (16 + 8 * P) * st.num_points + 4 * F * H * W + 4 * H * W
 
 
 def canonical_bic(st, n_px_active):
@@ -393,9 +395,9 @@ def main():
                    "points": st.num_points, "observations": st.num_observations,
                    "pattern": int(st.pattern.shape[0]), "image": list(st.ref.shape[::-1]),
                    "active_obs_px_per_iter": r["n_px_iter"], "accepted_steps": r["accepted"],
-                   "l2": "inputs larger than L2 (frozen J rows %.1f GB)" % (56 * st.num_observations * st.pattern.shape[0] / 1e9),
+                   "l2": "inputs larger than L2 (factored frozen IC Jacobian %.1f GB)" % (24 * st.num_observations * st.pattern.shape[0] / 1e9),
                    "parallelism": "replicas" if world > 1 else "single"},
-        "roofline": {"bound": "hbm", "kernel": "k_obs<OBS_IC> fused residual/Huber/J^T W r pass",
+        "roofline": {"bound": "hbm", "kernel": "k_obs_lane<OBS_IC> fused residual/Huber/J^T W r pass (factored J)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(), "alg_bytes_per_launch": alg,
                      "launch_ms": obs_ms, "share_of_step": obs_ms / per_step_ms,

@@ -81,7 +81,14 @@ Engine::Engine(const pba_problem* p) {
   trace_mark(nullptr, "create: start");
   images_.alloc(off[F_ + 1]);
   ck(cudaMemcpyAsync(images_.p, p->ref.data, off[1] * sizeof(float), cudaMemcpyHostToDevice, stream_), "upload ref");
-  // target images go up on a second stream, overlapped with the layout build on stream_
+  ref_ = FrameD{images_.p, p->ref.width, p->ref.height, p->ref.fx, p->ref.fy, p->ref.cx, p->ref.cy};
+  frames_h_.resize(F_);
+  for (int f = 0; f < F_; ++f) {
+    const pba_image& im = p->targets[f];
+    frames_h_[f] = FrameD{images_.p + off[f + 1], im.width, im.height, im.fx, im.fy, im.cx, im.cy};
+  }
+  frames_.alloc(std::max(F_, 1));
+  // target images go up on a second stream, overlapped with the layout build
   cudaStream_t up = nullptr;
   cudaEvent_t up_done = nullptr;
   ck(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "upload stream");
@@ -90,16 +97,8 @@ Engine::Engine(const pba_problem* p) {
     ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
                        cudaMemcpyHostToDevice, up),
        "upload target");
+  if (F_ > 0) ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, up), "frames");
   ck(cudaEventRecord(up_done, up), "upload record");
-  ref_ = FrameD{images_.p, p->ref.width, p->ref.height, p->ref.fx, p->ref.fy, p->ref.cx, p->ref.cy};
-  frames_h_.resize(F_);
-  for (int f = 0; f < F_; ++f) {
-    const pba_image& im = p->targets[f];
-    frames_h_[f] = FrameD{images_.p + off[f + 1], im.width, im.height, im.fx, im.fy, im.cx, im.cy};
-  }
-  frames_.alloc(std::max(F_, 1));
-  if (F_ > 0)
-    ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, stream_), "frames");
 
   build_layout(p);
   trace_mark(stream_, "create: layout");

@@ -59,6 +59,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// bulk L2 prefetch of [p, p + bytes) (16-byte aligned start, size rounded up to 16)
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + static_cast<uintptr_t>(bytes) + 15) & ~uintptr_t(15);
+  for (uintptr_t a = a0; a < a1; a += 65536) {
+    const uint32_t n = static_cast<uint32_t>((a1 - a) < 65536 ? (a1 - a) : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+  }
+}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
@@ -255,6 +264,10 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #ifndef PBA_IC_MINB
 #define PBA_IC_MINB 3
 #endif
+#ifndef PBA_LANE_PREFETCH
+#define PBA_LANE_PREFETCH 1
+#endif
+constexpr int kLanePrefetch = PBA_LANE_PREFETCH;  // block steps of L2 prefetch ahead (0 = off)
 
 __device__ __forceinline__ int64_t jm_index(int64_t q, int c, int k, int P) {
   return ((q >> 5) * 3 + c) * (static_cast<int64_t>(P) * 32) + k * 32 + (q & 31);
@@ -275,8 +288,10 @@ __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], 
   row[6] = fma(m0, p0.t[0], fma(m1, p0.t[1], m2 * p0.t[2]));
 }
 
-template <int MODE, int PT>
+template <int MODE, int PT, int LPO>
 __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
+  static_assert(LPO == 1 || (PT > 0 && PT % LPO == 0), "LPO lanes split a compile-time pattern evenly");
+  constexpr int OPB = NT / LPO;  // observations per block step
   constexpr bool kH = (MODE != OBS_IC);         // builds J^T W J, B, D
   constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC);
   const int t = blockIdx.x;
@@ -303,14 +318,37 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
 #pragma unroll
   for (int i = 0; i < 6; ++i) gacc[i] = 0.0;
   double energy = 0.0, nact = 0.0, noob = 0.0;
-  for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
-    const double2 an = a.anchor_fm[q];
-    const int n = a.ov.fm_point[q];
+  // L2 prefetch of the streamed per-observation inputs, kLanePrefetch block steps ahead
+  auto prefetch_step = [&](int64_t qs) {
+    if (qs >= q1) return;
+    const int64_t qe = qs + OPB < q1 ? qs + OPB : q1;
+    if (threadIdx.x == 0) l2_prefetch(a.anchor_fm + qs, (qe - qs) * sizeof(double2));
+    if (threadIdx.x == 32) l2_prefetch(a.ov.fm_point + qs, (qe - qs) * sizeof(int32_t));
+    if (threadIdx.x == 64 && a.mask_in && (MODE == OBS_IC || MODE == OBS_REFRESH))
+      l2_prefetch(a.mask_in + qs, (qe - qs) * sizeof(uint32_t));
+    if (threadIdx.x == 96 && (MODE == OBS_IC || MODE == OBS_REFRESH)) {
+      const int64_t b0 = jm_index(qs, 0, 0, P), b1 = jm_index(qe - 1, 0, 0, P) - ((qe - 1) & 31) + 3 * P * 32;
+      l2_prefetch(a.Jm + b0 - (qs & 31), (b1 - (b0 - (qs & 31))) * sizeof(double));
+    }
+  };
+  if (kLanePrefetch > 0) {
+    for (int i = 0; i < kLanePrefetch; ++i) prefetch_step(q0 + static_cast<int64_t>(i) * OPB);
+  }
+  const int sub = LPO > 1 ? static_cast<int>(threadIdx.x % LPO) : 0;
+  constexpr int KP = PT > 0 ? PT / LPO : 0;  // pixels per lane (compile time), 0 = all P
+  for (int64_t base = q0; base < q1; base += OPB) {
+    if (kLanePrefetch > 0) prefetch_step(base + static_cast<int64_t>(kLanePrefetch) * OPB);
+    const int64_t q = base + threadIdx.x / LPO;
+    const bool live = q < q1;
+    const int64_t qc = live ? q : q1 - 1;  // clamped for the loads of idle lanes
+    const double2 an = a.anchor_fm[qc];
+    const int n = a.ov.fm_point[qc];
     const double dv = __ldg(&a.d_eval[n]);
     const double* tv = a.tval + static_cast<int64_t>(n) * P;
-    const uint32_t mbits = (MODE == OBS_IC || MODE == OBS_REFRESH) && a.mask_in ? a.mask_in[q] : 0xffffffffu;
+    const uint32_t mbits = !live ? 0u
+                           : ((MODE == OBS_IC || MODE == OBS_REFRESH) && a.mask_in ? a.mask_in[q] : 0xffffffffu);
     const double d0n = (MODE == OBS_IC || MODE == OBS_REFRESH) ? __ldg(&a.d0[n]) : dv;
-    const double* jm = (MODE == OBS_FC) ? nullptr : a.Jm + jm_index(q, 0, 0, P);
+    const double* jm = (MODE == OBS_FC) ? nullptr : a.Jm + jm_index(qc, 0, 0, P);
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
     uint32_t bits = 0u;
@@ -322,8 +360,9 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
       const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + dv * p0.t[2];
       obs_ok = (dv > 0.0) && !(vza < kDegenerateDepthEps);
     }
-#pragma unroll (PT > 0 ? PT : 1)
-    for (int k = 0; k < P; ++k) {
+#pragma unroll (PT > 0 ? KP : 1)
+    for (int kk = 0; kk < (PT > 0 ? KP : P); ++kk) {
+      const int k = PT > 0 ? sub * KP + kk : kk;
       if (!((mbits >> k) & 1u)) continue;
       // template pixel (solver.cpp:42-49)
       const double pu = an.x + static_cast<double>(a.pat.dx[k]);
@@ -450,11 +489,25 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
         jw[2 * P * 32] = m2;
       }
     }
-    a.active_out[q] = bits;
-    a.rec[q] = make_double2(gnc, dc);
-    if constexpr (kH) {
+    if constexpr (LPO > 1) {  // per-observation sums over the LPO lanes of the observation
 #pragma unroll
-      for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+      for (int o = 1; o < LPO; o <<= 1) {
+        gnc += __shfl_xor_sync(0xffffffffu, gnc, o);
+        dc += __shfl_xor_sync(0xffffffffu, dc, o);
+        bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+        if constexpr (kH) {
+#pragma unroll
+          for (int i2 = 0; i2 < 6; ++i2) b6[i2] += __shfl_xor_sync(0xffffffffu, b6[i2], o);
+        }
+      }
+    }
+    if (live && sub == 0) {
+      a.active_out[q] = bits;
+      a.rec[q] = make_double2(gnc, dc);
+      if constexpr (kH) {
+#pragma unroll
+        for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+      }
     }
   }
   // ---- deterministic block reduction of the per-lane frame accumulators ----
@@ -1686,10 +1739,17 @@ std::atomic<int64_t> g_launches{0};
 void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+#ifndef PBA_IC_LPO
+#define PBA_IC_LPO 1
+#endif
+#ifndef PBA_H_LPO
+#define PBA_H_LPO 1
+#endif
 template <int MODE>
 void launch_lane(const ObsArgs& a, cudaStream_t s) {
-  if (a.pat.P == 8) k_obs_lane<MODE, 8><<<a.ov.ntiles, NT, 0, s>>>(a);
-  else k_obs_lane<MODE, 0><<<a.ov.ntiles, NT, 0, s>>>(a);
+  constexpr int L8 = MODE == OBS_IC ? PBA_IC_LPO : PBA_H_LPO;
+  if (a.pat.P == 8) k_obs_lane<MODE, 8, L8><<<a.ov.ntiles, NT, 0, s>>>(a);
+  else k_obs_lane<MODE, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a);
 }
 
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
@@ -1699,7 +1759,7 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {
   switch (mode) {
     case OBS_ENERGY: launch_energy(a, G, s); break;
     case OBS_IC: launch_lane<OBS_IC>(a, s); break;
-    case OBS_FC: k_obs_lane<OBS_FC, 0><<<a.ov.ntiles, NT, 0, s>>>(a); break;
+    case OBS_FC: k_obs_lane<OBS_FC, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a); break;
     case OBS_BUILD: launch_lane<OBS_BUILD>(a, s); break;
     default: launch_lane<OBS_REFRESH>(a, s); break;
   }

@@ -272,6 +272,46 @@ constexpr int kLanePrefetch = PBA_LANE_PREFETCH;  // block steps of L2 prefetch 
 __device__ __forceinline__ int64_t jm_index(int64_t q, int c, int k, int P) {
   return ((q >> 5) * 3 + c) * (static_cast<int64_t>(P) * 32) + k * 32 + (q & 31);
 }
+// 16-byte shared-memory loads of the frame-uniform pose / frame records: one L1 data-pipe
+// wavefront per two doubles (the pass is bounded by L1 wavefronts, half of them smem).
+__device__ __forceinline__ double2 lds2(const void* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ PoseD lds_pose(const PoseD& s) {
+  PoseD r;
+  const char* b = reinterpret_cast<const char*>(&s);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double2 v = lds2(b + 16 * i);
+    const int j = 2 * i;
+    if (j < 9) r.R[j] = v.x; else r.t[j - 9] = v.x;
+    if (j + 1 < 9) r.R[j + 1] = v.y; else r.t[j + 1 - 9] = v.y;
+  }
+  return r;
+}
+struct FrameL {  // register copy of the FrameD fields a pixel needs
+  const float* img;
+  int W, H;
+  double fx, fy, cx, cy;
+};
+__device__ __forceinline__ FrameL lds_frame(const FrameD& s) {
+  static_assert(sizeof(FrameD) == 48, "FrameD layout");
+  const char* b = reinterpret_cast<const char*>(&s);
+  const double2 v0 = lds2(b), v1 = lds2(b + 16), v2 = lds2(b + 32);
+  FrameL f;
+  f.img = reinterpret_cast<const float*>(__double_as_longlong(v0.x));
+  const long long wh = __double_as_longlong(v0.y);
+  f.W = static_cast<int>(wh & 0xffffffffll);
+  f.H = static_cast<int>(wh >> 32);
+  f.fx = v1.x;
+  f.fy = v1.y;
+  f.cx = v2.x;
+  f.cy = v2.y;
+  return f;
+}
+
 // R0 x_k for the pixel ray (x, y, 1), explicit fused order shared by build and consumers
 __device__ __forceinline__ void rot_ray(const PoseD& p0, double x, double y, double (&R0x)[3]) {
 #pragma unroll
@@ -297,8 +337,8 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
   const int t = blockIdx.x;
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t], q1 = a.ov.tile_q1[t];
-  __shared__ PoseD s_pe, s_p0;
-  __shared__ FrameD s_fr;
+  __shared__ __align__(16) PoseD s_pe, s_p0;
+  __shared__ __align__(16) FrameD s_fr;
   __shared__ double red[NT / 32][PT_STRIDE];
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
@@ -306,9 +346,6 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
     if (MODE != OBS_FC) s_p0 = a.pose0[f];
   }
   __syncthreads();
-  const FrameD& fr = s_fr;
-  const PoseD& pe = s_pe;
-  const PoseD& p0 = s_p0;
   const FrameD& rf = a.ref;
   const int P = PT > 0 ? PT : a.pat.P;
   const double gam = a.gamma;
@@ -354,6 +391,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
     uint32_t bits = 0u;
     bool obs_ok = true;
     if constexpr (MODE == OBS_BUILD) {
+      const PoseD p0 = lds_pose(s_p0);
       // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
       const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
       const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
@@ -371,6 +409,8 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
       const double y = (pv - rf.cy) * a.ref_ify;
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
+      const PoseD pe = lds_pose(s_pe);
+      const FrameL fr = lds_frame(s_fr);
       if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
         noob += 1.0;
       } else {
@@ -387,6 +427,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
           if constexpr (MODE == OBS_IC) {
             // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
             const double wr = fabs(r) <= gam ? r : copysign(gam, r);
+            const PoseD p0 = lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
             ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
@@ -395,6 +436,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
             gnc += row[6] * wr;
             bits |= 1u << k;
           } else if constexpr (MODE == OBS_REFRESH) {
+            const PoseD p0 = lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
             ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
@@ -449,6 +491,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
         // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
         double m0 = 0.0, m1 = 0.0, m2 = 0.0;
         if (act && obs_ok) {
+          const PoseD p0 = lds_pose(s_p0);
           // template gradient image_gradient(ref, x) (image.cpp:36-49)
           const double gu = rf.fx * x + rf.cx, gvp = rf.fy * y + rf.cy;
           const bool grad_ok = in_bounds_px(gu - 0.5, gvp, rf.W, rf.H) && in_bounds_px(gu + 0.5, gvp, rf.W, rf.H) &&
@@ -1742,13 +1785,11 @@ int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 #ifndef PBA_IC_LPO
 #define PBA_IC_LPO 1
 #endif
-#ifndef PBA_H_LPO
-#define PBA_H_LPO 1
-#endif
 template <int MODE>
 void launch_lane(const ObsArgs& a, cudaStream_t s) {
-  constexpr int L8 = MODE == OBS_IC ? PBA_IC_LPO : PBA_H_LPO;
-  if (a.pat.P == 8) k_obs_lane<MODE, 8, L8><<<a.ov.ntiles, NT, 0, s>>>(a);
+  // compile-time pattern (unrolled pixel loop) for the IC pass on 8-pixel patterns; the
+  // Hessian-building passes stay rolled (register pressure)
+  if (MODE == OBS_IC && a.pat.P == 8) k_obs_lane<MODE, (MODE == OBS_IC ? 8 : 0), (MODE == OBS_IC ? PBA_IC_LPO : 1)><<<a.ov.ntiles, NT, 0, s>>>(a);
   else k_obs_lane<MODE, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a);
 }
 

@@ -169,6 +169,7 @@ Engine::~Engine() {
     cudaEventDestroy(pd.b);
   }
   if (status_h_) cudaFreeHost(status_h_);
+  if (pe_h_) cudaFreeHost(pe_h_);
   if (flags_h_) cudaFreeHost(flags_h_);
   set_alloc_stream(stream_);  // members free stream-ordered; sh_ destroys the stream last
 }
@@ -428,8 +429,9 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.mask_in = mask_in;
   a.active_out = active_out;
   a.Jm = J_.p;
+  build_frame_tabs(pose);  // host copy of the evaluation poses -> kernel-parameter frame tables
   auto e = ev_begin(PBA_K_OBS_PASS);
-  launch_obs(OBS_IC, a, stream_);
+  launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_);
   ev_end(PBA_K_OBS_PASS, e);
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);
@@ -439,6 +441,41 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, partial_cf_.p, pose_old != nullptr, true, false, gf_[buf].p, rhs_[buf].p, nullptr, nullptr,
            true);
+}
+
+// Frame tables of the IC pass (kTabFrames frames per launch): the evaluation poses are read
+// back (the pass is ordered after the candidate update anyway), the frozen poses and the
+// intrinsics are host-resident.
+void Engine::build_frame_tabs(const PoseD* pose_d) {
+  if (!pe_h_) ck(cudaMallocHost(&pe_h_, std::max(F_, 1) * sizeof(PoseD)), "pinned poses");
+  if (F_ > 0) ck(cudaMemcpyAsync(pe_h_, pose_d, F_ * sizeof(PoseD), cudaMemcpyDeviceToHost, stream_), "poses");
+  if (pose0_h_.size() != static_cast<size_t>(F_)) {
+    pose0_h_.resize(F_);
+    if (F_ > 0) ck(cudaMemcpyAsync(pose0_h_.data(), pose0_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToHost, stream_), "p0");
+  }
+  ck(cudaStreamSynchronize(stream_), "pose sync");
+  const int ntab = (F_ + kTabFrames - 1) / kTabFrames;
+  tabs_.resize(ntab);
+  for (int i = 0; i < ntab; ++i) {
+    FrameTab& T = tabs_[i];
+    T.f0 = i * kTabFrames;
+    T.nf = std::min(kTabFrames, F_ - T.f0);
+    T.tile0 = ftile_ptr_h_[T.f0];
+    T.ntiles = ftile_ptr_h_[T.f0 + T.nf] - T.tile0;
+    for (int j = 0; j < T.nf; ++j) {
+      const int f = T.f0 + j;
+      FrameRec& r = T.r[j];
+      r.pe = pe_h_[f];
+      r.p0 = pose0_h_[f];
+      r.fx = frames_h_[f].fx;
+      r.fy = frames_h_[f].fy;
+      r.cx = frames_h_[f].cx;
+      r.cy = frames_h_[f].cy;
+      r.img = frames_h_[f].img;
+      r.W = frames_h_[f].W;
+      r.H = frames_h_[f].H;
+    }
+  }
 }
 
 void Engine::ic_rescale_rhs(int buf, double lambda) {
@@ -518,6 +555,7 @@ void Engine::ic_build(const pba_config* cfg) {
   ic_.lambda = ic_.cfg.lambda0;
   check_template();
   if (F_ > 0) ck(cudaMemcpyAsync(pose0_.p, pose_state_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p0");
+  pose0_h_.clear();  // host copy of the frozen poses is refreshed by build_frame_tabs
   if (N_ > 0) ck(cudaMemcpyAsync(d0_.p, d_state_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d0");
   for (int f = 0; f < F_; ++f) {  // :265-271
     const double* t = &t_state_[3 * f];

@@ -174,6 +174,10 @@ class Engine {
   DBuf<Status> status_;
   DBuf<int> flags_;
   Status* status_h_ = nullptr;    // pinned
+  PoseD* pe_h_ = nullptr;         // pinned: evaluation poses for the IC frame tables
+  std::vector<PoseD> pose0_h_;    // host copy of the frozen IC poses
+  std::vector<FrameTab> tabs_;    // IC pass frame tables (kernel parameters)
+  std::vector<int32_t> ftile_ptr_h_;  // host copy of ov_.ftile_ptr
   int* flags_h_ = nullptr;        // pinned
 
   SolverState ic_;
@@ -239,6 +243,7 @@ class Engine {
                double lambda, const PoseD* pose_old, const double* d_old);
   void ic_rescale_rhs(int buf, double lambda);
   void alloc_schur();
+  void build_frame_tabs(const PoseD* pose_d);
   std::vector<int32_t> zero_depth_points(const double* D);
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
   void ic_factorize_loop(double lambda);

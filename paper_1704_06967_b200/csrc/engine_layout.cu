@@ -370,6 +370,7 @@ void Engine::build_layout(const pba_problem* p) {
     up(tile_q0_, tq0);
     up(tile_q1_, tq1);
     up(ftile_ptr_, ftile_ptr);
+    ftile_ptr_h_ = ftile_ptr;
     ov_.ntiles = static_cast<int>(tile_frame.size());
     ck(cudaStreamSynchronize(s), "tiles sync");
   }

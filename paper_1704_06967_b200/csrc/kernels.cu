@@ -296,6 +296,7 @@ struct FrameL {  // register copy of the FrameD fields a pixel needs
   int W, H;
   double fx, fy, cx, cy;
 };
+__device__ __forceinline__ FrameL tab_frame(const FrameRec& r) { return FrameL{r.img, r.W, r.H, r.fx, r.fy, r.cx, r.cy}; }
 __device__ __forceinline__ FrameL lds_frame(const FrameD& s) {
   static_assert(sizeof(FrameD) == 48, "FrameD layout");
   const char* b = reinterpret_cast<const char*>(&s);
@@ -328,13 +329,17 @@ __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], 
   row[6] = fma(m0, p0.t[0], fma(m1, p0.t[1], m2 * p0.t[2]));
 }
 
-template <int MODE, int PT, int LPO>
-__global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
+// kTab: the frame-uniform records (candidate pose, frozen pose, intrinsics) come from a
+// kernel-parameter table (constant bank, read through the constant cache) instead of shared
+// memory: the per-pixel re-reads of the pose then cost no L1 data-pipe wavefronts, which
+// bound the shared-memory variant.
+template <int MODE, int PT, int LPO, bool kTab>
+__device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& tab) {
   static_assert(LPO == 1 || (PT > 0 && PT % LPO == 0), "LPO lanes split a compile-time pattern evenly");
   constexpr int OPB = NT / LPO;  // observations per block step
   constexpr bool kH = (MODE != OBS_IC);         // builds J^T W J, B, D
   constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC);
-  const int t = blockIdx.x;
+  const int t = kTab ? tab.tile0 + static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t], q1 = a.ov.tile_q1[t];
   __shared__ __align__(16) PoseD s_pe, s_p0;
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
     uint32_t bits = 0u;
     bool obs_ok = true;
     if constexpr (MODE == OBS_BUILD) {
-      const PoseD p0 = lds_pose(s_p0);
+      const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
       // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
       const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
       const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
@@ -409,8 +414,8 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
       const double y = (pv - rf.cy) * a.ref_ify;
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
-      const PoseD pe = lds_pose(s_pe);
-      const FrameL fr = lds_frame(s_fr);
+      const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
+      const FrameL fr = kTab ? tab_frame(tab.r[f - tab.f0]) : lds_frame(s_fr);
       if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
         noob += 1.0;
       } else {
@@ -427,7 +432,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
           if constexpr (MODE == OBS_IC) {
             // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
             const double wr = fabs(r) <= gam ? r : copysign(gam, r);
-            const PoseD p0 = lds_pose(s_p0);
+            const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
             ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
@@ -436,7 +441,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
             gnc += row[6] * wr;
             bits |= 1u << k;
           } else if constexpr (MODE == OBS_REFRESH) {
-            const PoseD p0 = lds_pose(s_p0);
+            const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
             ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
         // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
         double m0 = 0.0, m1 = 0.0, m2 = 0.0;
         if (act && obs_ok) {
-          const PoseD p0 = lds_pose(s_p0);
+          const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
           // template gradient image_gradient(ref, x) (image.cpp:36-49)
           const double gu = rf.fx * x + rf.cx, gvp = rf.fy * y + rf.cy;
           const bool grad_ok = in_bounds_px(gu - 0.5, gvp, rf.W, rf.H) && in_bounds_px(gu + 0.5, gvp, rf.W, rf.H) &&
@@ -578,6 +583,17 @@ __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MI
       for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
     a.partial[static_cast<int64_t>(t) * PT_STRIDE + lane] = v;
   }
+}
+
+template <int MODE, int PT, int LPO>
+__global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
+  const FrameTab* none = nullptr;
+  obs_lane_body<MODE, PT, LPO, false>(a, *none);
+}
+template <int MODE, int PT, int LPO>
+__global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB)
+    k_obs_lane_tab(const ObsArgs a, const FrameTab tab) {
+  obs_lane_body<MODE, PT, LPO, true>(a, tab);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1791,6 +1807,16 @@ void launch_lane(const ObsArgs& a, cudaStream_t s) {
   // Hessian-building passes stay rolled (register pressure)
   if (MODE == OBS_IC && a.pat.P == 8) k_obs_lane<MODE, (MODE == OBS_IC ? 8 : 0), (MODE == OBS_IC ? PBA_IC_LPO : 1)><<<a.ov.ntiles, NT, 0, s>>>(a);
   else k_obs_lane<MODE, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a);
+}
+
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s) {
+  for (int i = 0; i < ntabs; ++i) {
+    const int nb = tabs[i].ntiles;
+    if (nb == 0) continue;
+    if (a.pat.P == 8) k_obs_lane_tab<OBS_IC, 8, PBA_IC_LPO><<<nb, NT, 0, s>>>(a, tabs[i]);
+    else k_obs_lane_tab<OBS_IC, 0, 1><<<nb, NT, 0, s>>>(a, tabs[i]);
+    count_launches(1);
+  }
 }
 
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s) {

@@ -52,6 +52,22 @@ struct ObsArgs {
 };
 
 void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
+
+// Frame table of the IC pass for frames [f0, f0 + nf) (tiles [tile0, tile0 + ntiles)), passed
+// as a kernel parameter: the frame-uniform records are then read through the constant cache.
+struct FrameRec {
+  PoseD pe;                 // evaluation (candidate) pose
+  PoseD p0;                 // frozen IC pose
+  double fx, fy, cx, cy;
+  const float* img;
+  int W, H;
+};
+constexpr int kTabFrames = 120;  // 120 * 240 B + ObsArgs < 32 KB kernel-parameter limit
+struct FrameTab {
+  int f0, nf, tile0, ntiles;
+  FrameRec r[kTabFrames];
+};
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s);
 // doubles of the factored IC Jacobian store for NO observations of P pixels
 inline int64_t jm_doubles(int64_t NO, int P) { return ((NO + 31) / 32) * 3 * static_cast<int64_t>(P) * 32; }
 

@@ -170,6 +170,12 @@ Engine::~Engine() {
   }
   if (status_h_) cudaFreeHost(status_h_);
   if (pe_h_) cudaFreeHost(pe_h_);
+  if (side_) {
+    cudaStreamSynchronize(side_);
+    cudaStreamDestroy(side_);
+    cudaEventDestroy(fork_);
+    cudaEventDestroy(join_);
+  }
   if (flags_h_) cudaFreeHost(flags_h_);
   set_alloc_stream(stream_);  // members free stream-ordered; sh_ destroys the stream last
 }
@@ -431,7 +437,12 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.Jm = J_.p;
   build_frame_tabs(pose);  // host copy of the evaluation poses -> kernel-parameter frame tables
   auto e = ev_begin(PBA_K_OBS_PASS);
-  launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_);
+  if (!side_) {
+    ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+    ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "fork event");
+    ck(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "join event");
+  }
+  launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_, side_, fork_, join_);
   ev_end(PBA_K_OBS_PASS, e);
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);

@@ -177,6 +177,8 @@ class Engine {
   PoseD* pe_h_ = nullptr;         // pinned: evaluation poses for the IC frame tables
   std::vector<PoseD> pose0_h_;    // host copy of the frozen IC poses
   std::vector<FrameTab> tabs_;    // IC pass frame tables (kernel parameters)
+  cudaStream_t side_ = nullptr;   // second stream for the IC pass frame chunks
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<int32_t> ftile_ptr_h_;  // host copy of ov_.ftile_ptr
   int* flags_h_ = nullptr;        // pinned
 

@@ -1809,13 +1809,26 @@ void launch_lane(const ObsArgs& a, cudaStream_t s) {
   else k_obs_lane<MODE, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a);
 }
 
-void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s) {
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s, cudaStream_t side,
+                       cudaEvent_t fork, cudaEvent_t join) {
+  // the frame chunks are independent (disjoint tiles): chunks after the first run on a side
+  // stream so their launches overlap instead of serialising tail effects
+  const bool fan = ntabs > 1 && side && fork && join;
+  if (fan) {
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(side, fork, 0);
+  }
   for (int i = 0; i < ntabs; ++i) {
     const int nb = tabs[i].ntiles;
     if (nb == 0) continue;
-    if (a.pat.P == 8) k_obs_lane_tab<OBS_IC, 8, PBA_IC_LPO><<<nb, NT, 0, s>>>(a, tabs[i]);
-    else k_obs_lane_tab<OBS_IC, 0, 1><<<nb, NT, 0, s>>>(a, tabs[i]);
+    cudaStream_t st = (fan && i > 0) ? side : s;
+    if (a.pat.P == 8) k_obs_lane_tab<OBS_IC, 8, PBA_IC_LPO><<<nb, NT, 0, st>>>(a, tabs[i]);
+    else k_obs_lane_tab<OBS_IC, 0, 1><<<nb, NT, 0, st>>>(a, tabs[i]);
     count_launches(1);
+  }
+  if (fan) {
+    cudaEventRecord(join, side);
+    cudaStreamWaitEvent(s, join, 0);
   }
 }
 

@@ -67,7 +67,8 @@ struct FrameTab {
   int f0, nf, tile0, ntiles;
   FrameRec r[kTabFrames];
 };
-void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s);
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s, cudaStream_t side,
+                       cudaEvent_t fork, cudaEvent_t join);
 // doubles of the factored IC Jacobian store for NO observations of P pixels
 inline int64_t jm_doubles(int64_t NO, int P) { return ((NO + 31) / 32) * 3 * static_cast<int64_t>(P) * 32; }
 

@@ -2,6 +2,8 @@
 // Control flow mirrors /root/reference/proj/src/solver.cpp line by line (cited);
 // every per-pixel / per-point / per-frame computation is a kernel in kernels.cu.
 #include <algorithm>
+#include <unordered_map>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +27,66 @@ void trace_mark(cudaStream_t s, const char* what) {
   std::fprintf(stderr, "[pba trace] %-28s %8.2f ms\n", what,
                std::chrono::duration<double, std::milli>(now - last).count());
   last = now;
+}
+
+namespace {
+size_t round_block(size_t b) {
+  const size_t g = b >= (size_t(1) << 20) ? (size_t(2) << 20) : 256;
+  return (b + g - 1) / g * g;
+}
+struct BlockCache {
+  struct Block {
+    void* p;
+    cudaEvent_t ev;
+  };
+  std::mutex m;
+  std::unordered_multimap<size_t, Block> free;
+  size_t cached = 0;
+  static constexpr size_t kCap = size_t(96) << 30;  // bytes parked at most (then returned to the pool)
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();  // never destroyed: blocks may be released at process exit
+  return *c;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  const size_t rb = round_block(bytes);
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.m);
+    auto it = c.free.find(rb);
+    if (it != c.free.end()) {
+      const BlockCache::Block b = it->second;
+      c.free.erase(it);
+      c.cached -= rb;
+      ck(cudaStreamWaitEvent(s, b.ev, 0), "block reuse wait");  // after the previous owner's work
+      cudaEventDestroy(b.ev);
+      return b.p;
+    }
+  }
+  void* p = nullptr;
+  ck(cudaMallocAsync(&p, rb, s), "cudaMallocAsync");
+  return p;
+}
+
+void dev_free(void* p, size_t bytes, cudaStream_t s) {
+  const size_t rb = round_block(bytes);
+  BlockCache& c = block_cache();
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(ev, s) != cudaSuccess) {
+    if (ev) cudaEventDestroy(ev);
+    cudaFreeAsync(p, s);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(c.m);
+  if (c.cached + rb > BlockCache::kCap) {
+    cudaEventDestroy(ev);
+    cudaFreeAsync(p, s);
+    return;
+  }
+  c.free.emplace(rb, BlockCache::Block{p, ev});
+  c.cached += rb;
 }
 
 namespace {
@@ -88,19 +150,38 @@ Engine::Engine(const pba_problem* p) {
     frames_h_[f] = FrameD{images_.p + off[f + 1], im.width, im.height, im.fx, im.fy, im.cx, im.cy};
   }
   frames_.alloc(std::max(F_, 1));
-  // target images go up on a second stream, overlapped with the layout build
-  cudaStream_t up = nullptr;
-  cudaEvent_t up_done = nullptr;
-  ck(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "upload stream");
-  ck(cudaEventCreateWithFlags(&up_done, cudaEventDisableTiming), "upload event");
-  for (int f = 0; f < F_; ++f)
-    ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
-                       cudaMemcpyHostToDevice, up),
-       "upload target");
-  if (F_ > 0) ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, up), "frames");
-  ck(cudaEventRecord(up_done, up), "upload record");
+  // target images go up on a second stream once the observation list and anchors are up
+  // (they gate the layout build), so the image upload overlaps the layout build
+  struct UploadRes {  // released on every exit path (constructor errors included)
+    cudaStream_t up = nullptr;
+    cudaEvent_t up_done = nullptr, obs_up = nullptr;
+    ~UploadRes() {
+      if (up) {
+        cudaStreamSynchronize(up);
+        cudaStreamDestroy(up);
+      }
+      if (up_done) cudaEventDestroy(up_done);
+      if (obs_up) cudaEventDestroy(obs_up);
+    }
+  } ur;
+  ck(cudaStreamCreateWithFlags(&ur.up, cudaStreamNonBlocking), "upload stream");
+  ck(cudaEventCreateWithFlags(&ur.up_done, cudaEventDisableTiming), "upload event");
+  ck(cudaEventCreateWithFlags(&ur.obs_up, cudaEventDisableTiming), "obs upload event");
+  cudaStream_t up = ur.up;
+  cudaEvent_t up_done = ur.up_done, obs_up = ur.obs_up;
+  auto upload_targets = [&]() {
+    ck(cudaEventRecord(obs_up, stream_), "obs upload record");
+    ck(cudaStreamWaitEvent(up, obs_up, 0), "obs upload wait");
+    for (int f = 0; f < F_; ++f)
+      ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
+                         cudaMemcpyHostToDevice, up),
+         "upload target");
+    if (F_ > 0)
+      ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, up), "frames");
+    ck(cudaEventRecord(up_done, up), "upload record");
+  };
 
-  build_layout(p);
+  build_layout(p, upload_targets);
   trace_mark(stream_, "create: layout");
   const int ntiles = ov_.ntiles;
   tval_.alloc(std::max<size_t>(static_cast<size_t>(N_) * P_, 1));
@@ -156,8 +237,6 @@ Engine::Engine(const pba_problem* p) {
   // the caller's image buffers are free once create returns: finish the upload here
   ck(cudaStreamWaitEvent(stream_, up_done, 0), "upload wait");
   ck(cudaEventSynchronize(up_done), "upload sync");
-  cudaEventDestroy(up_done);
-  cudaStreamDestroy(up);
   trace_mark(stream_, "create: image upload tail");
 }
 

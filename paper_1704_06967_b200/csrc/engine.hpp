@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdint>
 #include <stdexcept>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -29,8 +30,13 @@ inline void ck(cudaError_t e, const char* what) {
 }
 
 // Device allocations are stream-ordered from the device's default memory pool, which is
-// configured to retain freed memory (release threshold = max): creating and destroying
-// handles for repeated solves then costs no cudaMalloc / cudaFree round trips.
+// configured to retain freed memory (release threshold = max), behind an exact-size block
+// cache: a released block is parked with an event recorded on its stream and handed to the
+// next request of the same (rounded) size after that event (stream-ordered, no host wait).
+// Repeated solves on same-shaped problems then never go back to the pool, whose large
+// requests can otherwise stall on mapping new memory.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
 cudaStream_t alloc_stream();           // stream of the engine being constructed / used
 // Host-side phase tracer (env PBA_TRACE=1): synchronizes s and prints the ms since the last mark.
 void trace_mark(cudaStream_t s, const char* what);
@@ -51,11 +57,11 @@ struct DBuf {
     release();
     if (count == 0) return;
     s = alloc_stream();
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s), "cudaMallocAsync");
+    p = static_cast<T*>(dev_alloc(count * sizeof(T), s));
     n = count;
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(p, n * sizeof(T), s);
     p = nullptr;
     n = 0;
   }
@@ -222,7 +228,7 @@ class Engine {
   void drain_profile();
 
   // layout (engine_layout.cu)
-  void build_layout(const pba_problem* p);
+  void build_layout(const pba_problem* p, const std::function<void()>& after_obs_upload);
   void mask_to_bits(const uint8_t* mask_user, uint32_t* bits_d);
   void bits_to_user(const uint32_t* bits_d, uint8_t* active_user);
   void rows_to_user(const double* src_fm, int w, double* dst_user);

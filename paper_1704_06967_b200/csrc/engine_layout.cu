@@ -216,7 +216,7 @@ int bits_for(int64_t v) {
 
 template struct DBuf<unsigned char>;
 
-void Engine::build_layout(const pba_problem* p) {
+void Engine::build_layout(const pba_problem* p, const std::function<void()>& after_obs_upload) {
   cudaStream_t s = stream_;
   // ---- caller CSR on the device (dense problems are generated in place) ----
   DBuf<int64_t> uptr;
@@ -250,6 +250,7 @@ void Engine::build_layout(const pba_problem* p) {
   anc_user.alloc(std::max(N_, 1));
   if (N_ > 0)
     ck(cudaMemcpyAsync(anc_user.p, p->anchors_px, N_ * sizeof(double2), cudaMemcpyHostToDevice, s), "anchors");
+  after_obs_upload();  // the caller starts the image upload behind the layout inputs
   DBuf<uint32_t> key, key_sorted;
   DBuf<int32_t> idx, perm_d, iperm_d;
   key.alloc(std::max(N_, 1));
@@ -302,6 +303,7 @@ void Engine::build_layout(const pba_problem* p) {
   anchor_.alloc(std::max(N_, 1));
   anchor_fm_.alloc(nO);
   ck(cudaMemsetAsync(fm_point_.p, 0, (nO + 8) * sizeof(int32_t), s), "memset");
+  trace_mark(s, "layout:   fm allocs");
   if (N_ > 0) {
     k_anchor_internal<<<(N_ + 255) / 256, 256, 0, s>>>(N_, perm_d.p, anc_user.p, anchor_.p);
     count_launches(1);
@@ -309,7 +311,9 @@ void Engine::build_layout(const pba_problem* p) {
   if (NO_ > 0) {
     k_iota<<<grid_for(NO_), 256, 0, s>>>(NO_, iota_o.p);
     count_launches(1);
+    trace_mark(s, "layout:   iota");
     radix_sort_pairs(pm_frame_.p, frames_sorted.p, iota_o.p, fm2pm.p, NO_, bits_for(F_), s);
+    trace_mark(s, "layout:   frame sort");
     k_fm_scatter<<<grid_for(NO_), 256, 0, s>>>(NO_, fm2pm.p, pm_point.p, pm2uo.p, anchor_.p, pm2fm_.p, fm_point_.p,
                                                uo2q_d_.p, anchor_fm_.p);
     count_launches(1);

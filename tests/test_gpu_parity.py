@@ -346,3 +346,29 @@ def test_deterministic_repeat(c1):
     r2 = solver.ic_solve(st, cfg)
     assert r1.final_energy == r2.final_energy
     assert np.array_equal(r1.final_inv_depths, r2.final_inv_depths)
+
+
+@pytest.fixture(scope="module")
+def many_frames():
+    # C4-shaped (azimuth visibility window, sub-pixel anchors, DSO8) with more frames than one
+    # IC frame table holds (kTabFrames = 120): exercises the chunked IC pass on two streams
+    cfg = scenes.baseline_config("C4", width=320, height=180, fx=250.0, frames=130, points=3000, iters=4)
+    return scenes.make_scene(cfg, device="cpu")
+
+
+@pytest.mark.parametrize("solver_kind", ["ic", "fc"])
+def test_run_matches_oracle_many_frames(many_frames, solver_kind):
+    st = many_frames.state
+    cfg = many_frames.cfg.solver_config()
+    g, o = pair(st)
+    rg, ro = (g.ic_run(cfg), o.ic_run(cfg)) if solver_kind == "ic" else (g.fc_run(cfg), o.fc_run(cfg))
+    _compare_runs(rg, ro, st.num_frames, st.num_points)
+
+
+def test_ic_run_refresh_hessian_matches_oracle(c1):  # refresh_ic_hessian (solver.cpp:505-531)
+    st = c1.state
+    cfg = c1.cfg.solver_config(max_iters=5, refresh_ic_hessian=True)
+    g, o = pair(st)
+    rg, ro = g.ic_run(cfg), o.ic_run(cfg)
+    assert rg.hessian_builds == ro.hessian_builds and rg.hessian_builds > 1
+    _compare_runs(rg, ro, st.num_frames, st.num_points)

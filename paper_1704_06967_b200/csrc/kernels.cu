@@ -424,7 +424,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         if (!in_margin(u, v, fr.W, fr.H)) {
           noob += 1.0;
         } else {
-          r = __ldg(tv + k) - bilinear(fr.img, fr.W, u, v);
+          double gdu = 0.0, gdv = 0.0;
+          if constexpr (MODE == OBS_FC) {
+            r = __ldg(tv + k) - bilinear_grad<true>(fr.img, fr.W, u, v, gdu, gdv);  // + image_gradient taps
+          } else {
+            r = __ldg(tv + k) - bilinear(fr.img, fr.W, u, v);
+          }
           act = true;
           energy += huber_loss(r, gam);
           nact += 1.0;
@@ -458,9 +463,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             bits |= 1u << k;
           } else if constexpr (MODE == OBS_FC) {
             // image_gradient on the target at the warped point (image.cpp:36-49)
-            const double du = bilinear(fr.img, fr.W, u + 0.5, v) - bilinear(fr.img, fr.W, u - 0.5, v);
-            const double dvv = bilinear(fr.img, fr.W, u, v + 0.5) - bilinear(fr.img, fr.W, u, v - 0.5);
-            const double gx = du * fr.fx, gy = dvv * fr.fy;
+            const double gx = gdu * fr.fx, gy = gdv * fr.fy;
             // fc_warp_jacobian (geometry.cpp:129-139); row = -(grad^T J_img)
             const double Rx0 = pe.R[0] * x + pe.R[1] * y + pe.R[2];
             const double Rx1 = pe.R[3] * x + pe.R[4] * y + pe.R[5];

@@ -185,7 +185,8 @@ Engine::Engine(const pba_problem* p) {
   trace_mark(stream_, "create: layout");
   const int ntiles = ov_.ntiles;
   tval_.alloc(std::max<size_t>(static_cast<size_t>(N_) * P_, 1));
-  launch_template_values(N_, pat_, ref_, anchor_.p, tval_.p, stream_);
+  tgrad_.alloc(std::max<size_t>(static_cast<size_t>(N_) * P_, 1));
+  launch_template_values(N_, pat_, ref_, anchor_.p, tval_.p, tgrad_.p, stream_);
 
   const size_t nN = std::max(N_, 1), nF = std::max(F_, 1), nO = std::max<int64_t>(NO_, 1);
   pose_state_.alloc(nF);
@@ -423,6 +424,7 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
   a.tval = tval_.p;
+  a.tgrad = tgrad_.p;
   a.d0 = d0_.p;
   a.pose0 = pose0_.p;  // frozen IC poses (rows of the factored IC Jacobian)
   a.gamma = gamma;

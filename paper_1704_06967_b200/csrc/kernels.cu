@@ -500,17 +500,16 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         double m0 = 0.0, m1 = 0.0, m2 = 0.0;
         if (act && obs_ok) {
           const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
-          // template gradient image_gradient(ref, x) (image.cpp:36-49)
-          const double gu = rf.fx * x + rf.cx, gvp = rf.fy * y + rf.cy;
-          const bool grad_ok = in_bounds_px(gu - 0.5, gvp, rf.W, rf.H) && in_bounds_px(gu + 0.5, gvp, rf.W, rf.H) &&
-                               in_bounds_px(gu, gvp - 0.5, rf.W, rf.H) && in_bounds_px(gu, gvp + 0.5, rf.W, rf.H);
+          // template gradient image_gradient(ref, x) (image.cpp:36-49): computed once per (n, k)
+          // with the template values (solver.cpp:296-304), NaN when its footprint leaves the image
+          const double2 tg = __ldg(a.tgrad + static_cast<int64_t>(n) * P + k);
+          const bool grad_ok = !isnan(tg.x);
           double R0x[3];
           rot_ray(p0, x, y, R0x);
           const double vz0 = R0x[2] + dv * p0.t[2];
           if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
             bits |= 1u << k;
-            const double gxi = (bilinear(rf.img, rf.W, gu + 0.5, gvp) - bilinear(rf.img, rf.W, gu - 0.5, gvp)) * rf.fx;
-            const double gyi = (bilinear(rf.img, rf.W, gu, gvp + 0.5) - bilinear(rf.img, rf.W, gu, gvp - 0.5)) * rf.fy;
+            const double gxi = tg.x, gyi = tg.y;
             const double zbar0 = vz0 / dv;
             const double g30 = gxi / zbar0, g31 = gyi / zbar0, g32 = -(gxi * x + gyi * y) / zbar0;
             const double a0 = p0.R[0] * g30 + p0.R[1] * g31 + p0.R[2] * g32;
@@ -818,14 +817,27 @@ __global__ void __launch_bounds__(NT, kBsMinB) k_backsub(const BacksubArgs a) {
 
 // Template values tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template,
 // solver.cpp:33-53): fixed for the whole solve, computed once per handle.
-__global__ void k_template_values(int N, PatternD pat, FrameD ref, const double2* __restrict__ anc,
-                                  double* __restrict__ tval) {
+__global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_ifx, double ref_ify,
+                                  const double2* __restrict__ anc, double* __restrict__ tval,
+                                  double2* __restrict__ tgrad) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<int64_t>(N) * pat.P) return;
   const int n = static_cast<int>(e / pat.P), k = static_cast<int>(e % pat.P);
   const double pu = anc[n].x + static_cast<double>(pat.dx[k]);
   const double pv = anc[n].y + static_cast<double>(pat.dy[k]);
   tval[e] = bilinear(ref.img, ref.W, pu, pv);
+  // template gradient at to_pixel(to_normalized(px)) (solver.cpp:296-304, image.cpp:36-49), the
+  // same expressions the IC build used per pixel; NaN marks a footprint outside the image
+  const double x = (pu - ref.cx) * ref_ifx, y = (pv - ref.cy) * ref_ify;
+  const double gu = ref.fx * x + ref.cx, gvp = ref.fy * y + ref.cy;
+  const bool ok = in_bounds_px(gu - 0.5, gvp, ref.W, ref.H) && in_bounds_px(gu + 0.5, gvp, ref.W, ref.H) &&
+                  in_bounds_px(gu, gvp - 0.5, ref.W, ref.H) && in_bounds_px(gu, gvp + 0.5, ref.W, ref.H);
+  double2 g = make_double2(NAN, NAN);
+  if (ok) {
+    g.x = (bilinear(ref.img, ref.W, gu + 0.5, gvp) - bilinear(ref.img, ref.W, gu - 0.5, gvp)) * ref.fx;
+    g.y = (bilinear(ref.img, ref.W, gu, gvp + 0.5) - bilinear(ref.img, ref.W, gu, gvp - 0.5)) * ref.fy;
+  }
+  tgrad[e] = g;
 }
 
 // Bpm[o] = B[pm2fm[o]] (point-major copy of the frozen IC pose-depth blocks)
@@ -1542,6 +1554,9 @@ __global__ void __launch_bounds__(256) k_tri_inv_col(const double* __restrict__ 
 // Replaces ~3 launches per block column + the per-column inverse CTAs of the earlier path.
 // ---------------------------------------------------------------------------------
 constexpr int CI_THREADS = 256;
+#ifndef PBA_CI_PER_SM
+#define PBA_CI_PER_SM 1
+#endif
 
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& gen) {
   __syncthreads();
@@ -1880,10 +1895,11 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
 }
 
 void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const double2* anc, double* tval,
-                            cudaStream_t s) {
+                            double2* tgrad, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(N) * pat.P;
   if (n == 0) return;
-  k_template_values<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(N, pat, ref, anc, tval);
+  k_template_values<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(N, pat, ref, 1.0 / ref.fx, 1.0 / ref.fy, anc,
+                                                                       tval, tgrad);
   count_launches(1);
 }
 
@@ -1991,7 +2007,7 @@ int chol_inv_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_inv, CI_THREADS, 0);
-    return std::max(1, sms * std::max(1, std::min(per, 1)));
+    return std::max(1, sms * std::max(1, std::min(per, PBA_CI_PER_SM)));
   }();
   return g;
 }

@@ -128,6 +128,7 @@ Engine::Engine(const pba_problem* p) {
   if (F_ > 0 && (!p->targets || !p->pose_R || !p->pose_t)) throw PbaError(PBA_E_ARG, "missing frames");
   if (N_ > 0 && (!p->anchors_px || !p->inv_depths)) throw PbaError(PBA_E_ARG, "missing points");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  if (const char* e = std::getenv("PBA_TAB_MIN_OBS")) tab_min_obs_ = std::atoll(e);
   sh_.s = stream_;
   init_memory_pool();
   set_alloc_stream(stream_);
@@ -516,14 +517,22 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.mask_in = mask_in;
   a.active_out = active_out;
   a.Jm = J_.p;
-  build_frame_tabs(pose);  // host copy of the evaluation poses -> kernel-parameter frame tables
+  // Large problems read the frame-uniform records from kernel-parameter frame tables (one host
+  // read-back of the evaluation poses per pass); small, launch-bound ones keep the shared-memory
+  // path and avoid the mid-iteration synchronisation.
+  const bool use_tab = NO_ >= tab_min_obs_;
+  if (use_tab) build_frame_tabs(pose);
   auto e = ev_begin(PBA_K_OBS_PASS);
-  if (!side_) {
-    ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
-    ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "fork event");
-    ck(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "join event");
+  if (use_tab) {
+    if (!side_) {
+      ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+      ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "fork event");
+      ck(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "join event");
+    }
+    launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_, side_, fork_, join_);
+  } else {
+    launch_obs(OBS_IC, a, stream_);
   }
-  launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_, side_, fork_, join_);
   ev_end(PBA_K_OBS_PASS, e);
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
   e = ev_begin(PBA_K_REDUCE);

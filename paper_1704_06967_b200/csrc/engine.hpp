@@ -184,6 +184,7 @@ class Engine {
   PoseD* pe_h_ = nullptr;         // pinned: evaluation poses for the IC frame tables
   std::vector<PoseD> pose0_h_;    // host copy of the frozen IC poses
   std::vector<FrameTab> tabs_;    // IC pass frame tables (kernel parameters)
+  int64_t tab_min_obs_ = int64_t(1) << 20;  // frame tables from this many observations on (env PBA_TAB_MIN_OBS)
   cudaStream_t side_ = nullptr;   // second stream for the IC pass frame chunks
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<int32_t> ftile_ptr_h_;  // host copy of ov_.ftile_ptr

@@ -194,6 +194,7 @@ def _compare_runs(rg, ro, F, N):
 
 @pytest.mark.parametrize("solver_kind", ["ic", "fc"])
 def test_run_matches_oracle_c1(c1, solver_kind):
+    # C1 is small: the IC pass reads the frame records from shared memory (no frame tables)
     st = c1.state
     cfg = c1.cfg.solver_config()  # 10 LM iterations (BASELINE C1)
     g, o = pair(st)
@@ -357,7 +358,8 @@ def many_frames():
 
 
 @pytest.mark.parametrize("solver_kind", ["ic", "fc"])
-def test_run_matches_oracle_many_frames(many_frames, solver_kind):
+def test_run_matches_oracle_many_frames(many_frames, solver_kind, monkeypatch):
+    monkeypatch.setenv("PBA_TAB_MIN_OBS", "0")  # force the frame-table IC pass (large-problem path)
     st = many_frames.state
     cfg = many_frames.cfg.solver_config()
     g, o = pair(st)

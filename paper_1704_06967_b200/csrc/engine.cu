@@ -202,6 +202,7 @@ Engine::Engine(const pba_problem* p) {
   mask_[1].alloc(nO + 8);
   scratch_bits_.alloc(nO + 8);
   rec_.alloc(nO);
+  rec_g_.alloc(nO);
   s_n_.alloc(nN);
   dx_n_.alloc(nN);
   xp_.alloc(6 * nF);
@@ -517,6 +518,7 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.mask_in = mask_in;
   a.active_out = active_out;
   a.Jm = J_.p;
+  a.rec_g = rec_g_.p;
   // Large problems read the frame-uniform records from kernel-parameter frame tables (one host
   // read-back of the evaluation poses per pass); small, launch-bound ones keep the shared-memory
   // path and avoid the mid-iteration synchronisation.
@@ -535,6 +537,7 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   }
   ev_end(PBA_K_OBS_PASS, e);
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
+  pa.rec_g = rec_g_.p;
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
   const MaxUpdArgs mu = maxupd_args(pose_old, pose, d_old, d);

@@ -164,6 +164,7 @@ class Engine {
   DBuf<double> H_[2];             // 21F
   DBuf<double> gn_[2], gf_[2], rhs_[2];
   DBuf<double2> rec_;
+  DBuf<double> rec_g_;            // IC pass g_n terms (8 B per observation)
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;

@@ -553,7 +553,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     }
     if (live && sub == 0) {
       a.active_out[q] = bits;
-      a.rec[q] = make_double2(gnc, dc);
+      if (MODE == OBS_IC && a.rec_g) a.rec_g[q] = gnc;  // IC needs the g_n term only (D is frozen)
+      else a.rec[q] = make_double2(gnc, dc);
       if constexpr (kH) {
 #pragma unroll
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
@@ -862,7 +863,20 @@ __global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
     double gs = 0.0, ds = 0.0, Dn = 0.0;
     if (a.mode == PT_GRAD || a.mode == PT_RESCALE) Dn = a.D[np_];
     if (a.mode == PT_RESCALE) gs = a.g_n[np_];
-    if (a.mode != PT_RESCALE) {
+    if (a.mode == PT_GRAD && a.rec_g) {  // 8-byte g_n terms (IC)
+      double ag[kPPW] = {0.0, 0.0, 0.0, 0.0};
+      for (int64_t o0 = t.O0 + lane; o0 < t.Oe; o0 += 32 * kPtUnroll) {
+        double rg[kPtUnroll];
+#pragma unroll
+        for (int u = 0; u < kPtUnroll; ++u) {
+          const int64_t o = o0 + 32 * u;
+          rg[u] = o < t.Oe ? a.rec_g[a.ov.pm2fm[o]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPtUnroll; ++u) seg_add(ag, t, o0 + 32 * u, rg[u]);
+      }
+      gs = seg_reduce(ag, lane);
+    } else if (a.mode != PT_RESCALE) {
       double ag[kPPW] = {0.0, 0.0, 0.0, 0.0}, ad[kPPW] = {0.0, 0.0, 0.0, 0.0};
       for (int64_t o0 = t.O0 + lane; o0 < t.Oe; o0 += 32 * kPtUnroll) {
         double2 rc[kPtUnroll];

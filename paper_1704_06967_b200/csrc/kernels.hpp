@@ -49,6 +49,7 @@ struct ObsArgs {
   const double* d0;            // N: frozen depths of the IC build (IC / REFRESH)
   double* B_out;               // NO*6 (FC/BUILD/REFRESH)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
+  double* rec_g;               // NO or null: IC pass g_n terms only (sum_k Jd w r)
   double* partial;             // ntiles * PT_STRIDE
 };
 
@@ -118,6 +119,7 @@ struct PointArgs {
   double lambda;          // damping used for s_n
   double* s_n;            // N out: g_n / (D_n + lambda)
   double* partial;        // nblocks * 2 {sum g_n^2, 0}
+  const double* rec_g = nullptr;  // NO or null: PT_GRAD reads these 8-byte g_n terms instead of rec
 };
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);

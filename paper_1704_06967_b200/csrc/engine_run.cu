@@ -62,6 +62,10 @@ void Engine::backsub(bool ic, const double* B, const double* D, const double* g_
   a.gauge_scale = gauge_.p;
   a.gauge_enabled = run_.cfg.normalize_depth_gauge ? 1 : 0;
   const auto e = ev_begin(PBA_K_REDUCE);
+  if (!a.Bpm) {  // frame-major blocks: dots first (coalesced), then the point-major 8-byte gather
+    launch_bdot(ov_, B, xp_.p, rec_g_.p, stream_);
+    a.tq = rec_g_.p;
+  }
   launch_backsub(a, stream_);
   ev_end(PBA_K_REDUCE, e);
 }

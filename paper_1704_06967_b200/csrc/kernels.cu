@@ -780,7 +780,18 @@ __global__ void __launch_bounds__(NT, kBsMinB) k_backsub(const BacksubArgs a) {
             if (seg == p) acc[p] += v;
         }
       }
-    } else {  // FC: gather the frame-major blocks
+    } else if (a.tq) {  // FC: per-observation dots B_nf . xp_f from the frame-major k_bdot sweep
+      for (int64_t o0 = t.O0 + lane; o0 < t.Oe; o0 += 32 * 4) {
+        double tv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t o = o0 + 32 * u;
+          tv[u] = o < t.Oe ? a.tq[a.ov.pm2fm[o]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) seg_add(acc, t, o0 + 32 * u, tv[u]);
+      }
+    } else {  // gather the frame-major blocks
       for (int64_t o = t.O0 + lane; o < t.Oe; o += 32) {
         const int f = a.ov.pm_frame[o];
         const double* b = a.B + static_cast<int64_t>(a.ov.pm2fm[o]) * 6;
@@ -813,6 +824,29 @@ __global__ void __launch_bounds__(NT, kBsMinB) k_backsub(const BacksubArgs a) {
       const double mean = v / static_cast<double>(a.ov.N);
       *a.gauge_scale = (a.gauge_enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
     }
+  }
+}
+
+// k_bdot: tq[q] = B_q . xp_f over the frame-major tiles (coalesced B; xp_f frame-uniform)
+__global__ void __launch_bounds__(NT) k_bdot(const ObsView ov, const double* __restrict__ B,
+                                             const double* __restrict__ xp, double* __restrict__ tq) {
+  const int t = blockIdx.x;
+  const int f = ov.tile_frame[t];
+  const int64_t q0 = ov.tile_q0[t], q1 = ov.tile_q1[t];
+  double x[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) x[c] = __ldg(xp + 6 * f + c);
+  const double2* __restrict__ B2 = reinterpret_cast<const double2*>(B);
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += NT) {
+    const double2 b0 = __ldcs(B2 + 3 * q), b1 = __ldcs(B2 + 3 * q + 1), b2 = __ldcs(B2 + 3 * q + 2);
+    double dot = 0.0;
+    dot += b0.x * x[0];
+    dot += b0.y * x[1];
+    dot += b1.x * x[2];
+    dot += b1.y * x[3];
+    dot += b2.x * x[4];
+    dot += b2.y * x[5];
+    tq[q] = dot;
   }
 }
 
@@ -1890,6 +1924,12 @@ static int reduce_blocks(int N, int minb) {
 }
 int backsub_blocks(int N) { return reduce_blocks(N, kBsMinB); }
 int point_blocks(int N) { return reduce_blocks(N, kPtMinB); }
+
+void launch_bdot(const ObsView& ov, const double* B, const double* xp, double* tq, cudaStream_t s) {
+  if (ov.ntiles == 0) return;
+  k_bdot<<<ov.ntiles, NT, 0, s>>>(ov, B, xp, tq);
+  count_launches(1);
+}
 
 void launch_backsub(const BacksubArgs& a, cudaStream_t s) {
   const int nb = backsub_blocks(a.ov.N);

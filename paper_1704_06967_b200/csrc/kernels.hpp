@@ -99,6 +99,7 @@ struct BacksubArgs {
   unsigned int* ticket;   // grid ticket (zero between launches)
   double* gauge_scale;    // out: mean of d_cand (1 when disabled / not positive-finite)
   int gauge_enabled;
+  const double* tq = nullptr;  // NO or null: per-observation B_nf . xp_f (k_bdot) instead of B / Bpm
 };
 int backsub_blocks(int N);
 // tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template, solver.cpp:33-53)
@@ -107,6 +108,8 @@ void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const
                             double2* tgrad, cudaStream_t s);
 void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s);
 void launch_backsub(const BacksubArgs& a, cudaStream_t s);
+// tq[q] = B_q . xp_f over the frame-major observations (FC back-substitution without B gathers)
+void launch_bdot(const ObsView& ov, const double* B, const double* xp, double* tq, cudaStream_t s);
 
 // Point-major gather of the per-observation records.
 enum PointMode : int { PT_GRAD = 0, PT_FCH = 1, PT_DONLY = 2, PT_RESCALE = 3 };

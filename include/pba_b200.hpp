@@ -112,6 +112,23 @@ struct EnergyResult {
 };
 
 namespace detail {
+// every warning in one call (pba_gpu_warnings_text): large problems can carry one per point
+inline std::vector<std::string> all_warnings(const pba_handle* h) {
+  std::vector<std::string> w;
+  if (pba_gpu_warning_count(h) == 0) return w;
+  const int64_t n = pba_gpu_warnings_text(h, nullptr, 0);
+  std::string buf(static_cast<size_t>(n) + 1, '\0');
+  pba_gpu_warnings_text(h, buf.data(), n + 1);
+  buf.resize(static_cast<size_t>(n));
+  size_t a = 0;
+  while (a <= buf.size()) {
+    const size_t b = buf.find('\n', a);
+    w.emplace_back(buf.substr(a, b == std::string::npos ? std::string::npos : b - a));
+    if (b == std::string::npos) break;
+    a = b + 1;
+  }
+  return w;
+}
 struct Handle {
   pba_handle* h{nullptr};
   int F{0}, N{0}, P{0};
@@ -209,12 +226,7 @@ struct Handle {
       }
       out.iters.push_back(std::move(s));
     }
-    const int nw = pba_gpu_warning_count(h);
-    for (int i = 0; i < nw; ++i) {
-      char buf[512];
-      pba_gpu_warning(h, i, buf, sizeof buf);
-      out.warnings.emplace_back(buf);
-    }
+    out.warnings = all_warnings(h);
     return out;
   }
 };
@@ -273,15 +285,7 @@ class IcSolver {
                                  H.pose_depth.empty() ? nullptr : H.pose_depth[0].data(), &H.lambda));
     return H;
   }
-  std::vector<std::string> warnings() const {
-    std::vector<std::string> w;
-    for (int i = 0; i < pba_gpu_warning_count(h_->h); ++i) {
-      char buf[512];
-      pba_gpu_warning(h_->h, i, buf, sizeof buf);
-      w.emplace_back(buf);
-    }
-    return w;
-  }
+  std::vector<std::string> warnings() const { return detail::all_warnings(h_->h); }
 
  private:
   std::unique_ptr<detail::Handle> h_;

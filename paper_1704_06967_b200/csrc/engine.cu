@@ -668,7 +668,17 @@ void Engine::ic_build(const pba_config* cfg) {
                              ": zero initial translation, inverse depth unobservable from this frame");
   }
   const size_t nO = std::max<int64_t>(NO_, 1);
-  J_.alloc(static_cast<size_t>(std::max<int64_t>(jm_doubles(NO_, P_), 1)));  // factored rows m (k_obs_lane)
+  {  // Frozen IC rows: rebuilt in every pass from the per-(point, pixel) template gradients (no
+     // per-pixel store; the pass is not HBM-bound, so this costs no time and saves 24 B/px of HBM),
+     // or, PBA_IC_RECOMPUTE=0, stored factored as m (24 B per pixel) when that fits comfortably.
+    const size_t jm_bytes = static_cast<size_t>(std::max<int64_t>(jm_doubles(NO_, P_), 1)) * sizeof(double);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const char* env = std::getenv("PBA_IC_RECOMPUTE");
+    const bool store = env && env[0] == '0' && jm_bytes <= free_b / 3;
+    if (store) J_.alloc(jm_bytes / sizeof(double));
+    else J_.release();
+  }
   Bic_.alloc(6 * nO);
   Dic_.alloc(std::max(N_, 1));
   Hic_.alloc(21 * std::max(F_, 1));

@@ -264,6 +264,7 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #ifndef PBA_IC_MINB
 #define PBA_IC_MINB 3
 #endif
+
 #ifndef PBA_LANE_PREFETCH
 #define PBA_LANE_PREFETCH 1
 #endif
@@ -318,6 +319,43 @@ __device__ __forceinline__ void rot_ray(const PoseD& p0, double x, double y, dou
 #pragma unroll
   for (int i = 0; i < 3; ++i) R0x[i] = fma(p0.R[3 * i], x, fma(p0.R[3 * i + 1], y, p0.R[3 * i + 2]));
 }
+// m of the closed-form IC row (solver.cpp:331-349) from the frozen template gradient (gx, gy) of
+// the pixel, its ray (x, y), the frozen frame pose p0 and the frozen depth d0.  The build and
+// every consumer evaluate this same function, so the rebuilt rows are bitwise the build's rows.
+// m = zbar0 a - (0, 0, a.t0) with a = R0 g3 / zbar0 and g3 = (gx, gy, -(gx x + gy y)):
+// zbar0 cancels in the first term, m = R0 g3 - (0, 0, (R0 g3).t0 d0 / vz0) (one division;
+// equal to the reference's order of operations up to roundoff).
+__device__ __forceinline__ void ic_m(const PoseD& p0, const double (&R0x)[3], double d0, double x, double y,
+                                     double gxi, double gyi, double& m0, double& m1, double& m2) {
+  const double vz0 = R0x[2] + d0 * p0.t[2];
+  const double g32 = -(gxi * x + gyi * y);
+  const double h0 = p0.R[0] * gxi + p0.R[1] * gyi + p0.R[2] * g32;
+  const double h1 = p0.R[3] * gxi + p0.R[4] * gyi + p0.R[5] * g32;
+  const double h2 = p0.R[6] * gxi + p0.R[7] * gyi + p0.R[8] * g32;
+  const double hdt = h0 * p0.t[0] + h1 * p0.t[1] + h2 * p0.t[2];
+  m0 = h0;
+  m1 = h1;
+  m2 = h2 - hdt * (d0 / vz0);
+}
+__device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], double d0, double m0, double m1,
+                                       double m2, double (&row)[7]);
+// the frozen row of pixel k: read from the stored m (blocked layout, jm = the observation's block
+// base) or, kRecompute (no store: large problems), rebuilt from the frozen template gradient
+template <bool kRecompute>
+__device__ __forceinline__ void ic_jrow(const PoseD& p0, const double (&R0x)[3], double d0, double x, double y,
+                                        const double2* __restrict__ tg, int k, const double* __restrict__ jm, int P,
+                                        double (&row)[7]) {
+  double m0, m1, m2;
+  if (kRecompute) {
+    const double2 g = __ldg(tg + k);
+    ic_m(p0, R0x, d0, x, y, g.x, g.y, m0, m1, m2);
+  } else {
+    m0 = __ldg(jm + k * 32);
+    m1 = __ldg(jm + (P + k) * 32);
+    m2 = __ldg(jm + (2 * P + k) * 32);
+  }
+  ic_row(p0, R0x, d0, m0, m1, m2, row);
+}
 __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], double d0, double m0, double m1,
                                        double m2, double (&row)[7]) {
   row[0] = fma(R0x[1], m2, -(R0x[2] * m1));
@@ -333,7 +371,7 @@ __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], 
 // kernel-parameter table (constant bank, read through the constant cache) instead of shared
 // memory: the per-pixel re-reads of the pose then cost no L1 data-pipe wavefronts, which
 // bound the shared-memory variant.
-template <int MODE, int PT, int LPO, bool kTab>
+template <int MODE, int PT, int LPO, bool kTab, bool kRc>
 __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& tab) {
   static_assert(LPO == 1 || (PT > 0 && PT % LPO == 0), "LPO lanes split a compile-time pattern evenly");
   constexpr int OPB = NT / LPO;  // observations per block step
@@ -368,7 +406,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     if (threadIdx.x == 32) l2_prefetch(a.ov.fm_point + qs, (qe - qs) * sizeof(int32_t));
     if (threadIdx.x == 64 && a.mask_in && (MODE == OBS_IC || MODE == OBS_REFRESH))
       l2_prefetch(a.mask_in + qs, (qe - qs) * sizeof(uint32_t));
-    if (threadIdx.x == 96 && (MODE == OBS_IC || MODE == OBS_REFRESH)) {
+    if (threadIdx.x == 96 && !kRc && (MODE == OBS_IC || MODE == OBS_REFRESH)) {
       const int64_t b0 = jm_index(qs, 0, 0, P), b1 = jm_index(qe - 1, 0, 0, P) - ((qe - 1) & 31) + 3 * P * 32;
       l2_prefetch(a.Jm + b0 - (qs & 31), (b1 - (b0 - (qs & 31))) * sizeof(double));
     }
@@ -390,7 +428,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     const uint32_t mbits = !live ? 0u
                            : ((MODE == OBS_IC || MODE == OBS_REFRESH) && a.mask_in ? a.mask_in[q] : 0xffffffffu);
     const double d0n = (MODE == OBS_IC || MODE == OBS_REFRESH) ? __ldg(&a.d0[n]) : dv;
-    const double* jm = (MODE == OBS_FC) ? nullptr : a.Jm + jm_index(qc, 0, 0, P);
+    const double* jm = (MODE == OBS_FC || kRc) ? nullptr : a.Jm + jm_index(qc, 0, 0, P);
+    const double2* tv_g = a.tgrad + static_cast<int64_t>(n) * P;  // frozen template gradients of the point
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
     uint32_t bits = 0u;
@@ -440,7 +479,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
-            ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
+            ic_jrow<kRc>(p0, R0x, d0n, x, y, tv_g, k, jm, P, row);
 #pragma unroll
             for (int c = 0; c < 6; ++c) gacc[c] += row[c] * wr;
             gnc += row[6] * wr;
@@ -449,7 +488,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
-            ic_row(p0, R0x, d0n, __ldg(jm + k * 32), __ldg(jm + (P + k) * 32), __ldg(jm + (2 * P + k) * 32), row);
+            ic_jrow<kRc>(p0, R0x, d0n, x, y, tv_g, k, jm, P, row);
             const double w = huber_weight(r, gam);
             int h = 0;
 #pragma unroll
@@ -509,16 +548,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           const double vz0 = R0x[2] + dv * p0.t[2];
           if (grad_ok && !(vz0 < kDegenerateDepthEps)) {
             bits |= 1u << k;
-            const double gxi = tg.x, gyi = tg.y;
-            const double zbar0 = vz0 / dv;
-            const double g30 = gxi / zbar0, g31 = gyi / zbar0, g32 = -(gxi * x + gyi * y) / zbar0;
-            const double a0 = p0.R[0] * g30 + p0.R[1] * g31 + p0.R[2] * g32;
-            const double a1 = p0.R[3] * g30 + p0.R[4] * g31 + p0.R[5] * g32;
-            const double a2 = p0.R[6] * g30 + p0.R[7] * g31 + p0.R[8] * g32;
-            const double adt = a0 * p0.t[0] + a1 * p0.t[1] + a2 * p0.t[2];
-            m0 = zbar0 * a0;
-            m1 = zbar0 * a1;
-            m2 = zbar0 * a2 - adt;
+            ic_m(p0, R0x, dv, x, y, tg.x, tg.y, m0, m1, m2);
             double row[7];
             ic_row(p0, R0x, dv, m0, m1, m2, row);
             const double w = huber_weight(r, gam);  // W0 (solver.cpp:279)
@@ -533,10 +563,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             dc += w * row[6] * row[6];
           }
         }
-        double* jw = a.Jmw + jm_index(q, 0, k, P);
-        jw[0] = m0;
-        jw[P * 32] = m1;
-        jw[2 * P * 32] = m2;
+        if (a.Jmw) {  // store m unless the consumers rebuild it
+          double* jw = a.Jmw + jm_index(q, 0, k, P);
+          jw[0] = m0;
+          jw[P * 32] = m1;
+          jw[2 * P * 32] = m2;
+        }
       }
     }
     if constexpr (LPO > 1) {  // per-observation sums over the LPO lanes of the observation
@@ -591,12 +623,18 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
 template <int MODE, int PT, int LPO>
 __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
   const FrameTab* none = nullptr;
-  obs_lane_body<MODE, PT, LPO, false>(a, *none);
+  if (MODE == OBS_IC || MODE == OBS_REFRESH) {
+    if (a.Jm) obs_lane_body<MODE, PT, LPO, false, false>(a, *none);
+    else obs_lane_body<MODE, PT, LPO, false, true>(a, *none);
+  } else {
+    obs_lane_body<MODE, PT, LPO, false, false>(a, *none);
+  }
 }
 template <int MODE, int PT, int LPO>
 __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB)
     k_obs_lane_tab(const ObsArgs a, const FrameTab tab) {
-  obs_lane_body<MODE, PT, LPO, true>(a, tab);
+  if (a.Jm) obs_lane_body<MODE, PT, LPO, true, false>(a, tab);
+  else obs_lane_body<MODE, PT, LPO, true, true>(a, tab);
 }
 
 // ---------------------------------------------------------------------------------

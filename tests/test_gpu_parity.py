@@ -367,6 +367,15 @@ def test_run_matches_oracle_many_frames(many_frames, solver_kind, monkeypatch):
     _compare_runs(rg, ro, st.num_frames, st.num_points)
 
 
+def test_ic_run_stored_rows_match_oracle(c1, monkeypatch):
+    # the alternative layout: the build stores the factored rows m and the passes read them
+    monkeypatch.setenv("PBA_IC_RECOMPUTE", "0")
+    st = c1.state
+    cfg = c1.cfg.solver_config()
+    g, o = pair(st)
+    _compare_runs(g.ic_run(cfg), o.ic_run(cfg), st.num_frames, st.num_points)
+
+
 def test_ic_run_refresh_hessian_matches_oracle(c1):  # refresh_ic_hessian (solver.cpp:505-531)
     st = c1.state
     cfg = c1.cfg.solver_config(max_iters=5, refresh_ic_hessian=True)

@@ -172,7 +172,7 @@ class Engine {
   DBuf<unsigned int> ticket_;     // grid tickets {k_backsub, k_finalize}, k_chol_inv barrier {count, generation}
   DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
-  DBuf<int32_t> chunk_pts_;
+  DBuf<int32_t> chunk_pts_, schur_chunk_of_;
   DBuf<int4> schur_blocks_, schur_chunks_;
   DBuf<int64_t> schur_chunk_off_;
   DBuf<double> schur_dense_, schur_wsort_;

@@ -4,6 +4,7 @@
 // plan.  Sorting uses CUB radix sorts (stable), everything else is gather/scatter
 // kernels, so handle creation costs milliseconds even at 4*10^7 observations.
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <cstring>
 #include <numeric>
@@ -145,21 +146,6 @@ __global__ void k_window_keys(int N, const int64_t* __restrict__ pm_ptr, const i
   const int64_t a = pm_ptr[i], b = pm_ptr[i + 1];
   key[i] = (b > a) ? (static_cast<uint32_t>(pm_frame[a]) << 16) | static_cast<uint32_t>(pm_frame[b - 1]) : 0xffffffffu;
   idx[i] = i;
-}
-
-__global__ void k_chunk_windows(int nchunks, int npts, int chunk, const int32_t* __restrict__ order,
-                                const int64_t* __restrict__ pm_ptr, const int32_t* __restrict__ pm_frame,
-                                int2* __restrict__ win) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nchunks) return;
-  const int p0 = c * chunk, p1 = min(npts, p0 + chunk);
-  int fmin = 1 << 30, fmax = -1;
-  for (int p = p0; p < p1; ++p) {
-    const int n = order[p];
-    fmin = min(fmin, pm_frame[pm_ptr[n]]);
-    fmax = max(fmax, pm_frame[pm_ptr[n + 1] - 1]);
-  }
-  win[c] = make_int2(fmin, fmax);
 }
 
 // ---- caller-order <-> frame-major conversions of per-observation arrays ----
@@ -380,10 +366,16 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
   }
 
   trace_mark(s, "layout: tiles");
-  // ---- Schur chunk plan: points sorted by visibility window (first, last frame), chunks of
-  //      kChunk points; one work item per 64x64 upper tile-block of each chunk's window ----
+  // ---- Schur chunk plan: points sorted by visibility window (first frame, last frame) and cut
+  //      greedily into chunks whose union window keeps the padded width LD = roundup(6 W, 64) of
+  //      the chunk's first window (so merging windows costs no extra DMMA columns), up to
+  //      kMaxChunk points; one work item per 64x64 upper tile-block of each chunk's window.
+  //      Long chunks mean long K loops and few fixed-point folds of each tile into S. ----
   {
-    constexpr int kChunk = 512;
+    const int kMaxChunk = [] {
+      const char* e = std::getenv("PBA_SCHUR_CHUNK");
+      return e ? std::max(32, std::atoi(e)) : 4096;
+    }();
     DBuf<uint32_t> wkey, wkey_sorted;
     DBuf<int32_t> widx;
     wkey.alloc(std::max(N_, 1));
@@ -396,43 +388,47 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
       k_window_keys<<<(N_ + 255) / 256, 256, 0, s>>>(N_, pm_ptr_.p, pm_frame_.p, wkey.p, widx.p);
       count_launches(1);
       radix_sort_pairs(wkey.p, wkey_sorted.p, widx.p, chunk_pts_.p, N_, 32, s);
-      std::vector<int64_t> cnt_h(N_ + 1);
-      // number of points with observations = N - #empty (empty keys sort last)
-      ck(cudaMemcpy(cnt_h.data(), pm_ptr_.p, (N_ + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "pm_ptr");
-      for (int i = 0; i < N_; ++i) npts += cnt_h[i + 1] > cnt_h[i] ? 1 : 0;
-      const int nchunks = (npts + kChunk - 1) / kChunk;
-      DBuf<int2> win;
-      win.alloc(std::max(nchunks, 1));
-      if (nchunks > 0) {
-        k_chunk_windows<<<(nchunks + 127) / 128, 128, 0, s>>>(nchunks, npts, kChunk, chunk_pts_.p, pm_ptr_.p,
-                                                              pm_frame_.p, win.p);
-        count_launches(1);
-      }
-      std::vector<int2> w(nchunks);
-      if (nchunks > 0)
-        ck(cudaMemcpyAsync(w.data(), win.p, nchunks * sizeof(int2), cudaMemcpyDeviceToHost, s), "win");
-      ck(cudaStreamSynchronize(s), "win sync");
-      std::vector<int4> chunks(nchunks);
-      std::vector<int64_t> off(nchunks);
+      std::vector<uint32_t> keys(N_);
+      ck(cudaMemcpy(keys.data(), wkey_sorted.p, N_ * sizeof(uint32_t), cudaMemcpyDeviceToHost), "window keys");
+      // points without observations carry key 0xffffffff and sort last
+      while (npts < N_ && keys[npts] != 0xffffffffu) ++npts;
+      std::vector<int4> chunks;
+      std::vector<int64_t> off;
+      std::vector<int32_t> chunk_of(std::max(npts, 1));
       int64_t total = 0;
-      for (int c = 0; c < nchunks; ++c) {
-        const int fmin = w[c].x, W = w[c].y - w[c].x + 1;
-        const int LD = ((6 * W + 63) / 64) * 64;
+      for (int p = 0; p < npts;) {
+        int fmin = static_cast<int>(keys[p] >> 16), fmax = static_cast<int>(keys[p] & 0xffffu);
+        const int LD = ((6 * (fmax - fmin + 1) + 63) / 64) * 64;
+        int q = p + 1;
+        while (q < npts && q - p < kMaxChunk) {
+          const int a0 = std::min(fmin, static_cast<int>(keys[q] >> 16));
+          const int a1 = std::max(fmax, static_cast<int>(keys[q] & 0xffffu));
+          if (6 * (a1 - a0 + 1) > LD) break;
+          fmin = a0;
+          fmax = a1;
+          ++q;
+        }
         const int nb = LD / 64;
         if (nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
-        const int c0 = c * kChunk, c1 = std::min(npts, c0 + kChunk);
-        chunks[c] = make_int4(c0, c1, fmin, LD);
-        off[c] = total;
-        total += static_cast<int64_t>(c1 - c0) * LD;
+        const int c = static_cast<int>(chunks.size());
+        chunks.push_back(make_int4(p, q, fmin, LD));
+        off.push_back(total);
+        total += static_cast<int64_t>(q - p) * LD;
+        for (int i = p; i < q; ++i) chunk_of[i] = c;
         for (int rb = 0; rb < nb; ++rb)
           for (int cb = rb; cb < nb; ++cb) sblocks.push_back(make_int4(c, 0, 0, rb | (cb << 16)));
+        p = q;
       }
+      const int nchunks = static_cast<int>(chunks.size());
       schur_chunks_.alloc(std::max(nchunks, 1));
       schur_chunk_off_.alloc(std::max(nchunks, 1));
+      schur_chunk_of_.alloc(std::max(npts, 1));
       if (nchunks > 0) {
         ck(cudaMemcpyAsync(schur_chunks_.p, chunks.data(), nchunks * sizeof(int4), cudaMemcpyHostToDevice, s), "chunks");
         ck(cudaMemcpyAsync(schur_chunk_off_.p, off.data(), nchunks * sizeof(int64_t), cudaMemcpyHostToDevice, s),
            "chunk off");
+        ck(cudaMemcpyAsync(schur_chunk_of_.p, chunk_of.data(), npts * sizeof(int32_t), cudaMemcpyHostToDevice, s),
+           "chunk of");
       }
       schur_dense_elems_ = total;
       ck(cudaStreamSynchronize(s), "chunks sync");
@@ -442,8 +438,8 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
       ck(cudaMemcpyAsync(schur_blocks_.p, sblocks.data(), sblocks.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
          "blocks");
     ck(cudaStreamSynchronize(s), "plan sync");
-    schur_plan_ = SchurPlan{chunk_pts_.p, npts, schur_chunks_.p, schur_chunk_off_.p, nullptr, nullptr, schur_blocks_.p,
-                            static_cast<int>(sblocks.size())};
+    schur_plan_ = SchurPlan{chunk_pts_.p, npts, schur_chunk_of_.p, schur_chunks_.p, schur_chunk_off_.p, nullptr,
+                            nullptr, schur_blocks_.p, static_cast<int>(sblocks.size())};
   }
 
   trace_mark(s, "layout: schur plan");

@@ -1278,7 +1278,6 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
 // K-looping over the chunk's points through shared memory.  8 warps x 8 DMMA 8x8 tiles.
 // Results enter S through the same deterministic fixed-point RED as k_schur_pts.
 constexpr int SCH_TB = 64;   // tile-block edge (window-local dimensions)
-constexpr int SCH_CHUNK = 512;  // points per chunk (must match the host plan)
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -1290,11 +1289,12 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // frame window (zero where the point does not observe a frame), LD_c = roundup(6 W_c, 64).
 __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const double* __restrict__ B,
                                                        const int32_t* __restrict__ chunk_pts, int npts,
+                                                       const int32_t* __restrict__ chunk_of,
                                                        const int4* __restrict__ chunks,
                                                        const int64_t* __restrict__ chunk_off, double* __restrict__ dense) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= npts) return;
-  const int c = warp / SCH_CHUNK;
+  const int c = chunk_of[warp];
   const int4 ch = chunks[c];  // {begin, end, fmin, LD}
   const int fmin = ch.z, LD = ch.w;
   double* row = dense + chunk_off[c] + static_cast<int64_t>(warp - ch.x) * LD;
@@ -2047,7 +2047,8 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
   int launched = 2;
   if (dense) {
     if (densify) {
-      k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, plan->chunk_pts, plan->npts, plan->chunks,
+      k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, plan->chunk_pts, plan->npts, plan->chunk_of,
+                                                                    plan->chunks,
                                                                     plan->chunk_off, plan->dense);
       ++launched;
     }

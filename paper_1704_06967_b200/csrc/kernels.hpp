@@ -194,6 +194,7 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
 struct SchurPlan {
   const int32_t* chunk_pts;  // internal point ids in window order (points with observations)
   int npts;
+  const int32_t* chunk_of;   // npts: chunk of the p-th window-sorted point
   const int4* chunks;        // per chunk {begin, end, fmin, LD = roundup(6 W, 64)}
   const int64_t* chunk_off;  // per chunk offset (doubles) of its dense [points x LD] block
   double* dense;             // densified blocks b_n (scratch; valid while B is unchanged)

@@ -145,7 +145,7 @@ class Engine {
   DBuf<FrameD> frames_;
   DBuf<double2> anchor_, anchor_fm_;
   DBuf<double> tval_;             // template values N*P
-  DBuf<double2> tgrad_;           // template gradients N*P (IC build)
+  DBuf<double4> tgrad_;           // template records {tval, gx, gy, 0} N*P (IC passes)
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
   DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
   DBuf<int32_t> uo2q_d_;         // caller obs -> frame-major obs q

@@ -314,6 +314,13 @@ __device__ __forceinline__ FrameL lds_frame(const FrameD& s) {
   return f;
 }
 
+// one 256-bit read-only load (LDG.256) of a template record
+__device__ __forceinline__ double4 ld_tpl(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 // R0 x_k for the pixel ray (x, y, 1), explicit fused order shared by build and consumers
 __device__ __forceinline__ void rot_ray(const PoseD& p0, double x, double y, double (&R0x)[3]) {
 #pragma unroll
@@ -323,7 +330,7 @@ __device__ __forceinline__ void rot_ray(const PoseD& p0, double x, double y, dou
 // the pixel, its ray (x, y), the frozen frame pose p0 and the frozen depth d0.  The build and
 // every consumer evaluate this same function, so the rebuilt rows are bitwise the build's rows.
 // m = zbar0 a - (0, 0, a.t0) with a = R0 g3 / zbar0 and g3 = (gx, gy, -(gx x + gy y)):
-// zbar0 cancels in the first term, m = R0 g3 - (0, 0, (R0 g3).t0 d0 / vz0) (one division;
+// zbar0 cancels in the first term, m = R0 g3 - (0, 0, (R0 g3).t0 d0 / vz0) (one reciprocal;
 // equal to the reference's order of operations up to roundoff).
 __device__ __forceinline__ void ic_m(const PoseD& p0, const double (&R0x)[3], double d0, double x, double y,
                                      double gxi, double gyi, double& m0, double& m1, double& m2) {
@@ -335,7 +342,7 @@ __device__ __forceinline__ void ic_m(const PoseD& p0, const double (&R0x)[3], do
   const double hdt = h0 * p0.t[0] + h1 * p0.t[1] + h2 * p0.t[2];
   m0 = h0;
   m1 = h1;
-  m2 = h2 - hdt * (d0 / vz0);
+  m2 = h2 - hdt * (d0 * rcp_nr(vz0));  // |vz0| >= 1e-12 (degenerate pixels are masked at the build)
 }
 __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], double d0, double m0, double m1,
                                        double m2, double (&row)[7]);
@@ -343,12 +350,11 @@ __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], 
 // base) or, kRecompute (no store: large problems), rebuilt from the frozen template gradient
 template <bool kRecompute>
 __device__ __forceinline__ void ic_jrow(const PoseD& p0, const double (&R0x)[3], double d0, double x, double y,
-                                        const double2* __restrict__ tg, int k, const double* __restrict__ jm, int P,
+                                        double gx, double gy, int k, const double* __restrict__ jm, int P,
                                         double (&row)[7]) {
   double m0, m1, m2;
   if (kRecompute) {
-    const double2 g = __ldg(tg + k);
-    ic_m(p0, R0x, d0, x, y, g.x, g.y, m0, m1, m2);
+    ic_m(p0, R0x, d0, x, y, gx, gy, m0, m1, m2);
   } else {
     m0 = __ldg(jm + k * 32);
     m1 = __ldg(jm + (P + k) * 32);
@@ -429,7 +435,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
                            : ((MODE == OBS_IC || MODE == OBS_REFRESH) && a.mask_in ? a.mask_in[q] : 0xffffffffu);
     const double d0n = (MODE == OBS_IC || MODE == OBS_REFRESH) ? __ldg(&a.d0[n]) : dv;
     const double* jm = (MODE == OBS_FC || kRc) ? nullptr : a.Jm + jm_index(qc, 0, 0, P);
-    const double2* tv_g = a.tgrad + static_cast<int64_t>(n) * P;  // frozen template gradients of the point
+    const double4* tpl = a.tgrad + static_cast<int64_t>(n) * P;  // frozen {tval, gx, gy} of the point
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
     uint32_t bits = 0u;
@@ -453,6 +459,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       const double y = (pv - rf.cy) * a.ref_ify;
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
+      double4 T = make_double4(0.0, NAN, NAN, 0.0);  // template record {tval, gx, gy} (non-FC modes)
       const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
       const FrameL fr = kTab ? tab_frame(tab.r[f - tab.f0]) : lds_frame(s_fr);
       if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
@@ -467,7 +474,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           if constexpr (MODE == OBS_FC) {
             r = __ldg(tv + k) - bilinear_grad<true>(fr.img, fr.W, u, v, gdu, gdv);  // + image_gradient taps
           } else {
-            r = __ldg(tv + k) - bilinear(fr.img, fr.W, u, v);
+            T = ld_tpl(tpl + k);
+            r = T.x - bilinear(fr.img, fr.W, u, v);
           }
           act = true;
           energy += huber_loss(r, gam);
@@ -479,7 +487,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
-            ic_jrow<kRc>(p0, R0x, d0n, x, y, tv_g, k, jm, P, row);
+            ic_jrow<kRc>(p0, R0x, d0n, x, y, T.y, T.z, k, jm, P, row);
 #pragma unroll
             for (int c = 0; c < 6; ++c) gacc[c] += row[c] * wr;
             gnc += row[6] * wr;
@@ -488,7 +496,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
-            ic_jrow<kRc>(p0, R0x, d0n, x, y, tv_g, k, jm, P, row);
+            ic_jrow<kRc>(p0, R0x, d0n, x, y, T.y, T.z, k, jm, P, row);
             const double w = huber_weight(r, gam);
             int h = 0;
 #pragma unroll
@@ -541,7 +549,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
           // template gradient image_gradient(ref, x) (image.cpp:36-49): computed once per (n, k)
           // with the template values (solver.cpp:296-304), NaN when its footprint leaves the image
-          const double2 tg = __ldg(a.tgrad + static_cast<int64_t>(n) * P + k);
+          const double2 tg = make_double2(T.y, T.z);
           const bool grad_ok = !isnan(tg.x);
           double R0x[3];
           rot_ray(p0, x, y, R0x);
@@ -892,7 +900,7 @@ __global__ void __launch_bounds__(NT) k_bdot(const ObsView ov, const double* __r
 // solver.cpp:33-53): fixed for the whole solve, computed once per handle.
 __global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_ifx, double ref_ify,
                                   const double2* __restrict__ anc, double* __restrict__ tval,
-                                  double2* __restrict__ tgrad) {
+                                  double4* __restrict__ tgrad) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<int64_t>(N) * pat.P) return;
   const int n = static_cast<int>(e / pat.P), k = static_cast<int>(e % pat.P);
@@ -905,10 +913,10 @@ __global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_if
   const double gu = ref.fx * x + ref.cx, gvp = ref.fy * y + ref.cy;
   const bool ok = in_bounds_px(gu - 0.5, gvp, ref.W, ref.H) && in_bounds_px(gu + 0.5, gvp, ref.W, ref.H) &&
                   in_bounds_px(gu, gvp - 0.5, ref.W, ref.H) && in_bounds_px(gu, gvp + 0.5, ref.W, ref.H);
-  double2 g = make_double2(NAN, NAN);
+  double4 g = make_double4(tval[e], NAN, NAN, 0.0);  // {template value, gx, gy, 0}: one 32-byte load
   if (ok) {
-    g.x = (bilinear(ref.img, ref.W, gu + 0.5, gvp) - bilinear(ref.img, ref.W, gu - 0.5, gvp)) * ref.fx;
-    g.y = (bilinear(ref.img, ref.W, gu, gvp + 0.5) - bilinear(ref.img, ref.W, gu, gvp - 0.5)) * ref.fy;
+    g.y = (bilinear(ref.img, ref.W, gu + 0.5, gvp) - bilinear(ref.img, ref.W, gu - 0.5, gvp)) * ref.fx;
+    g.z = (bilinear(ref.img, ref.W, gu, gvp + 0.5) - bilinear(ref.img, ref.W, gu, gvp - 0.5)) * ref.fy;
   }
   tgrad[e] = g;
 }
@@ -1987,7 +1995,7 @@ void launch_point(const PointArgs& a, cudaStream_t s) {
 }
 
 void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const double2* anc, double* tval,
-                            double2* tgrad, cudaStream_t s) {
+                            double4* tgrad, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(N) * pat.P;
   if (n == 0) return;
   k_template_values<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(N, pat, ref, 1.0 / ref.fx, 1.0 / ref.fy, anc,

@@ -34,7 +34,7 @@ struct ObsArgs {
   PatternD pat;
   const double2* anchor_fm;    // NO: anchor pixel of obs q (frame-major copy, static, TMA-staged)
   const double* tval;          // N*P: template values (internal point order)
-  const double2* tgrad;        // N*P: template gradients (IC build), NaN = footprint outside the image
+  const double4* tgrad;        // N*P: template records {tval, gx, gy, 0} (IC modes), gx NaN = footprint outside
   const double* d_eval;        // N: inverse depths at the evaluation parameters (internal order)
   const double* d_old;         // N or null: inverse depths at the old parameters (max update)
   double gamma;
@@ -105,7 +105,7 @@ int backsub_blocks(int N);
 // tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template, solver.cpp:33-53)
 // and tgrad[n*P + k] = image_gradient(ref, .) at the template pixel (NaN: footprint outside)
 void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const double2* anc, double* tval,
-                            double2* tgrad, cudaStream_t s);
+                            double4* tgrad, cudaStream_t s);
 void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s);
 void launch_backsub(const BacksubArgs& a, cudaStream_t s);
 // tq[q] = B_q . xp_f over the frame-major observations (FC back-substitution without B gathers)

@@ -426,6 +426,7 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.pat = pat_;
   a.anchor_fm = anchor_fm_.p;
   a.tval = tval_.p;
+  for (int k = 0; k < 8 && k < P_; ++k) a.pat_d[k] = make_double2(pat_.dx[k], pat_.dy[k]);
   a.tgrad = tgrad_.p;
   a.d0 = d0_.p;
   a.pose0 = pose0_.p;  // frozen IC poses (rows of the factored IC Jacobian)

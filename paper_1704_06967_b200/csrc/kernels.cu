@@ -453,8 +453,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       const int k = PT > 0 ? sub * KP + kk : kk;
       if (!((mbits >> k) & 1u)) continue;
       // template pixel (solver.cpp:42-49)
-      const double pu = an.x + static_cast<double>(a.pat.dx[k]);
-      const double pv = an.y + static_cast<double>(a.pat.dy[k]);
+      const double pu = an.x + (PT > 0 ? a.pat_d[k].x : static_cast<double>(a.pat.dx[k]));  // no I2F when unrolled
+      const double pv = an.y + (PT > 0 ? a.pat_d[k].y : static_cast<double>(a.pat.dy[k]));
       const double x = (pu - rf.cx) * a.ref_ifx;
       const double y = (pv - rf.cy) * a.ref_ify;
       double xn, yn, vx, vy, vz, r = 0.0;

@@ -417,13 +417,16 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       l2_prefetch(a.Jm + b0 - (qs & 31), (b1 - (b0 - (qs & 31))) * sizeof(double));
     }
   };
-  if (kLanePrefetch > 0) {
+  // bulk L2 prefetch one block step ahead; off for the IC passes that rebuild the rows (not
+  // HBM-bound: the prefetch instructions cost more than they hide there)
+  constexpr bool kPf = kLanePrefetch > 0 && !((MODE == OBS_IC || MODE == OBS_REFRESH) && kRc);
+  if (kPf) {
     for (int i = 0; i < kLanePrefetch; ++i) prefetch_step(q0 + static_cast<int64_t>(i) * OPB);
   }
   const int sub = LPO > 1 ? static_cast<int>(threadIdx.x % LPO) : 0;
   constexpr int KP = PT > 0 ? PT / LPO : 0;  // pixels per lane (compile time), 0 = all P
   for (int64_t base = q0; base < q1; base += OPB) {
-    if (kLanePrefetch > 0) prefetch_step(base + static_cast<int64_t>(kLanePrefetch) * OPB);
+    if (kPf) prefetch_step(base + static_cast<int64_t>(kLanePrefetch) * OPB);
     const int64_t q = base + threadIdx.x / LPO;
     const bool live = q < q1;
     const int64_t qc = live ? q : q1 - 1;  // clamped for the loads of idle lanes

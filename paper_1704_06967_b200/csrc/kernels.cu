@@ -265,6 +265,9 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #define PBA_IC_MINB 3
 #endif
 
+#ifndef PBA_IC_STORED_PATH
+#define PBA_IC_STORED_PATH 1  // compile the stored-rows body too (PBA_IC_RECOMPUTE=0 at run time)
+#endif
 #ifndef PBA_LANE_PREFETCH
 #define PBA_LANE_PREFETCH 1
 #endif
@@ -631,20 +634,21 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   }
 }
 
+__device__ FrameTab g_no_tab;  // bound to the table parameter of the shared-memory variant, never read
+
 template <int MODE, int PT, int LPO>
 __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB) k_obs_lane(const ObsArgs a) {
-  const FrameTab* none = nullptr;
   if (MODE == OBS_IC || MODE == OBS_REFRESH) {
-    if (a.Jm) obs_lane_body<MODE, PT, LPO, false, false>(a, *none);
-    else obs_lane_body<MODE, PT, LPO, false, true>(a, *none);
+    if (PBA_IC_STORED_PATH && a.Jm) obs_lane_body<MODE, PT, LPO, false, false>(a, g_no_tab);
+    else obs_lane_body<MODE, PT, LPO, false, true>(a, g_no_tab);
   } else {
-    obs_lane_body<MODE, PT, LPO, false, false>(a, *none);
+    obs_lane_body<MODE, PT, LPO, false, false>(a, g_no_tab);
   }
 }
 template <int MODE, int PT, int LPO>
 __global__ void __launch_bounds__(NT, MODE == OBS_IC ? PBA_IC_MINB : PBA_LANE_MINB)
     k_obs_lane_tab(const ObsArgs a, const FrameTab tab) {
-  if (a.Jm) obs_lane_body<MODE, PT, LPO, true, false>(a, tab);
+  if (PBA_IC_STORED_PATH && a.Jm) obs_lane_body<MODE, PT, LPO, true, false>(a, tab);
   else obs_lane_body<MODE, PT, LPO, true, true>(a, tab);
 }
 

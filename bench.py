@@ -66,6 +66,30 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        # NVML thread at a 2 ms cadence (the timed region is tens of ms); nvidia-smi -lms fallback
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            hd = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv = (pynvml, hd)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(hd, pynvml.NVML_CLOCK_SM)
+            self.stop_ev = threading.Event()
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+
+            def loop():
+                while True:
+                    sm = pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hd)
+                    self.rows.append([str(sm), str(self.mx), "", ""]
+                                     + ["Active" if rs & b else "Not Active" for b in bits])
+                    if self.stop_ev.wait(0.002):
+                        break
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -80,13 +104,17 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self):
-        if self.proc is None:
+        if getattr(self, "nv", None) is not None:
+            self.stop_ev.set()
+            self.t.join(timeout=5)
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
         rows = [r for r in self.rows if len(r) >= 8]
         if not rows:  # timed region shorter than one sampling period: take one snapshot now
             try:

@@ -611,7 +611,21 @@ void Engine::alloc_schur() {
     schur_wsort_.alloc(static_cast<size_t>(std::max(schur_plan_.npts, 1)));
     schur_plan_.dense = schur_dense_.p;
     schur_plan_.wsort = schur_wsort_.p;
+    // slots of frames a point does not observe stay zero: the passes only ever write observed slots
+    ck(cudaMemsetAsync(schur_dense_.p, 0, static_cast<size_t>(std::max<int64_t>(schur_dense_elems_, 1)) * sizeof(double),
+                       stream_), "dense zero");
+    dense_row_.alloc(static_cast<size_t>(std::max(N_, 1)));
+    launch_dense_rows(schur_plan_, dense_row_.p, stream_);
   }
+}
+
+// The Hessian-building passes write each b_n block into its Schur chunk row as well (no separate
+// densify kernel: FC saves it every iteration, IC at the build); the dense rows then hold B_out.
+void Engine::fuse_dense(ObsArgs& a) {
+  alloc_schur();
+  a.B_dense = schur_plan_.dense;
+  a.dense_row = dense_row_.p;
+  dense_B_ = a.B_dense ? a.B_out : nullptr;
 }
 
 bool Engine::factor_reduced(const double* H, const double* B, const double* D, double lambda) {
@@ -691,7 +705,7 @@ void Engine::ic_build(const pba_config* cfg) {
   a.active_out = mask_[0].p;
   a.Jmw = J_.p;
   a.B_out = Bic_.p;
-  dense_B_ = nullptr;  // the densified Schur blocks are stale
+  fuse_dense(a);
   trace_mark(stream_, "ic_build: setup+alloc");
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_BUILD, a, stream_);

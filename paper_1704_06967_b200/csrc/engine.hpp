@@ -176,6 +176,7 @@ class Engine {
   DBuf<int4> schur_blocks_, schur_chunks_;
   DBuf<int64_t> schur_chunk_off_;
   DBuf<double> schur_dense_, schur_wsort_;
+  DBuf<int64_t> dense_row_;  // N: chunk-row slot base of each point (the fused dense write)
   const double* dense_B_ = nullptr;  // B whose blocks schur_dense_ holds (null = stale)
   int64_t schur_dense_elems_ = 0;
   SchurPlan schur_plan_{};
@@ -254,6 +255,7 @@ class Engine {
                double lambda, const PoseD* pose_old, const double* d_old);
   void ic_rescale_rhs(int buf, double lambda);
   void alloc_schur();
+  void fuse_dense(ObsArgs& a);  // the pass also scatters B into the Schur chunk rows
   void build_frame_tabs(const PoseD* pose_d);
   std::vector<int32_t> zero_depth_points(const double* D);
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);

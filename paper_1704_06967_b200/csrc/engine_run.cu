@@ -130,7 +130,7 @@ void Engine::ic_refresh() {
   a.active_out = scratch_bits_.p;
   a.Jm = J_.p;
   a.B_out = Bic_.p;
-  dense_B_ = nullptr;
+  fuse_dense(a);
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_REFRESH, a, stream_);
   ev_end(PBA_K_IC_BUILD, e);
@@ -165,7 +165,7 @@ void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, 
   a.mask_in = nullptr;
   a.active_out = scratch_bits_.p;
   a.B_out = B_[buf].p;
-  dense_B_ = nullptr;
+  fuse_dense(a);
   auto e = ev_begin(PBA_K_OBS_PASS);
   launch_obs(OBS_FC, a, stream_);
   ev_end(PBA_K_OBS_PASS, e);

@@ -604,6 +604,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       if constexpr (kH) {
 #pragma unroll
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+        if (a.B_dense) {  // the Schur chunk row slot of (n, f): 16-byte aligned (rows are 64-double multiples)
+          double2* dst = reinterpret_cast<double2*>(a.B_dense + a.dense_row[n] + 6 * f);
+          dst[0] = make_double2(b6[0], b6[1]);
+          dst[1] = make_double2(b6[2], b6[3]);
+          dst[2] = make_double2(b6[4], b6[5]);
+        }
       }
     }
   }
@@ -2048,6 +2054,23 @@ void launch_max_reproj(const ObsView& ov, const FrameD* frames, const FrameD& re
                        int dy0, const PoseD* pa, const double* da, const PoseD* pb, const double* db, double* partial,
                        int nblocks, cudaStream_t s) {
   k_max_reproj<<<nblocks, NT, 0, s>>>(ov, frames, ref, anchor, dx0, dy0, pa, da, pb, db, partial);
+  count_launches(1);
+}
+
+__global__ void k_dense_rows(const int32_t* __restrict__ chunk_pts, int npts, const int32_t* __restrict__ chunk_of,
+                             const int4* __restrict__ chunks, const int64_t* __restrict__ chunk_off,
+                             int64_t* __restrict__ dense_row) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  const int c = chunk_of[p];
+  const int4 ch = chunks[c];
+  dense_row[chunk_pts[p]] = chunk_off[c] + static_cast<int64_t>(p - ch.x) * ch.w - 6 * ch.z;
+}
+
+void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s) {
+  if (plan.npts <= 0) return;
+  k_dense_rows<<<(plan.npts + 255) / 256, 256, 0, s>>>(plan.chunk_pts, plan.npts, plan.chunk_of, plan.chunks,
+                                                       plan.chunk_off, dense_row);
   count_launches(1);
 }
 

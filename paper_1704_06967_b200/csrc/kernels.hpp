@@ -49,6 +49,8 @@ struct ObsArgs {
   double* Jmw;                 // BUILD output of m
   const double* d0;            // N: frozen depths of the IC build (IC / REFRESH)
   double* B_out;               // NO*6 (FC/BUILD/REFRESH)
+  double* B_dense;             // or null: also scatter b_n into the Schur chunk rows (SchurPlan::dense)
+  const int64_t* dense_row;    // N: offset of point n's chunk row minus 6 fmin (slot of frame f at + 6 f)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
   double* rec_g;               // NO or null: IC pass g_n terms only (sum_k Jd w r)
   double* partial;             // ntiles * PT_STRIDE
@@ -203,6 +205,8 @@ struct SchurPlan {
   const int4* blocks;        // per work item {chunk, 0, 0, rb | cb << 16}
   int nblocks;
 };
+// dense_row[n] = chunk_off + (p - chunk begin) * LD - 6 fmin for the p-th window-sorted point n
+void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s);
 // Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.
 // plan == nullptr selects the per-point pair kernel.
 // densify = false reuses plan->dense from the previous call with the same B.

@@ -124,6 +124,9 @@ typedef struct pba_energy_result {
 /* ---- generic ---------------------------------------------------------------- */
 const char* pba_status_string(int status);
 void pba_config_default(pba_config* cfg);                 /* SolverConfig{} defaults */
+/* perturb_parameters (synth.cpp:308-320), host only: R (9F), t (3F), d (N) in place; the
+   std::mt19937_64 / std::normal_distribution stream of the reference CLI's `solve` (pba.cpp:62). */
+int pba_perturb_parameters(int32_t F, double* R, double* t, int32_t N, double* d, double sigma, uint64_t seed);
 
 /* ---- handle lifecycle: IcSolver(ProblemState, SolverConfig) solver.hpp:117,
    FcSolver(ProblemState, SolverConfig) solver.hpp:176.  Uploads the problem. */

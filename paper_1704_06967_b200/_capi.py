@@ -155,6 +155,10 @@ class Backend:
             self.status_string = self.lib.pba_status_string
             self.status_string.restype = C.c_char_p
             self.status_string.argtypes = [C.c_int]
+            # host-only utility of the CLI (synth.cpp:308-320); no device work
+            self.perturb_parameters = self.lib.pba_perturb_parameters
+            self.perturb_parameters.restype = C.c_int
+            self.perturb_parameters.argtypes = _ORACLE_ONLY["perturb_parameters"][1]
         self.config_default = self.lib.pba_config_default if kind == "gpu" else None
 
 

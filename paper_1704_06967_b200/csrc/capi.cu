@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <random>
 #include <string>
 
 #include "engine.hpp"
@@ -53,6 +54,27 @@ const char* pba_status_string(int s) {
     case PBA_E_SPEC_INFEASIBLE: return "SpecInfeasible";
     default: return "unknown";
   }
+}
+
+// perturb_parameters (synth.cpp:308-320): one std::mt19937_64 stream, N(0, sigma) draws on the six
+// tangent coordinates of every pose (pose_boxplus, geometry.cpp:93-98: R <- exp(w) R, t <- t + v),
+// then one per inverse depth.  Host only (the CLI's `solve` input, pba.cpp:55-62).
+int pba_perturb_parameters(int32_t F, double* R, double* t, int32_t N, double* d, double sigma, uint64_t seed) {
+  if (F < 0 || N < 0 || (F > 0 && (!R || !t)) || (N > 0 && !d)) return PBA_E_ARG;
+  if (!(sigma > 0.0)) return PBA_OK;
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, sigma);
+  for (int f = 0; f < F; ++f) {
+    double delta[6];
+    for (int i = 0; i < 6; ++i) delta[i] = gauss(rng);
+    double E[9], Rn[9];
+    pba_b200::so3_exp(delta, E);
+    pba_b200::mat3_mul(E, R + 9 * f, Rn);
+    for (int i = 0; i < 9; ++i) R[9 * f + i] = Rn[i];
+    for (int i = 0; i < 3; ++i) t[3 * f + i] += delta[3 + i];
+  }
+  for (int n = 0; n < N; ++n) d[n] += gauss(rng);
+  return PBA_OK;
 }
 
 void pba_config_default(pba_config* c) {  // SolverConfig{} (solver.hpp:45-54)

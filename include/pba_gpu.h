@@ -197,6 +197,26 @@ int pba_gpu_max_reproj_update(pba_handle* h, const double* R, const double* t,
 /* normalize_depth_gauge (solver.cpp:135-143) applied to the problem parameters. */
 int pba_gpu_normalize_gauge(pba_handle* h);
 
+/* ---- point-sharded runs -------------------------------------
+   Each rank's handle holds a disjoint subset of the points with all of their observations;
+   frames, images and poses are replicated.  The reference has no multi-process path: the
+   exchange replaces the sums over n of solver.cpp (assemble_gradient :450-468, the Schur
+   update :381-389, the rhs term :407-416, the gauge mean :135-143, the energy :97) by sums
+   over the ranks.  Per IC iteration one all-gather of {g_f, c_f, status} (12F + 8 doubles)
+   and one of the depth sum; per (re)factorization one int64 sum of the fixed-point Schur
+   accumulator (36F^2, exact); FC adds H (21F) to the first.  Every rank then runs the same
+   replicated pose solve and LM decisions (bitwise identical inputs), and back-substitutes
+   its own depths.
+   op PBA_X_GATHER: send `count` doubles at `send` (device), receive world*count doubles
+   rank-major at `recv` (device).  op PBA_X_SUM_I64: in-place sum of `count` int64 at `send`.
+   The callee orders the exchange after the work queued on `stream` (a cudaStream_t) and
+   before the work queued there after it returns (e.g. NCCL on that stream).  0 = success.
+   fn == NULL restores the single-process path. */
+enum { PBA_X_GATHER = 0, PBA_X_SUM_I64 = 1 };
+typedef int (*pba_exchange_fn)(void* ctx, int op, void* send, void* recv, int64_t count, void* stream);
+int pba_gpu_set_exchange(pba_handle* h, int32_t rank, int32_t world, int64_t num_points_total,
+                         pba_exchange_fn fn, void* ctx);
+
 /* ---- instrumentation ------------------------------------------------------- */
 void* pba_gpu_stream(pba_handle* h);                 /* the handle's cudaStream_t */
 /* When on, the hot kernels are bracketed by CUDA events on the handle's stream;

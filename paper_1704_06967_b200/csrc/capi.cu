@@ -217,6 +217,10 @@ int pba_gpu_max_reproj_update(pba_handle* h, const double* R, const double* t, c
 int pba_gpu_normalize_gauge(pba_handle* h) {
   return guarded(h, [&](Engine& e) { e.normalize_gauge(); });
 }
+int pba_gpu_set_exchange(pba_handle* h, int32_t rank, int32_t world, int64_t num_points_total, pba_exchange_fn fn,
+                         void* ctx) {
+  return guarded(h, [&](Engine& e) { e.set_exchange(rank, world, num_points_total, fn, ctx); });
+}
 void* pba_gpu_stream(pba_handle* h) { return (h && h->e) ? static_cast<void*>(h->e->stream()) : nullptr; }
 int pba_gpu_set_profiling(pba_handle* h, int on) {
   return guarded(h, [&](Engine& e) { e.set_profiling(on != 0); });

@@ -377,8 +377,8 @@ void Engine::kernel_times(int64_t* counts, double* total_ms) {
   }
 }
 
-void Engine::check_template() const {
-  if (!template_ok_) throw PbaError(PBA_E_OUT_OF_BOUNDS, "template patch pixel outside reference image");
+void Engine::check_template() {
+  xcheck(template_ok_, PBA_E_OUT_OF_BOUNDS, "template patch pixel outside reference image");
 }
 
 Status Engine::read_status() {
@@ -436,8 +436,73 @@ ObsArgs Engine::obs_args(double gamma) const {
   return a;
 }
 
+// ---- rank exchange (point-sharded runs) ----
+void Engine::set_exchange(int rank, int world, int64_t n_total, pba_exchange_fn fn, void* ctx) {
+  if (fn && (world < 1 || rank < 0 || rank >= world || n_total < N_))
+    throw PbaError(PBA_E_ARG, "set_exchange: need 0 <= rank < world and num_points_total >= this shard's points");
+  xch_ = Xch{};
+  if (!fn) return;
+  xch_ = Xch{rank, world, n_total, fn, ctx};
+  cf_.alloc(6 * static_cast<size_t>(std::max(F_, 1)));
+  gauge_sum_.alloc(1);
+}
+
+void Engine::xreduce(const std::vector<XSeg>& segs) {
+  XPlan plan{};
+  int K = 0;
+  for (const XSeg& g : segs) {
+    if (!g.p || g.n <= 0) continue;
+    if (plan.nseg == 8) throw PbaError(PBA_E_ARG, "xreduce: too many segments");
+    K += g.n;
+    plan.seg_end[plan.nseg] = K;
+    plan.seg_max[plan.nseg] = g.max ? 1 : 0;
+    ++plan.nseg;
+  }
+  if (K == 0) return;
+  const size_t W = static_cast<size_t>(xch_.world);
+  if (xsend_.n < static_cast<size_t>(K)) xsend_.alloc(K);
+  if (xrecv_.n < W * K) xrecv_.alloc(W * K);
+  int off = 0;
+  for (const XSeg& g : segs) {
+    if (!g.p || g.n <= 0) continue;
+    ck(cudaMemcpyAsync(xsend_.p + off, g.p, g.n * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "x pack");
+    off += g.n;
+  }
+  if (xch_.fn(xch_.ctx, PBA_X_GATHER, xsend_.p, xrecv_.p, K, stream_) != 0)
+    throw PbaError(PBA_E_ARG, "rank exchange (gather) failed");
+  launch_xreduce(xrecv_.p, xch_.world, K, plan, xsend_.p, stream_);
+  off = 0;
+  for (const XSeg& g : segs) {
+    if (!g.p || g.n <= 0) continue;
+    ck(cudaMemcpyAsync(g.p, xsend_.p + off, g.n * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "x unpack");
+    off += g.n;
+  }
+}
+
+void Engine::xsum_i64(unsigned long long* p, int64_t n) {
+  if (n <= 0) return;
+  if (xch_.fn(xch_.ctx, PBA_X_SUM_I64, p, nullptr, n, stream_) != 0)
+    throw PbaError(PBA_E_ARG, "rank exchange (int64 sum) failed");
+}
+
+void Engine::xcheck(bool ok, int code, const std::string& msg) {
+  if (!sharded()) {
+    if (!ok) throw PbaError(code, msg);
+    return;
+  }
+  gauge_sum_.alloc(1);
+  const double bad = ok ? 0.0 : 1.0;
+  ck(cudaMemcpyAsync(gauge_sum_.p, &bad, sizeof(double), cudaMemcpyHostToDevice, stream_), "xcheck");
+  xreduce({{gauge_sum_.p, 1, false}});
+  double tot = 0.0;
+  ck(cudaMemcpyAsync(&tot, gauge_sum_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "xcheck");
+  ck(cudaStreamSynchronize(stream_), "xcheck");
+  if (tot > 0.0) throw PbaError(code, ok ? msg + " (on another shard)" : msg);
+}
+
 void Engine::finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
                       double* rhs, const double* g_f_in, double* H, bool status) {
+  if (sharded() && rhs && partial && !g_f) g_f = g_tmp_.p;  // the rank sum needs g itself
   FinalizeArgs f{};
   f.ov = ov_;
   f.partial = partial;
@@ -454,8 +519,23 @@ void Engine::finalize(const double* partial, const double* partial_cf, bool bs, 
   f.status = status ? status_.p : nullptr;
   f.fscal = fscal_.p;
   f.ticket = ticket_.p + 1;
+  if (sharded()) {  // rhs = -g + c_f is formed from the rank sums of g and c_f
+    f.rhs = nullptr;
+    f.cf_out = rhs ? cf_.p : nullptr;
+  }
   const auto e = ev_begin(PBA_K_REDUCE);
   launch_finalize(f, stream_);
+  if (sharded()) {
+    double* st = status ? reinterpret_cast<double*>(status_.p) : nullptr;
+    static_assert(sizeof(Status) == 8 * sizeof(double), "Status layout");
+    xreduce({{partial ? g_f : nullptr, 6 * F_, false},
+             {rhs ? cf_.p : nullptr, 6 * F_, false},
+             {(want_h && partial) ? H : nullptr, 21 * F_, false},
+             {st, 3, false},                          // energy, #active, #oob
+             {st ? st + 3 : nullptr, 1, true},        // max reprojection update
+             {st ? st + 4 : nullptr, 4, false}});     // sum d, #invalid, #non-finite, |g_n|^2
+    if (rhs) launch_rhs(6 * F_, g_f ? g_f : g_f_in, cf_.p, rhs, stream_);
+  }
   ev_end(PBA_K_REDUCE, e);
 }
 
@@ -634,7 +714,9 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   auto e = ev_begin(PBA_K_SCHUR);
   alloc_schur();
   const bool densify = dense_B_ != B;  // the dense blocks depend on B only (not on D or lambda)
-  launch_schur(ov_, H, B, D, lambda, S_.p, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_);
+  launch_schur_acc(ov_, H, B, D, lambda, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_);
+  if (sharded()) xsum_i64(schur_acc_.p, 36 * static_cast<int64_t>(F_) * F_);  // exact: fixed point
+  launch_schur_final(ov_, H, lambda, schur_scale_.p, schur_acc_.p, S_.p, stream_);
   dense_B_ = B;
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);

@@ -114,6 +114,9 @@ class Engine {
 
   std::string last_error;
 
+  // point-sharded runs (pba_gpu_set_exchange)
+  void set_exchange(int rank, int world, int64_t n_total, pba_exchange_fn fn, void* ctx);
+
   // make this engine's stream the allocation stream of the calling thread (every C-ABI entry)
   void bind() const { set_alloc_stream(stream_); }
 
@@ -194,6 +197,24 @@ class Engine {
 
   SolverState ic_;
 
+  // rank exchange of point-sharded runs (null fn = single process)
+  struct Xch {
+    int rank = 0, world = 1;
+    int64_t n_total = 0;
+    pba_exchange_fn fn = nullptr;
+    void* ctx = nullptr;
+  } xch_;
+  struct XSeg {
+    double* p;
+    int n;
+    bool max;
+  };
+  DBuf<double> xsend_, xrecv_, cf_, gauge_sum_;
+  bool sharded() const { return xch_.fn != nullptr; }
+  void xreduce(const std::vector<XSeg>& segs);          // sum / max over the ranks, in rank order
+  void xsum_i64(unsigned long long* p, int64_t n);       // exact in-place integer sum
+  void xcheck(bool ok, int code, const std::string& msg);  // the same error on every rank
+
   // run (stepping) state
   struct Run {
     bool active = false;
@@ -238,7 +259,7 @@ class Engine {
   void rows_to_user(const double* src_fm, int w, double* dst_user);
   void rows_from_user(const double* src_user, int w, double* dst_fm);
   // helpers
-  void check_template() const;
+  void check_template();  // every rank raises the same OutOfBounds in a sharded run
   void upload_poses(DBuf<PoseD>& dst, const double* R, const double* t);
   void upload_depths_user(DBuf<double>& dst, const double* d_user);
   void download_poses(const DBuf<PoseD>& src, double* R, double* t);

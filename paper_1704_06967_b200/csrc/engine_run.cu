@@ -61,12 +61,17 @@ void Engine::backsub(bool ic, const double* B, const double* D, const double* g_
   a.ticket = ticket_.p;
   a.gauge_scale = gauge_.p;
   a.gauge_enabled = run_.cfg.normalize_depth_gauge ? 1 : 0;
+  a.gauge_sum = sharded() ? gauge_sum_.p : nullptr;
   const auto e = ev_begin(PBA_K_REDUCE);
   if (!a.Bpm) {  // frame-major blocks: dots first (coalesced), then the point-major 8-byte gather
     launch_bdot(ov_, B, xp_.p, rec_g_.p, stream_);
     a.tq = rec_g_.p;
   }
   launch_backsub(a, stream_);
+  if (sharded()) {  // the gauge mean is over every rank's points
+    xreduce({{gauge_sum_.p, 1, false}});
+    launch_gauge_from_sum(gauge_sum_.p, static_cast<double>(xch_.n_total), a.gauge_enabled, gauge_.p, stream_);
+  }
   ev_end(PBA_K_REDUCE, e);
 }
 

@@ -880,6 +880,7 @@ __global__ void __launch_bounds__(NT, kBsMinB) k_backsub(const BacksubArgs a) {
     for (int b = lane; b < gridDim.x; b += 32) v += __ldcg(a.partial + 4 * b);
     v = warp_sum(v);
     if (lane == 0) {
+      if (a.gauge_sum) *a.gauge_sum = v;
       const double mean = v / static_cast<double>(a.ov.N);
       *a.gauge_scale = (a.gauge_enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
     }
@@ -919,7 +920,8 @@ __global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_if
   const int n = static_cast<int>(e / pat.P), k = static_cast<int>(e % pat.P);
   const double pu = anc[n].x + static_cast<double>(pat.dx[k]);
   const double pv = anc[n].y + static_cast<double>(pat.dy[k]);
-  tval[e] = bilinear(ref.img, ref.W, pu, pv);
+  // a template pixel outside the image is refused at build (OutOfBounds, solver.cpp:43-45): never sample it
+  tval[e] = in_bounds_px(pu, pv, ref.W, ref.H) ? bilinear(ref.img, ref.W, pu, pv) : NAN;
   // template gradient at to_pixel(to_normalized(px)) (solver.cpp:296-304, image.cpp:36-49), the
   // same expressions the IC build used per pixel; NaN marks a footprint outside the image
   const double x = (pu - ref.cx) * ref_ifx, y = (pv - ref.cy) * ref_ify;
@@ -1116,6 +1118,7 @@ __global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
       if (a.g_f) a.g_f[6 * f + threadIdx.x] = g;
       if (a.rhs) a.rhs[6 * f + threadIdx.x] = -g + vals[6 + threadIdx.x];
     }
+    if (a.cf_out && threadIdx.x < 6) a.cf_out[6 * f + threadIdx.x] = vals[6 + threadIdx.x];
     if (a.want_h && a.H && threadIdx.x < 21) a.H[21 * f + threadIdx.x] = vals[12 + threadIdx.x];
     if (threadIdx.x < 4) a.fscal[4 * f + threadIdx.x] = vals[33 + threadIdx.x];
   }
@@ -2074,15 +2077,15 @@ void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s
   count_launches(1);
 }
 
-void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
-                  double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s) {
+void launch_schur_acc(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda,
+                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s) {
   const int n = 6 * ov.F;
   const int64_t total = static_cast<int64_t>(n) * n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
   const bool dense = plan && plan->nblocks > 0;
   k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total, dense ? plan->chunk_pts : nullptr,
                                        dense ? plan->npts : 0, D, lambda, dense ? plan->wsort : nullptr);
-  int launched = 2;
+  int launched = 1;
   if (dense) {
     if (densify) {
       k_schur_densify<<<(plan->npts * 32 + 255) / 256, 256, 0, s>>>(ov, B, plan->chunk_pts, plan->npts, plan->chunk_of,
@@ -2105,8 +2108,63 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
       ++launched;
     }
   }
-  k_schur_final<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, scale, acc, S);
   count_launches(launched);
+}
+
+void launch_schur_final(const ObsView& ov, const double* H21, double lambda, const double* scale,
+                        const unsigned long long* acc, double* S, cudaStream_t s) {
+  const int n = 6 * ov.F;
+  const int64_t total = static_cast<int64_t>(n) * n;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
+  k_schur_final<<<blocks, 256, 0, s>>>(ov.F, H21, lambda, scale, acc, S);
+  count_launches(1);
+}
+
+void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda, double* S,
+                  double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s) {
+  launch_schur_acc(ov, H21, B, D, lambda, scale, acc, plan, densify, s);
+  launch_schur_final(ov, H21, lambda, scale, acc, S, s);
+}
+
+__global__ void k_xreduce(const double* __restrict__ in, int world, int K, const XPlan plan, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  int sg = 0;
+  while (sg < plan.nseg - 1 && k >= plan.seg_end[sg]) ++sg;
+  const bool mx = plan.seg_max[sg] != 0;
+  double v = in[k];
+  for (int r = 1; r < world; ++r) {
+    const double x = in[static_cast<int64_t>(r) * K + k];
+    v = mx ? fmax(v, x) : v + x;
+  }
+  out[k] = v;
+}
+
+void launch_xreduce(const double* in, int world, int K, const XPlan& plan, double* out, cudaStream_t s) {
+  if (K <= 0) return;
+  k_xreduce<<<(K + 255) / 256, 256, 0, s>>>(in, world, K, plan, out);
+  count_launches(1);
+}
+
+__global__ void k_rhs(int n, const double* __restrict__ g, const double* __restrict__ cf, double* __restrict__ rhs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rhs[i] = -g[i] + cf[i];
+}
+
+void launch_rhs(int n, const double* g, const double* cf, double* rhs, cudaStream_t s) {
+  if (n <= 0) return;
+  k_rhs<<<(n + 255) / 256, 256, 0, s>>>(n, g, cf, rhs);
+  count_launches(1);
+}
+
+__global__ void k_gauge_from_sum(const double* __restrict__ sum, double n_total, int enabled, double* __restrict__ gauge) {
+  const double mean = *sum / n_total;
+  *gauge = (enabled && mean > 0.0 && isfinite(mean)) ? mean : 1.0;
+}
+
+void launch_gauge_from_sum(const double* sum, double n_total, int enabled, double* gauge, cudaStream_t s) {
+  k_gauge_from_sum<<<1, 1, 0, s>>>(sum, n_total, enabled, gauge);
+  count_launches(1);
 }
 
 void launch_cholesky(double* S, int n, int* fail, cudaStream_t s) {

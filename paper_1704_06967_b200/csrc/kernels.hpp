@@ -103,6 +103,7 @@ struct BacksubArgs {
   double* gauge_scale;    // out: mean of d_cand (1 when disabled / not positive-finite)
   int gauge_enabled;
   const double* tq = nullptr;  // NO or null: per-observation B_nf . xp_f (k_bdot) instead of B / Bpm
+  double* gauge_sum = nullptr; // or null: also the raw sum of d_cand (sharded runs form the mean over ranks)
 };
 int backsub_blocks(int N);
 // tval[n*P + k] = bilinear(ref, anchor_n + offset_k) (build_template, solver.cpp:33-53)
@@ -172,6 +173,7 @@ struct FinalizeArgs {
   double* rhs;                // 6F or null (requires partial_cf; uses g_f_in if partial==null)
   const double* g_f_in;       // 6F: gradient when the obs partial is absent (rescale)
   double* H;                  // 21F or null
+  double* cf_out;             // 6F or null: the Schur rhs term c_f itself (sharded runs sum it over ranks)
   Status* status;             // or null
   double* fscal;              // F*4 scratch: per-frame {energy, #active, #oob, max update}
   unsigned int* ticket;       // grid ticket (zero between launches)
@@ -213,6 +215,27 @@ void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s
 void launch_schur(const ObsView& ov, const double* H21, const double* B, const double* D,
                   double lambda, double* S, double* scale, unsigned long long* acc, const SchurPlan* plan,
                   bool densify, cudaStream_t s);
+// The two halves of launch_schur: the fixed-point accumulation of sum_n b_n b_n^T / (D_n + lambda)
+// into acc (scale from H21), and S = blockdiag(H + lambda I) - acc / scale.  A point-sharded run sums
+// acc over the ranks in between (exact: integer addition).
+void launch_schur_acc(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda,
+                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s);
+void launch_schur_final(const ObsView& ov, const double* H21, double lambda, const double* scale,
+                        const unsigned long long* acc, double* S, cudaStream_t s);
+
+// ---- rank exchange of point-sharded runs ----
+// out[k] = sum (or max, for k in a max segment) over r = 0..world-1 of in[r * K + k], in rank order
+// (bitwise identical on every rank).  Segments: [seg_end[i-1], seg_end[i]) with flag seg_max[i].
+struct XPlan {
+  int nseg;
+  int seg_end[8];
+  int seg_max[8];
+};
+void launch_xreduce(const double* in, int world, int K, const XPlan& plan, double* out, cudaStream_t s);
+// rhs[i] = -g[i] + cf[i] (k_finalize's order)
+void launch_rhs(int n, const double* g, const double* cf, double* rhs, cudaStream_t s);
+// gauge = sum / n_total when enabled and positive-finite, else 1 (normalize_depth_gauge, solver.cpp:135-143)
+void launch_gauge_from_sum(const double* sum, double n_total, int enabled, double* gauge, cudaStream_t s);
 
 // In-place dense Cholesky (lower) of the n x n row-major S; *fail set on a
 // non-positive / non-finite pivot (stands in for Eigen::LDLT::info()).

@@ -81,13 +81,16 @@ def test_energy_empty_problem_raises():  # test_solver.cpp:103-108
             solver.energy_eval(st, 0.03, backend=be)
 
 
-def test_template_out_of_bounds_raises():  # solver.cpp:43-45
+@pytest.mark.parametrize("anchor", [(0.5, 10.0), (0.0, 0.0), (-50.0, -50.0), (1e6, 3.0)])
+def test_template_out_of_bounds_raises(anchor):  # solver.cpp:43-45 (far outside: no sampling, no fault)
     st = ref_scene(frames=2, points=3)
     st.anchors_px = st.anchors_px.copy()
-    st.anchors_px[0] = [0.5, 10.0]
+    st.anchors_px[0] = anchor
     for be in ("gpu", "oracle"):
         with pytest.raises(solver.OutOfBounds):
             solver.energy_eval(st, 0.03, backend=be)
+    with pytest.raises(solver.OutOfBounds):
+        solver.ic_solve(st, SolverConfig(max_iters=2))
 
 
 def test_energy_gauge_invariance_gpu():  # test_solver.cpp:110-122

@@ -11,9 +11,11 @@ LM iterations, download).  One JSON line is printed by rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-Multi-GPU (torchrun): "replicas only" in this round -- every rank runs an independent
-replica of the workload on its own GPU (weak scaling, value = sum over ranks,
-time = max over ranks); see DESIGN.md §6 for the point-sharded design.
+Multi-GPU (torchrun): by default every rank runs an independent replica of the workload on its
+own GPU (``--mode replicas``: weak scaling, value = sum over ranks, time = max over ranks).
+``--mode sharded`` splits ONE workload's points over the ranks (strong scaling; the engine's
+rank exchange over NCCL): value = the workload's active pixels per iteration / the
+max over ranks of the iteration time.
 """
 from __future__ import annotations
 
@@ -48,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fc", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
     return ap.parse_args()
 
 
@@ -303,7 +306,9 @@ def run_ours(args, rank, world):
 
     dev = torch.device("cuda", rank % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
-    sc_cfg = scenes.baseline_config(args.config, seed=scenes.baseline_config(args.config).seed + rank)
+    sharded = args.mode == "sharded"
+    seed = scenes.baseline_config(args.config).seed + (0 if sharded else rank)  # sharded: one workload
+    sc_cfg = scenes.baseline_config(args.config, seed=seed)
     t0 = time.perf_counter()
     scene = scenes.make_scene(sc_cfg, device=str(dev))
     gen_s = time.perf_counter() - t0
@@ -311,8 +316,19 @@ def run_ours(args, rank, world):
     cfg = sc_cfg.solver_config(threshold_px=0.0, max_iters=10_000, max_bad_steps=8)
     lib = _capi.backend("gpu")
 
+    def make_handle(state):
+        """A handle on this rank's share: the whole problem, or its point shard with the NCCL exchange."""
+        if not sharded:
+            return solver.Handle(state, "gpu")
+        from paper_1704_06967_b200 import sharding
+        x = sharding.TorchExchange()
+        sh = sharding.shard_problem(state, x.rank, x.world)
+        hh = solver.Handle(sh.state, "gpu")
+        x.attach(hh, sh.num_points_total)
+        return hh
+
     # ---------------- device-resident timing of IC iterations ----------------
-    h = solver.Handle(st, "gpu")
+    h = make_handle(st)
     t0 = time.perf_counter()
     h.begin(True, cfg)           # upload done; IC build + initial pass (untimed)
     build_s = time.perf_counter() - t0
@@ -356,7 +372,7 @@ def run_ours(args, rank, world):
     # ---------------- FC iterations (same workload) ----------------
     fc = None
     if not args.no_fc and args.fc_steps > 0:
-        hf = solver.Handle(st, "gpu")
+        hf = make_handle(st)
         hf.begin(False, cfg)
         stf = torch.cuda.ExternalStream(hf.stream(), device=dev)
         evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -401,12 +417,19 @@ def run_ours(args, rank, world):
                + st.t.nbytes + (0 if st.obs_ptr is None else st.obs_ptr.nbytes + st.obs_frame.nbytes))
         d2h = st.R.nbytes + st.t.nbytes + st.inv_depths.nbytes
         tot_px, tot_s, step_ms = 0, 0.0, []
+        if sharded:  # this rank's share of the inputs (replicated frames, its points), as a user would pass them
+            from paper_1704_06967_b200 import sharding
+
+            def solve_e2e(state, c):
+                return sharding.solve_distributed(state, c, "ic", gather=False)
+        else:
+            solve_e2e = solver.ic_solve
         for _ in range(args.e2e_warmup):  # untimed: first-touch of the device memory pool
-            solver.ic_solve(st_pin, c2)
+            solve_e2e(st_pin, c2)
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            rep = solver.ic_solve(st_pin, c2)
+            rep = solve_e2e(st_pin, c2)
             dt = time.perf_counter() - t0
             tot_s += dt
             step_ms.append(round(1e3 * dt, 2))
@@ -466,12 +489,16 @@ def main():
         print(json.dumps(line))
         return
 
-    if world > 1:
+    pg = world > 1 or args.mode == "sharded"  # the sharded engine exchanges over NCCL even at N = 1
+    if pg:
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        lr = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", lr))
     r = run_ours(args, rank, world)
     st = r["st"]
     per_step_ms = r["dev_ms"] / args.steps
@@ -486,10 +513,12 @@ def main():
         dist.all_reduce(tot[:1], op=dist.ReduceOp.SUM)
         mx = t.clone()
         dist.all_reduce(mx[1:], op=dist.ReduceOp.MAX)
-        value = float(tot[0]) / (float(mx[1]) / 1e3)
+        # sharded: every rank reports the exchanged (global) active count of the one workload
+        px = r["px_total"] if args.mode == "sharded" else float(tot[0])
+        value = px / (float(mx[1]) / 1e3)
         ms = float(mx[1]) / args.steps
     if rank != 0:
-        if world > 1:
+        if pg:
             import torch.distributed as dist
             dist.destroy_process_group()
         return
@@ -515,7 +544,7 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.mode == "sharded" else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -524,7 +553,8 @@ def main():
                    "pattern": int(st.pattern.shape[0]), "image": list(st.ref.shape[::-1]),
                    "active_obs_px_per_iter": r["n_px_iter"], "accepted_steps": r["accepted"],
                    "l2": "inputs larger than L2 (factored frozen IC Jacobian %.1f GB)" % (24 * st.num_observations * st.pattern.shape[0] / 1e9),
-                   "parallelism": "replicas" if world > 1 else "single"},
+                   "parallelism": (f"point-sharded x{world}" if args.mode == "sharded"
+                                   else ("replicas" if world > 1 else "single"))},
         "roofline": {"bound": "hbm", "kernel": "k_obs_lane<OBS_IC> fused residual/Huber/J^T W r pass (factored J)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(), "alg_bytes_per_launch": svy,
@@ -547,7 +577,7 @@ def main():
         "setup_s": {"scene_gen": round(r["gen_s"], 2), "ic_build_and_first_pass": round(r["build_s"], 3)},
     }
     print(json.dumps(line))
-    if world > 1:
+    if pg:
         import torch.distributed as dist
         dist.destroy_process_group()
 

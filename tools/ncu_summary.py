@@ -36,9 +36,16 @@ def launches(path):
         name = r["Kernel Name"].split("(")[0]
         per[name][0] += 1
         per[name][1] += ms
-    tot = sum(v[1] for v in per.values())
-    return {k: {"launches": v[0], "total_ms": round(v[1], 4), "share": round(v[1] / tot, 4)}
-            for k, v in sorted(per.items(), key=lambda kv: -kv[1][1])}
+    # the library's kernels (anonymous namespace k_*); torch's scene-generation kernels are reported
+    # as one aggregate line
+    ours = {k: v for k, v in per.items() if "unnamed>::k_" in k}
+    other = [sum(v[0] for k, v in per.items() if k not in ours), sum(v[1] for k, v in per.items() if k not in ours)]
+    tot = sum(v[1] for v in ours.values())
+    out = {k: {"launches": v[0], "total_ms": round(v[1], 4), "share": round(v[1] / tot, 4)}
+           for k, v in sorted(ours.items(), key=lambda kv: -kv[1][1])}
+    out["(not this library: torch scene generation, excluded from the shares)"] = {
+        "launches": other[0], "total_ms": round(other[1], 4), "share": None}
+    return out
 
 
 def full(path):

@@ -197,6 +197,40 @@ int pba_gpu_max_reproj_update(pba_handle* h, const double* R, const double* t,
 /* normalize_depth_gauge (solver.cpp:135-143) applied to the problem parameters. */
 int pba_gpu_normalize_gauge(pba_handle* h);
 
+/* ---- joint multi-host window with per-frame affine brightness ----
+   NOT in the reference (single reference frame, no photometric parameters: solver.hpp:33-43,
+   SPEC.md:318); this is the DSO-style joint form of BASELINE C2, forwards compositional, checked
+   against the oracle's statement of the same model (oracle/multihost.cpp, which gives the
+   equations).  Every point is hosted in one frame; it is observed in other frames through the
+   relative pose T_t T_h^-1, with r = e^(a_t - a_h) (tpl - b_h) + b_t - I_t(warp).  Frame 0 is
+   held.  With every point hosted in frame 0 and the affine parameters held, a run is the
+   reference's FcSolver::run (solver.cpp:663-843) on frames 1..K-1. */
+typedef struct pba_mh_problem {
+  int32_t num_frames;            /* K >= 2 */
+  const pba_image* images;       /* K images, each with its intrinsics */
+  const double* pose_R;          /* 9K row-major, X_i = R_i X_w + t_i */
+  const double* pose_t;          /* 3K */
+  const double* affine_a;        /* K or NULL (= 0) */
+  const double* affine_b;        /* K or NULL (= 0) */
+  int32_t num_points;
+  const int32_t* host;           /* N: host frame of each point */
+  const double* anchors_px;      /* 2N: pixels of the host image */
+  const double* inv_depths;      /* N: in the host camera */
+  int32_t pattern_size;          /* P <= 32 */
+  const int32_t* pattern;        /* 2P offsets, pattern[0] = (0, 0) */
+  const int64_t* obs_ptr;        /* N+1 CSR of target frames (each != host), or NULL = every other frame */
+  const int32_t* obs_frame;
+  int32_t optimize_affine;       /* 1: (a, b) of frames 1..K-1 are parameters; 0: held */
+} pba_mh_problem;
+typedef struct pba_mh_handle pba_mh_handle;
+int pba_gpu_mh_create(const pba_mh_problem* problem, pba_mh_handle** out);
+void pba_gpu_mh_destroy(pba_mh_handle* h);
+const char* pba_gpu_mh_last_error(const pba_mh_handle* h);
+int pba_gpu_mh_energy(pba_mh_handle* h, double gamma, pba_energy_result* out);
+/* FcSolver::run rules on the joint window; rep->final_R / final_t hold all K frames,
+   a_out / b_out (K, or NULL) the final affine parameters. */
+int pba_gpu_mh_fc_run(pba_mh_handle* h, const pba_config* cfg, pba_report* rep, double* a_out, double* b_out);
+
 /* ---- point-sharded runs -------------------------------------
    Each rank's handle holds a disjoint subset of the points with all of their observations;
    frames, images and poses are replicated.  The reference has no multi-process path: the

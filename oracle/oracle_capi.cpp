@@ -489,3 +489,84 @@ int pba_oracle_perturb_parameters(int32_t F, double* R, double* t, int32_t N, do
 }
 
 }  // extern "C"
+
+// ---- joint multi-host window (multihost.cpp) ---------------------------------------
+struct pba_oracle_mh_handle {
+  MhProblem p;
+  std::string last_error;
+};
+
+namespace {
+template <typename Fn>
+int guarded_mh(pba_oracle_mh_handle* h, Fn&& fn) {
+  pba_oracle_handle tmp;  // carries the error text of the shared exception mapping
+  const int rc = guarded(&tmp, fn);
+  if (h && rc != PBA_OK) h->last_error = tmp.last_error;
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int pba_oracle_mh_create(const pba_mh_problem* q, pba_oracle_mh_handle** out) {
+  if (!q || !out) return PBA_E_ARG;
+  auto h = std::make_unique<pba_oracle_mh_handle>();
+  const int rc = guarded_mh(h.get(), [&] {
+    const int K = q->num_frames, N = q->num_points, P = q->pattern_size;
+    if (K < 2 || N < 0 || P < 1) throw Error("bad multi-host problem sizes");
+    MhProblem& p = h->p;
+    for (int f = 0; f < K; ++f) {
+      p.images.push_back(to_image(q->images[f]));
+      p.poses.push_back(to_pose(q->pose_R + 9 * f, q->pose_t + 3 * f));
+    }
+    if (q->affine_a) p.affine_a.assign(q->affine_a, q->affine_a + K);
+    if (q->affine_b) p.affine_b.assign(q->affine_b, q->affine_b + K);
+    for (int n = 0; n < N; ++n) {
+      p.host.push_back(q->host[n]);
+      p.anchors_px.emplace_back(q->anchors_px[2 * n], q->anchors_px[2 * n + 1]);
+      p.inv_depths.push_back(q->inv_depths[n]);
+    }
+    p.patch.offsets.clear();
+    for (int k = 0; k < P; ++k) p.patch.offsets.push_back({q->pattern[2 * k], q->pattern[2 * k + 1]});
+    if (q->obs_ptr) {
+      p.obs_ptr.assign(q->obs_ptr, q->obs_ptr + N + 1);
+      p.obs_frame.assign(q->obs_frame, q->obs_frame + q->obs_ptr[N]);
+    }
+    p.optimize_affine = q->optimize_affine != 0;
+  });
+  if (rc != PBA_OK) return rc;
+  *out = h.release();
+  return PBA_OK;
+}
+
+void pba_oracle_mh_destroy(pba_oracle_mh_handle* h) { delete h; }
+
+const char* pba_oracle_mh_last_error(const pba_oracle_mh_handle* h) { return h ? h->last_error.c_str() : ""; }
+
+int pba_oracle_mh_energy(pba_oracle_mh_handle* h, double gamma, pba_energy_result* out) {
+  if (!h) return PBA_E_ARG;
+  return guarded_mh(h, [&] {
+    const MhEnergy e = mh_energy(h->p, HuberLoss{gamma});
+    if (out) {
+      out->energy = e.energy;
+      out->num_active = e.num_active;
+      out->num_out_of_bounds = e.num_oob;
+    }
+  });
+}
+
+int pba_oracle_mh_fc_run(pba_oracle_mh_handle* h, const pba_config* cfg, pba_report* rep, double* a_out,
+                         double* b_out) {
+  if (!h) return PBA_E_ARG;
+  return guarded_mh(h, [&] {
+    const MhReport r = mh_fc_solve(h->p, to_config(cfg));
+    const int K = static_cast<int>(h->p.images.size());
+    if (rep) fill_report(r.base, K, static_cast<int>(h->p.anchors_px.size()), rep);
+    for (int f = 0; f < K; ++f) {
+      if (a_out) a_out[f] = r.final_a[f];
+      if (b_out) b_out[f] = r.final_b[f];
+    }
+  });
+}
+
+}  // extern "C"

@@ -408,6 +408,33 @@ class FcSolver {  // solver.hpp:172-182
 
 SolveReport ic_solve(const ProblemState& state, const SolverConfig& config);
 SolveReport fc_solve(const ProblemState& state, const SolverConfig& config);
+
+// ---- joint multi-host window + per-frame affine brightness (multihost.cpp) ----------
+// OUR model (the reference has no multi-host solver): forwards
+// compositional, reduces to fc_solve when every point is hosted in frame 0 and the affine
+// parameters are held.  See multihost.cpp for the equations.
+struct MhProblem {
+  std::vector<Image> images;          // K frames, each with its intrinsics
+  std::vector<Pose> poses;            // K (X_i = R_i X_w + t_i); frame 0 held
+  std::vector<double> affine_a, affine_b;  // K or empty (= 0); frame 0 held
+  std::vector<int> host;              // N host frame of each point
+  std::vector<Vec2> anchors_px;       // N, pixels of the host image
+  std::vector<double> inv_depths;     // N, in the host camera
+  PatchPattern patch{PatchPattern::square(1)};
+  std::vector<int64_t> obs_ptr;       // CSR by point of target frames (!= host); empty = all others
+  std::vector<int32_t> obs_frame;
+  bool optimize_affine{true};
+};
+struct MhEnergy {
+  double energy{0.0};
+  int64_t num_active{0}, num_oob{0};
+};
+struct MhReport {
+  SolveReport base;                   // poses of all K frames, depths, counters
+  std::vector<double> final_a, final_b;
+};
+MhEnergy mh_energy(const MhProblem& p, const HuberLoss& huber);
+MhReport mh_fc_solve(const MhProblem& p, const SolverConfig& config);
 std::vector<double> solve_normal_equations_schur(const BlockHessian& H,
                                                  const std::vector<double>& g, double lambda);
 std::vector<double> solve_normal_equations_dense(const BlockHessian& H,

@@ -51,6 +51,15 @@ int pba_oracle_max_reproj_update(pba_oracle_handle* h, const double* R, const do
 int pba_oracle_normalize_gauge(pba_oracle_handle* h);
 
 /* Reference test-scene generator (synth.hpp:14-80). */
+/* joint multi-host window (oracle/multihost.cpp); mirrors pba_gpu_mh_* */
+typedef struct pba_oracle_mh_handle pba_oracle_mh_handle;
+int pba_oracle_mh_create(const pba_mh_problem* problem, pba_oracle_mh_handle** out);
+void pba_oracle_mh_destroy(pba_oracle_mh_handle* h);
+const char* pba_oracle_mh_last_error(const pba_oracle_mh_handle* h);
+int pba_oracle_mh_energy(pba_oracle_mh_handle* h, double gamma, pba_energy_result* out);
+int pba_oracle_mh_fc_run(pba_oracle_mh_handle* h, const pba_config* cfg, pba_report* rep, double* a_out,
+                         double* b_out);
+
 typedef struct pba_oracle_scene_spec {
   int32_t width, height;
   double fx, fy, cx, cy;

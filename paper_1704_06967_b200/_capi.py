@@ -67,6 +67,13 @@ class pba_report(C.Structure):
                 ("message", C.c_char * 256)]
 
 
+class pba_mh_problem(C.Structure):
+    _fields_ = [("num_frames", i32), ("images", P(pba_image)), ("pose_R", P(f64)), ("pose_t", P(f64)),
+                ("affine_a", P(f64)), ("affine_b", P(f64)), ("num_points", i32), ("host", P(i32)),
+                ("anchors_px", P(f64)), ("inv_depths", P(f64)), ("pattern_size", i32), ("pattern", P(i32)),
+                ("obs_ptr", P(i64)), ("obs_frame", P(i32)), ("optimize_affine", i32)]
+
+
 class pba_energy_result(C.Structure):
     _fields_ = [("energy", f64), ("num_active", i64), ("num_out_of_bounds", i64)]
 
@@ -106,6 +113,12 @@ _COMMON = {
     "apply_update": (C.c_int, [VP, C.c_int, P(f64), P(f64), P(f64), P(f64), P(C.c_int)]),
     "max_reproj_update": (C.c_int, [VP, P(f64), P(f64), P(f64), P(f64)]),
     "normalize_gauge": (C.c_int, [VP]),
+    # joint multi-host window (pba_gpu_mh_* / pba_oracle_mh_*)
+    "mh_create": (C.c_int, [P(pba_mh_problem), P(VP)]),
+    "mh_destroy": (None, [VP]),
+    "mh_last_error": (C.c_char_p, [VP]),
+    "mh_energy": (C.c_int, [VP, f64, P(pba_energy_result)]),
+    "mh_fc_run": (C.c_int, [VP, P(pba_config), P(pba_report), P(f64), P(f64)]),
 }
 _GPU_ONLY = {
     "ic_begin": (C.c_int, [VP, P(pba_config)]),

@@ -310,3 +310,108 @@ def subsample_points(st: ProblemState, n_keep: int, seed: int = 0) -> ProblemSta
         of = np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, np.int32)
     return ProblemState(st.ref, st.ref_K, st.targets, st.targets_K, st.R.copy(), st.t.copy(),
                         st.anchors_px[idx].copy(), st.inv_depths[idx].copy(), st.pattern, op, of)
+
+
+# ----------------------------------------------------------------------------- joint C2 window
+
+@dataclass
+class WindowScene:
+    """A DSO-style window (BASELINE C2 joint form): K keyframes, points hosted in every keyframe."""
+    problem: "object"            # multihost.MultiHostProblem with the perturbed initial parameters
+    R_true: np.ndarray
+    t_true: np.ndarray
+    d_true: np.ndarray
+    a_true: np.ndarray
+    b_true: np.ndarray
+    huber_delta: float = 9.0
+    iters: int = 5
+
+    def solver_config(self, **kw) -> SolverConfig:
+        c = SolverConfig(gamma=self.huber_delta, max_iters=self.iters, lambda0=1e-6 * 255.0 ** 2)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+
+def make_window_scene(keyframes: int = 7, points_per_kf: int = 2000, width: int = 640, height: int = 480,
+                      fx: float = 500.0, arc_deg: float = 24.0, affine_sigma: float = 0.05, rot_deg: float = 1.0,
+                      trans_sigma: float = 0.01, depth_noise: float = 0.05, seed: int = 2, iters: int = 5,
+                      pattern: Optional[np.ndarray] = None, device: Optional[str] = None) -> WindowScene:
+    """BASELINE C2 joint form: `keyframes` views of the textured sphere on an arc (frame 0 = the world
+    frame), `points_per_kf` points hosted in every keyframe and observed in all the others, per-frame
+    affine brightness I_i = e^(a_i) L + b_i with a ~ N(0, sigma), b ~ 255 N(0, sigma) (frame 0: 0).
+    Initial parameters: poses of frames 1.. perturbed, affine 0, inverse depths with multiplicative
+    noise.  Synthetic and seeded; the reference has no generator for this form."""
+    from .multihost import MultiHostProblem
+
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    gen = torch.Generator().manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    W, H = width, height
+    K = (fx, fx, (W - 1) / 2.0, (H - 1) / 2.0)
+    center = np.array([0.0, 0.0, 2.0])
+    wt = int(round(2 * math.pi * fx * 1.0))
+    tex_obj = _noise_texture(wt // 2, wt, 2.0, gen, dev)
+    tex_env = _noise_texture(wt // 2, wt, 2.0, gen, dev)
+    KF = keyframes
+    span = math.radians(arc_deg)
+    R_true = np.zeros((KF, 3, 3))
+    t_true = np.zeros((KF, 3))
+    for f in range(KF):  # frame 0 at the identity, the others on an arc about the sphere centre
+        alpha = 0.0 if f == 0 else span * (f / max(KF - 1, 1) - 0.5)
+        Rf = _so3_exp(np.array([0.0, alpha, 0.0]))
+        R_true[f] = Rf
+        t_true[f] = center - Rf @ center
+    a_true = np.concatenate([[0.0], affine_sigma * rng.normal(size=KF - 1)])
+    b_true = np.concatenate([[0.0], 255.0 * affine_sigma * rng.normal(size=KF - 1)])
+    L = [_render(R_true[f], t_true[f], K, W, H, center, tex_obj, tex_env, dev) for f in range(KF)]
+    images = np.stack([(math.exp(a_true[f]) * L[f] + b_true[f]).astype(np.float32) for f in range(KF)])
+    pat = DSO8 if pattern is None else np.asarray(pattern, np.int32)
+    m = int(np.abs(pat).max()) + 2
+    uu, vv = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    hosts, anchors, depths = [], [], []
+    for f in range(KF):  # anchors on the sphere's silhouette in keyframe f; depth along f's ray
+        Rt = R_true[f].T
+        C = -(Rt @ t_true[f])
+        dcam = np.stack([(uu - K[2]) / fx, (vv - K[3]) / fx, np.ones_like(uu)], -1)
+        dw = dcam @ Rt.T
+        dn = dw / np.linalg.norm(dw, axis=-1, keepdims=True)
+        oc = C - center
+        bq = (dn * oc).sum(-1)
+        disc = bq * bq - (oc @ oc - 1.0)
+        on = disc > 0
+        on_er = on.copy()
+        for dy in range(-m, m + 1):
+            for dx in range(-m, m + 1):
+                on_er &= np.roll(np.roll(on, dy, 0), dx, 1)
+        on_er[:m, :] = on_er[-m:, :] = False
+        on_er[:, :m] = on_er[:, -m:] = False
+        cand = np.flatnonzero(on_er.ravel())
+        pick = rng.choice(cand, size=points_per_kf, replace=points_per_kf > cand.size)
+        an = np.stack([pick % W, pick // W], -1).astype(np.float64)
+        ray = np.stack([(an[:, 0] - K[2]) / fx, (an[:, 1] - K[3]) / fx, np.ones(len(an))], -1)
+        rw = ray @ Rt.T
+        rn = rw / np.linalg.norm(rw, axis=-1, keepdims=True)
+        b2 = (rn * oc).sum(-1)
+        s = -b2 - np.sqrt(np.maximum(b2 * b2 - (oc @ oc - 1.0), 0.0))
+        Xw = C + rn * s[:, None]
+        z = (Xw @ R_true[f].T + t_true[f])[:, 2]   # depth in the host camera
+        hosts.append(np.full(len(an), f, np.int32))
+        anchors.append(an)
+        depths.append(1.0 / z)
+    host = np.concatenate(hosts)
+    anchors = np.concatenate(anchors)
+    d_true = np.concatenate(depths)
+    mean = d_true.mean()  # depth gauge (synth.cpp:285-291)
+    d_true = d_true / mean
+    t_true = t_true * mean
+    R0, t0 = R_true.copy(), t_true.copy()
+    for f in range(1, KF):
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        R0[f] = _so3_exp(axis * math.radians(rot_deg) * rng.normal()) @ R_true[f]
+        t0[f] = t_true[f] + rng.normal(scale=trans_sigma, size=3)
+    d0 = np.abs(d_true * (1.0 + depth_noise * rng.normal(size=d_true.size))) + 1e-6
+    prob = MultiHostProblem(images, np.tile(np.array(K), (KF, 1)), R0, t0, host, anchors, d0, pat,
+                            a=np.zeros(KF), b=np.zeros(KF), optimize_affine=True)
+    return WindowScene(prob, R_true, t_true, d_true, a_true, b_true, iters=iters)

@@ -1,0 +1,146 @@
+"""Joint multi-host window with per-frame affine brightness.
+
+The reference has no multi-host solver, so the joint model is checked against the oracle's own
+statement of it (oracle/multihost.cpp) — parity pinned to the reference only through the
+reduction: with every point hosted in frame 0 and the affine parameters held, the window is the
+reference's single-host FC problem (checked on the CPU against the pinned oracle FC, and on the
+GPU)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1704_06967_b200 import multihost as mh
+from paper_1704_06967_b200 import scenes, solver
+from paper_1704_06967_b200.solver import Handle, OutOfBounds, SolverConfig
+
+from ._helpers import oracle_scene, rel
+
+P_TOL = 1e-4
+E_TOL = 1e-5
+
+
+def _window(kf=4, ppk=40, **kw):
+    return scenes.make_window_scene(keyframes=kf, points_per_kf=ppk, width=160, height=120, fx=130.0, arc_deg=12.0,
+                                    device="cpu", **kw)
+
+
+def _runs_close(a, b, tol=P_TOL):
+    assert a.iterations == b.iterations
+    assert a.converged == b.converged and a.diverged == b.diverged
+    assert a.rejected_steps == b.rejected_steps
+    assert a.hessian_builds == b.hessian_builds and a.hessian_factorizations == b.hessian_factorizations
+    assert [s.accepted for s in a.iters] == [s.accepted for s in b.iters]
+    assert [s.num_active for s in a.iters] == [s.num_active for s in b.iters]
+    for x, y in zip(a.iters, b.iters):
+        assert abs(x.energy - y.energy) <= tol * abs(y.energy)
+    assert rel(a.final_inv_depths, b.final_inv_depths) <= tol
+    assert rel(a.final_t, b.final_t) <= tol
+    assert rel(a.final_R, b.final_R) <= tol
+
+
+# ----------------------------------------------------------------------------- CPU (oracle)
+
+def test_oracle_window_of_a_single_host_problem_is_the_reference_fc():
+    st = oracle_scene(frames=3, points=10, sigma=1e-3, perturb_seed=8)
+    cfg = SolverConfig(max_iters=20)
+    ref = Handle(st, "oracle").fc_run(cfg)
+    p = mh.from_single_host(st)
+    e_ref = solver.energy_eval(st, 0.03, backend="oracle")
+    e_mh = mh.MultiHostHandle(p, "oracle").energy(0.03)
+    assert e_mh.energy == e_ref.energy and e_mh.num_active == e_ref.num_active  # same sums, same order
+    r = mh.mh_fc_solve(p, cfg, backend="oracle")
+    assert r.converged and r.iterations == ref.iterations and r.rejected_steps == ref.rejected_steps
+    for a, b in zip(r.iters, ref.iters):
+        assert abs(a.energy - b.energy) <= 1e-10 * b.energy
+    assert np.abs(r.final_inv_depths - ref.final_inv_depths).max() < 1e-10
+    assert np.abs(r.final_t[1:] - ref.final_t).max() < 1e-10
+    assert np.array_equal(r.final_R[0], np.eye(3)) and np.array_equal(r.final_t[0], np.zeros(3))  # frame 0 held
+
+
+def test_oracle_joint_window_recovers_affine_and_descends():
+    sc = _window(iters=15)
+    r = mh.mh_fc_solve(sc.problem, sc.solver_config(), backend="oracle")
+    es = [it.energy for it in r.iters]
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(es, es[1:]))
+    e0 = mh.MultiHostHandle(sc.problem, "oracle").energy(9.0).energy
+    assert es[-1] < 0.5 * e0
+    assert r.final_a[0] == 0.0 and r.final_b[0] == 0.0  # frame 0 held
+    assert np.abs(r.final_b[1:] - sc.b_true[1:]).max() < 5.0  # offsets of ~13 intensity units recovered
+    held = mh.MultiHostProblem(**{**sc.problem.__dict__, "optimize_affine": False})
+    rh = mh.mh_fc_solve(held, sc.solver_config(), backend="oracle")
+    assert np.array_equal(rh.final_a, np.zeros(4)) and rh.final_energy > r.final_energy
+
+
+def test_oracle_rejects_bad_windows():
+    sc = _window(kf=3, ppk=5)
+    p = sc.problem
+    bad = mh.MultiHostProblem(**{**p.__dict__, "host": np.full(p.num_points, 7, np.int32)})
+    with pytest.raises(solver.Error):
+        mh.MultiHostHandle(bad, "oracle").energy(9.0)
+    an = p.anchors_px.copy()
+    an[0] = (0.0, 0.0)
+    with pytest.raises(OutOfBounds):
+        mh.MultiHostHandle(mh.MultiHostProblem(**{**p.__dict__, "anchors_px": an}), "oracle").energy(9.0)
+
+
+# ----------------------------------------------------------------------------- GPU
+
+@pytest.mark.gpu
+def test_gpu_window_of_a_single_host_problem_matches_the_reference_fc():
+    """The reduction against the PINNED oracle FC (the reference's FcSolver::run restatement)."""
+    for st in (oracle_scene(frames=3, points=10, sigma=1e-3, perturb_seed=8),
+               scenes.make_scene(scenes.baseline_config("C1"), device="cpu").state):
+        gamma = 0.03 if st.ref.max() <= 1.0 else 9.0
+        cfg = SolverConfig(gamma=gamma, max_iters=10, lambda0=1e-6 if gamma < 1 else 1e-6 * 255.0 ** 2)
+        ref = Handle(st, "oracle").fc_run(cfg)
+        r = mh.mh_fc_solve(mh.from_single_host(st), cfg, backend="gpu")
+        r.final_t, r.final_R = r.final_t[1:], r.final_R[1:]
+        _runs_close(r, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("affine", [True, False])
+def test_gpu_joint_window_matches_oracle(affine):
+    sc = _window(iters=10)
+    p = mh.MultiHostProblem(**{**sc.problem.__dict__, "optimize_affine": affine})
+    cfg = sc.solver_config(record_snapshots=True)
+    eg = mh.MultiHostHandle(p, "gpu").energy(9.0)
+    eo = mh.MultiHostHandle(p, "oracle").energy(9.0)
+    assert eg.num_active == eo.num_active and eg.num_out_of_bounds == eo.num_out_of_bounds
+    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+    rg = mh.mh_fc_solve(p, cfg, backend="gpu")
+    ro = mh.mh_fc_solve(p, cfg, backend="oracle")
+    _runs_close(rg, ro)
+    assert np.abs(rg.final_a - ro.final_a).max() <= P_TOL and np.abs(rg.final_b - ro.final_b).max() <= P_TOL * 255
+    for a, b in zip(rg.iters, ro.iters):
+        assert rel(a.inv_depths, b.inv_depths) <= P_TOL
+
+
+@pytest.mark.gpu
+def test_gpu_joint_window_visibility_list_and_determinism():
+    sc = _window(kf=5, ppk=30, iters=6)
+    p = sc.problem
+    rng = np.random.default_rng(3)
+    ptr, fr = [0], []
+    for n in range(p.num_points):  # a random non-empty subset of the other frames
+        others = [f for f in range(5) if f != p.host[n]]
+        keep = [f for f in others if rng.random() < 0.6] or [others[0]]
+        fr += keep
+        ptr.append(len(fr))
+    q = mh.MultiHostProblem(**{**p.__dict__, "obs_ptr": np.array(ptr), "obs_frame": np.array(fr)})
+    cfg = sc.solver_config()
+    r1, r2 = mh.mh_fc_solve(q, cfg), mh.mh_fc_solve(q, cfg)
+    assert r1.final_energy == r2.final_energy and np.array_equal(r1.final_inv_depths, r2.final_inv_depths)
+    _runs_close(r1, mh.mh_fc_solve(q, cfg, backend="oracle"))
+
+
+@pytest.mark.gpu
+def test_gpu_window_errors():
+    sc = _window(kf=3, ppk=5)
+    an = sc.problem.anchors_px.copy()
+    an[0] = (-40.0, 0.0)
+    with pytest.raises(OutOfBounds):
+        mh.MultiHostHandle(mh.MultiHostProblem(**{**sc.problem.__dict__, "anchors_px": an}), "gpu").energy(9.0)
+    with pytest.raises(solver.Error):
+        mh.MultiHostHandle(mh.MultiHostProblem(**{**sc.problem.__dict__, "host": np.full(15, 9, np.int32)}), "gpu")

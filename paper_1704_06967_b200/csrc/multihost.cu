@@ -244,6 +244,17 @@ __device__ __forceinline__ void moments(const double* rc, double (&M)[9][9], dou
   }
 }
 
+// the chain matrices of every pair at the current parameters (read by k_mh_frames / k_mh_point)
+__global__ void k_mh_pairmap(int npairs, int Q, const int2* __restrict__ pairs, const PoseD* __restrict__ pose,
+                             const double* __restrict__ a, PairMap* __restrict__ maps) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  const int h = pairs[p].x, t = pairs[p].y;
+  PairMap pm;
+  pair_map(pose[t], pose[h], exp(a[t] - a[h]), Q, pm);
+  maps[p] = pm;
+}
+
 // per pair p = (h, t): records of its observations summed in q order
 __global__ void k_mh_pair(const int64_t* __restrict__ pair_ptr, const int64_t* __restrict__ pair_obs,
                           const double* __restrict__ rec, double* __restrict__ pair_rec) {
@@ -256,9 +267,8 @@ __global__ void k_mh_pair(const int64_t* __restrict__ pair_ptr, const int64_t* _
 }
 
 // H_FF (nF x nF, full) and g_F: one thread per (entry | gradient row), pairs in order
-__global__ void k_mh_frames(const MhDev m, int npairs, const int2* __restrict__ pairs, const PoseD* __restrict__ pose,
-                            const double* __restrict__ a, const double* __restrict__ pair_rec,
-                            double* __restrict__ H, double* __restrict__ gF) {
+__global__ void k_mh_frames(const MhDev m, int npairs, const int2* __restrict__ pairs, const PairMap* __restrict__ maps,
+                            const double* __restrict__ pair_rec, double* __restrict__ H, double* __restrict__ gF) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int nF = m.nF, Q = m.Q;
   const int nent = nF * nF + nF;
@@ -275,8 +285,7 @@ __global__ void k_mh_frames(const MhDev m, int npairs, const int2* __restrict__ 
     if (ir < 0) continue;
     const int ic = isg ? 0 : (fc == t ? cc : (fc == h ? Q + cc : -1));
     if (!isg && ic < 0) continue;
-    PairMap pm;
-    pair_map(pose[t], pose[h], exp(a[t] - a[h]), Q, pm);
+    const PairMap& pm = maps[p];
     double M[9][9], gt[9];
     moments(pair_rec + static_cast<int64_t>(p) * MH_REC, M, gt);
     if (isg) {
@@ -299,7 +308,7 @@ __global__ void k_mh_frames(const MhDev m, int npairs, const int2* __restrict__ 
 }
 
 // per point: b_n (nF, dense), D_n, g_n from its observations' records (obs order)
-__global__ void k_mh_point(const MhDev m, const PoseD* __restrict__ pose, const double* __restrict__ a,
+__global__ void k_mh_point(const MhDev m, const int32_t* __restrict__ pair_of, const PairMap* __restrict__ maps,
                            const double* __restrict__ rec, double* __restrict__ Bn, double* __restrict__ D,
                            double* __restrict__ gn) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -311,8 +320,7 @@ __global__ void k_mh_point(const MhDev m, const PoseD* __restrict__ pose, const 
   for (int64_t q = m.obs_ptr[n]; q < m.obs_ptr[n + 1]; ++q) {
     const int t = m.obs_frame[q];
     const double* rc = rec + q * MH_REC;
-    PairMap pm;
-    pair_map(pose[t], pose[h], exp(a[t] - a[h]), m.Q, pm);
+    const PairMap& pm = maps[pair_of[static_cast<int64_t>(h) * m.K + t]];
     double M[9][9], gt[9];
     moments(rc, M, gt);
     // b columns: sum w J_abs,c J_d = sum_i C[c][i] M[i][8]
@@ -333,31 +341,48 @@ __global__ void k_mh_point(const MhDev m, const PoseD* __restrict__ pose, const 
   gn[n] = gd;
 }
 
-// S = H + lambda I - sum_n b_n b_n^T / (D_n + lambda) (upper computed, mirrored); rhs = -g_F + sum_n b_n g_n / (D_n + lambda)
-__global__ void k_mh_schur(int nF, int N, const double* __restrict__ H, const double* __restrict__ gF,
-                           const double* __restrict__ Bn, const double* __restrict__ D, const double* __restrict__ gn,
-                           double lambda, double* __restrict__ S, double* __restrict__ rhs) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < nF * nF) {
-    const int r = e / nF, c = e % nF;
-    if (c < r) return;
-    double v = H[e] + (r == c ? lambda : 0.0);
-    for (int n = 0; n < N; ++n) {
-      const double br = Bn[static_cast<int64_t>(n) * nF + r];
-      if (br == 0.0) continue;
-      v -= br * Bn[static_cast<int64_t>(n) * nF + c] / (D[n] + lambda);
+// S = H + lambda I - sum_n b_n b_n^T / (D_n + lambda) (upper computed, mirrored); rhs = -g_F + sum_n b_n g_n / (D_n + lambda).
+// One block per upper entry / rhs row: thread i sums the points n = i, i + MH_NT, ... in order, then a
+// fixed tree over the threads (deterministic).
+__global__ void __launch_bounds__(MH_NT) k_mh_schur(int nF, int N, const double* __restrict__ H,
+                                                    const double* __restrict__ gF, const double* __restrict__ Bn,
+                                                    const double* __restrict__ D, const double* __restrict__ gn,
+                                                    double lambda, double* __restrict__ S, double* __restrict__ rhs) {
+  __shared__ double sh[MH_NT];
+  const int e = blockIdx.x;
+  const int nup = nF * (nF + 1) / 2;
+  int r, c = -1;
+  if (e < nup) {  // e -> (r, c), r <= c
+    r = 0;
+    int rem = e;
+    while (rem >= nF - r) {
+      rem -= nF - r;
+      ++r;
     }
-    S[static_cast<int64_t>(r) * nF + c] = v;
-    S[static_cast<int64_t>(c) * nF + r] = v;
-  } else if (e < nF * nF + nF) {
-    const int r = e - nF * nF;
-    double v = -gF[r];
-    for (int n = 0; n < N; ++n) {
-      const double br = Bn[static_cast<int64_t>(n) * nF + r];
-      if (br == 0.0) continue;
-      v += br * (gn[n] / (D[n] + lambda));
+    c = r + rem;
+  } else {
+    r = e - nup;
+  }
+  double v = 0.0;
+  for (int n = threadIdx.x; n < N; n += MH_NT) {
+    const double br = Bn[static_cast<int64_t>(n) * nF + r];
+    if (br == 0.0) continue;
+    v += c >= 0 ? br * Bn[static_cast<int64_t>(n) * nF + c] / (D[n] + lambda) : br * (gn[n] / (D[n] + lambda));
+  }
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = MH_NT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (c >= 0) {
+      const double val = H[static_cast<int64_t>(r) * nF + c] + (r == c ? lambda : 0.0) - sh[0];
+      S[static_cast<int64_t>(r) * nF + c] = val;
+      S[static_cast<int64_t>(c) * nF + r] = val;
+    } else {
+      rhs[r] = -gF[r] + sh[0];
     }
-    rhs[r] = v;
   }
 }
 
@@ -461,6 +486,8 @@ class MhEngine {
   DBuf<int32_t> host_, obs_frame_, obs_point_;
   DBuf<int64_t> obs_ptr_, pair_ptr_, pair_obs_;
   DBuf<int2> pairs_;
+  DBuf<int32_t> pair_of_;   // K*K: pair index of (h, t)
+  DBuf<PairMap> maps_;
   DBuf<double2> anchor_, tnorm_;
   DBuf<double> tval_;
   DBuf<PoseD> pose_[2], pose_cand_;
@@ -553,6 +580,12 @@ MhEngine::MhEngine(const pba_mh_problem* p) {
   up(obs_frame_, ofr);
   up(obs_point_, opt);
   up(pairs_, pairs_h_);
+  {
+    std::vector<int32_t> pof(static_cast<size_t>(K_) * K_, -1);
+    for (size_t i = 0; i < pairs_h_.size(); ++i) pof[static_cast<size_t>(pairs_h_[i].x) * K_ + pairs_h_[i].y] = static_cast<int32_t>(i);
+    up(pair_of_, pof);
+    maps_.alloc(std::max<size_t>(pairs_h_.size(), 1));
+  }
   up(pair_ptr_, pptr);
   up(pair_obs_, pobs);
   std::vector<int32_t> host(p->host, p->host + N_);
@@ -650,17 +683,21 @@ void MhEngine::build_system(const PoseD* pose, const double* a) {
     count_launches(1);
   }
   const int nent = nF_ * nF_ + nF_;
-  k_mh_frames<<<(nent + 127) / 128, 128, 0, stream_>>>(dev_, np, pairs_.p, pose, a, pair_rec_.p, H_.p, gF_.p);
+  if (np > 0) {
+    k_mh_pairmap<<<(np + 63) / 64, 64, 0, stream_>>>(np, Q_, pairs_.p, pose, a, maps_.p);
+    count_launches(1);
+  }
+  k_mh_frames<<<(nent + 127) / 128, 128, 0, stream_>>>(dev_, np, pairs_.p, maps_.p, pair_rec_.p, H_.p, gF_.p);
   count_launches(1);
   if (N_ > 0) {
-    k_mh_point<<<(N_ + 127) / 128, 128, 0, stream_>>>(dev_, pose, a, rec_.p, Bn_.p, D_.p, gn_.p);
+    k_mh_point<<<(N_ + 127) / 128, 128, 0, stream_>>>(dev_, pair_of_.p, maps_.p, rec_.p, Bn_.p, D_.p, gn_.p);
     count_launches(1);
   }
 }
 
 bool MhEngine::solve(double lambda, int* flags_out) {
-  const int nent = nF_ * nF_ + nF_;
-  k_mh_schur<<<(nent + 127) / 128, 128, 0, stream_>>>(nF_, N_, H_.p, gF_.p, Bn_.p, D_.p, gn_.p, lambda, S_.p, rhs_.p);
+  const int nent = nF_ * (nF_ + 1) / 2 + nF_;
+  k_mh_schur<<<nent, MH_NT, 0, stream_>>>(nF_, N_, H_.p, gF_.p, Bn_.p, D_.p, gn_.p, lambda, S_.p, rhs_.p);
   count_launches(1);
   ck(cudaMemsetAsync(flags_.p, 0, 4 * sizeof(int), stream_), "flags");
   launch_chol_inv(S_.p, nF_, Dinv_.p, X_.p, XT_.p, flags_.p, bar_.p, stream_);

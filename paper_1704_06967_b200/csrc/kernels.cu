@@ -521,7 +521,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const double Rx0 = pe.R[0] * x + pe.R[1] * y + pe.R[2];
             const double Rx1 = pe.R[3] * x + pe.R[4] * y + pe.R[5];
             const double Rx2 = pe.R[6] * x + pe.R[7] * y + pe.R[8];
-            const double iz = 1.0 / vz;
+            const double iz = rcp_nr(vz);  // |vz| >= 1e-12 here (warp_point); <= 1 ulp from 1 / vz
             const double P02 = -vx * iz * iz, P12 = -vy * iz * iz;
             double row[7];
             row[0] = -(gx * (P02 * Rx1) + gy * (iz * -Rx2 + P12 * Rx1));

@@ -150,7 +150,7 @@ class Engine {
   DBuf<double> tval_;             // template values N*P
   DBuf<double4> tgrad_;           // template records {tval, gx, gy, 0} N*P (IC passes)
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
-  DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_;
+  DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_, tile_order_;
   DBuf<int32_t> uo2q_d_;         // caller obs -> frame-major obs q
   DBuf<int32_t> perm_d_;         // internal point -> user point (device copy)
   DBuf<int32_t> zero_idx_;       // scratch: compacted user indices (+1 counter slot)

@@ -362,7 +362,29 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
     up(ftile_ptr_, ftile_ptr);
     ftile_ptr_h_ = ftile_ptr;
     ov_.ntiles = static_cast<int>(tile_frame.size());
-    ck(cudaStreamSynchronize(s), "tiles sync");
+    // Launch order of the lane passes: within each group of kTabFrames frames (one IC-pass launch),
+    // tiles sorted by their first point, then frame, so that the CTAs resident together work on
+    // the same points in neighbouring frames and share the points' template records in L2.
+    // Env PBA_TILE_ORDER=0 keeps the frame-major order.
+    tile_order_.release();
+    const char* env = std::getenv("PBA_TILE_ORDER");
+    if (!(env && env[0] == '0') && ov_.ntiles > 0) {
+      DBuf<int32_t> key;
+      key.alloc(ov_.ntiles);
+      launch_tile_first_point(ov_.ntiles, tile_q0_.p, fm_point_.p, key.p, s);
+      std::vector<int32_t> kh(ov_.ntiles);
+      ck(cudaMemcpyAsync(kh.data(), key.p, ov_.ntiles * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "tile keys");
+      ck(cudaStreamSynchronize(s), "tile keys sync");
+      std::vector<int32_t> order(ov_.ntiles);
+      for (int g0 = 0; g0 < F_; g0 += kTabFrames) {
+        const int t0 = ftile_ptr[g0], t1 = ftile_ptr[std::min(F_, g0 + kTabFrames)];
+        for (int t = t0; t < t1; ++t) order[t] = t;
+        std::stable_sort(order.begin() + t0, order.begin() + t1,
+                         [&](int32_t x, int32_t y) { return kh[x] < kh[y]; });  // ties: frame order
+      }
+      up(tile_order_, order);
+      ck(cudaStreamSynchronize(s), "tile order sync");
+    }
   }
 
   trace_mark(s, "layout: tiles");
@@ -456,6 +478,7 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
   ov_.tile_q0 = tile_q0_.p;
   ov_.tile_q1 = tile_q1_.p;
   ov_.ftile_ptr = ftile_ptr_.p;
+  ov_.tile_order = tile_order_.p;
 }
 
 // ---- per-observation conversions between the caller's order and the frame-major layout ----

@@ -386,7 +386,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   constexpr int OPB = NT / LPO;  // observations per block step
   constexpr bool kH = (MODE != OBS_IC);         // builds J^T W J, B, D
   constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC);
-  const int t = kTab ? tab.tile0 + static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+  const int tb = kTab ? tab.tile0 + static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
+  const int t = a.ov.tile_order ? a.ov.tile_order[tb] : tb;  // launch order only: partials stay per tile
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t], q1 = a.ov.tile_q1[t];
   __shared__ __align__(16) PoseD s_pe, s_p0;
@@ -2068,6 +2069,17 @@ __global__ void k_dense_rows(const int32_t* __restrict__ chunk_pts, int npts, co
   const int c = chunk_of[p];
   const int4 ch = chunks[c];
   dense_row[chunk_pts[p]] = chunk_off[c] + static_cast<int64_t>(p - ch.x) * ch.w - 6 * ch.z;
+}
+
+__global__ void k_tile_first_point(int ntiles, const int64_t* __restrict__ tile_q0, const int32_t* __restrict__ fm_point,
+                                   int32_t* __restrict__ key) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) key[t] = fm_point[tile_q0[t]];
+}
+void launch_tile_first_point(int ntiles, const int64_t* tile_q0, const int32_t* fm_point, int32_t* key, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  k_tile_first_point<<<(ntiles + 255) / 256, 256, 0, s>>>(ntiles, tile_q0, fm_point, key);
+  count_launches(1);
 }
 
 void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s) {

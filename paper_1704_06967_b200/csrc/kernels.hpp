@@ -207,6 +207,8 @@ struct SchurPlan {
   const int4* blocks;        // per work item {chunk, 0, 0, rb | cb << 16}
   int nblocks;
 };
+// key[t] = internal point of the first observation of tile t
+void launch_tile_first_point(int ntiles, const int64_t* tile_q0, const int32_t* fm_point, int32_t* key, cudaStream_t s);
 // dense_row[n] = chunk_off + (p - chunk begin) * LD - 6 fmin for the p-th window-sorted point n
 void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s);
 // Deterministic (64-bit fixed-point) accumulation; scale: 6F scratch, acc: 36F^2 scratch.

@@ -96,7 +96,7 @@ constexpr size_t kEnergySmem = kStages * kEnergyStageBytes;
 template <int G>
 __global__ void __launch_bounds__(NT_OBS, PBA_OBS_MINB_IC) k_obs_energy(const ObsArgs a) {
   constexpr int OPS = NT / G;  // observations per block step
-  const int t = blockIdx.x;
+  const int t = a.ov.tile_order ? a.ov.tile_order[blockIdx.x] : static_cast<int>(blockIdx.x);  // launch order only
   const int f = a.ov.tile_frame[t];
   const int64_t q0 = a.ov.tile_q0[t];
   const int64_t q1 = a.ov.tile_q1[t];
@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
 __global__ void __launch_bounds__(NT) k_cf(const ObsView ov, const double* __restrict__ B,
                                            const double* __restrict__ s_n, double* __restrict__ partial,
                                            const MaxUpdArgs mu) {
-  const int t = blockIdx.x;
+  const int t = ov.tile_order ? ov.tile_order[blockIdx.x] : static_cast<int>(blockIdx.x);  // launch order only
   const int64_t q0 = ov.tile_q0[t], q1 = ov.tile_q1[t];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool want_upd = mu.pose_cand != nullptr;

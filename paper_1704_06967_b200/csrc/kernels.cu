@@ -1339,7 +1339,7 @@ __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const d
 // K loop streams SY_KB points per stage into shared memory with cp.async (2 stages,
 // zero-filled past the chunk end); the weight w_p = 1/(D_n + lambda) scales the A fragment.
 constexpr int SY_KB = 32;      // points per stage
-constexpr int SY_LDS = 72;     // smem row stride (doubles): fragment loads are 2 wavefronts
+constexpr int SY_LDS = 68;     // smem row stride (doubles): 68 = 4 mod 16 puts the 4 k-rows of a half-warp fragment load on distinct banks (2 wavefronts)
 constexpr int SY_STAGES = 2;
 constexpr int SY_THREADS = 128;
 constexpr size_t SY_SMEM = static_cast<size_t>(SY_STAGES) * (2 * SY_KB * SY_LDS + SY_KB) * sizeof(double);

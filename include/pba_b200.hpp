@@ -331,4 +331,105 @@ inline std::vector<double> solve_normal_equations_schur(const BlockHessian& H, c
   return dx;
 }
 
+// ---- joint multi-host window with per-frame affine brightness (pba_gpu_mh_*; no reference
+//      counterpart: the model is stated in oracle/multihost.cpp) ----
+struct MultiHostProblem {
+  std::vector<Image> images;               // K frames, each with its intrinsics; frame 0 held
+  std::vector<Pose> poses;                 // K: X_i = R_i X_w + t_i
+  std::vector<double> affine_a, affine_b;  // K or empty (= 0)
+  std::vector<int32_t> host;               // N
+  std::vector<std::array<double, 2>> anchors_px;
+  std::vector<double> inv_depths;
+  std::vector<std::array<int32_t, 2>> pattern{{0, 0}, {-1, -1}, {0, -1}, {1, -1}, {-1, 0},
+                                              {1, 0},  {-1, 1},  {0, 1},  {1, 1}};
+  std::vector<int64_t> obs_ptr;            // CSR of target frames (empty = every other frame)
+  std::vector<int32_t> obs_frame;
+  bool optimize_affine{true};
+};
+struct MultiHostReport : SolveReport {
+  std::vector<double> final_a, final_b;
+};
+
+inline MultiHostReport mh_fc_solve(const MultiHostProblem& p, const SolverConfig& config) {
+  const int K = static_cast<int>(p.images.size()), N = static_cast<int>(p.anchors_px.size());
+  std::vector<pba_image> im(K);
+  std::vector<double> R(9 * static_cast<size_t>(K)), t(3 * static_cast<size_t>(K)), an(2 * static_cast<size_t>(N));
+  std::vector<int32_t> pat;
+  for (int f = 0; f < K; ++f) {
+    const Image& g = p.images[f];
+    im[f] = pba_image{g.width, g.height, g.K.fx, g.K.fy, g.K.cx, g.K.cy, g.data.data()};
+    for (int i = 0; i < 9; ++i) R[9 * f + i] = p.poses[f].R[i];
+    for (int i = 0; i < 3; ++i) t[3 * f + i] = p.poses[f].t[i];
+  }
+  for (int n = 0; n < N; ++n) {
+    an[2 * n] = p.anchors_px[n][0];
+    an[2 * n + 1] = p.anchors_px[n][1];
+  }
+  for (const auto& o : p.pattern) {
+    pat.push_back(o[0]);
+    pat.push_back(o[1]);
+  }
+  pba_mh_problem q{};
+  q.num_frames = K;
+  q.images = im.data();
+  q.pose_R = R.data();
+  q.pose_t = t.data();
+  q.affine_a = p.affine_a.empty() ? nullptr : p.affine_a.data();
+  q.affine_b = p.affine_b.empty() ? nullptr : p.affine_b.data();
+  q.num_points = N;
+  q.host = p.host.data();
+  q.anchors_px = an.data();
+  q.inv_depths = p.inv_depths.data();
+  q.pattern_size = static_cast<int32_t>(p.pattern.size());
+  q.pattern = pat.data();
+  q.obs_ptr = p.obs_ptr.empty() ? nullptr : p.obs_ptr.data();
+  q.obs_frame = p.obs_frame.empty() ? nullptr : p.obs_frame.data();
+  q.optimize_affine = p.optimize_affine ? 1 : 0;
+  pba_mh_handle* h = nullptr;
+  throw_status(pba_gpu_mh_create(&q, &h), pba_gpu_mh_last_error(nullptr));
+  std::unique_ptr<pba_mh_handle, void (*)(pba_mh_handle*)> guard(h, pba_gpu_mh_destroy);
+  const int cap = config.max_iters > 0 ? config.max_iters : 1;
+  MultiHostReport out;
+  std::vector<double> Rf(9 * static_cast<size_t>(K)), tf(3 * static_cast<size_t>(K));
+  out.final_inv_depths.resize(N);
+  out.final_a.resize(K);
+  out.final_b.resize(K);
+  std::vector<pba_iter_stats> its(cap);
+  pba_report rep{};
+  rep.final_R = Rf.data();
+  rep.final_t = tf.data();
+  rep.final_inv_depths = out.final_inv_depths.data();
+  rep.iters = its.data();
+  rep.iters_capacity = cap;
+  const pba_config c = config.c();
+  throw_status(pba_gpu_mh_fc_run(h, &c, &rep, out.final_a.data(), out.final_b.data()), pba_gpu_mh_last_error(h));
+  out.converged = rep.converged;
+  out.diverged = rep.diverged;
+  out.iterations = rep.iterations;
+  out.hessian_builds = rep.hessian_builds;
+  out.hessian_factorizations = rep.hessian_factorizations;
+  out.rejected_steps = rep.rejected_steps;
+  out.final_energy = rep.final_energy;
+  out.total_wall_ms = rep.total_wall_ms;
+  out.masked_residuals = rep.masked_residuals;
+  out.message = rep.message;
+  for (int f = 0; f < K; ++f) {
+    Pose q2;
+    for (int i = 0; i < 9; ++i) q2.R[i] = Rf[9 * f + i];
+    for (int i = 0; i < 3; ++i) q2.t[i] = tf[3 * f + i];
+    out.final_poses.push_back(q2);
+  }
+  for (int i = 0; i < rep.num_iters; ++i) {
+    IterationStats st;
+    st.iter = its[i].iter;
+    st.energy = its[i].energy;
+    st.max_update_px = its[i].max_update_px;
+    st.wall_ms = its[i].wall_ms;
+    st.hessian_builds = its[i].hessian_builds;
+    st.hessian_factorizations = its[i].hessian_factorizations;
+    out.iters.push_back(st);
+  }
+  return out;
+}
+
 }  // namespace pba_b200

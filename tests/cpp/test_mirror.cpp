@@ -149,6 +149,34 @@ static void zero_translation_warning() {  // test_solver.cpp:266-278
   for (double dd : s.hessian().depth_depth) CHECK(dd == 0.0);
 }
 
+static void joint_window_reduces_to_fc() {  // the joint window of a single-host problem = fc_solve
+  auto pr = make_pair(oracle::render_sequence(small_spec(3, 10)), 1, 1e-3, 8);
+  pba_b200::MultiHostProblem w;
+  w.images.push_back(pr.g.ref);
+  w.poses.push_back(pba_b200::Pose{});
+  for (size_t f = 0; f < pr.g.targets.size(); ++f) {
+    w.images.push_back(pr.g.targets[f]);
+    w.poses.push_back(pr.g.poses[f]);
+  }
+  w.host.assign(pr.g.anchors_px.size(), 0);
+  w.anchors_px = pr.g.anchors_px;
+  w.inv_depths = pr.g.inv_depths;
+  w.pattern = pr.g.pattern;
+  w.optimize_affine = false;
+  pba_b200::SolverConfig cfg;
+  cfg.max_iters = 10;
+  const auto r = pba_b200::mh_fc_solve(w, cfg);
+  oracle::SolverConfig oc;
+  oc.max_iters = 10;
+  const auto ref = oracle::fc_solve(pr.o, oc);
+  CHECK(r.iterations == ref.iterations);
+  CHECK(r.converged == ref.converged);
+  CHECK(std::abs(r.final_energy - ref.final_energy) <= 1e-5 * ref.final_energy);
+  CHECK(r.final_poses.size() == pr.g.poses.size() + 1 && r.final_a.size() == w.images.size());
+  for (size_t n = 0; n < ref.final_inv_depths.size(); ++n)
+    CHECK(std::abs(r.final_inv_depths[n] - ref.final_inv_depths[n]) <= 1e-4 * std::abs(ref.final_inv_depths[n]));
+}
+
 int main() {
   struct {
     const char* name;
@@ -157,7 +185,8 @@ int main() {
                {"energy_eval throws when nothing is in bounds", empty_problem_throws},
                {"one IC step equals the oracle (gauge removed)", ic_step_matches_oracle},
                {"noisy start: both converge, counters correct", noisy_start_counters},
-               {"zero initial translation warning", zero_translation_warning}};
+               {"zero initial translation warning", zero_translation_warning},
+               {"joint multi-host window of a single-host problem = fc_solve", joint_window_reduces_to_fc}};
   int failed = 0;
   for (auto& c : cases) {
     const int before = g_fail;

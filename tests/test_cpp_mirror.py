@@ -19,4 +19,4 @@ def test_cpp_mirror_cases():
         subprocess.run(["make", "-C", str(REPO / "oracle"), "mirror"], check=True)
     out = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("PASS") == 5, out.stdout
+    assert out.stdout.count("PASS") == 6 and "FAIL" not in out.stdout, out.stdout

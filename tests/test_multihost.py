@@ -144,3 +144,14 @@ def test_gpu_window_errors():
         mh.MultiHostHandle(mh.MultiHostProblem(**{**sc.problem.__dict__, "anchors_px": an}), "gpu").energy(9.0)
     with pytest.raises(solver.Error):
         mh.MultiHostHandle(mh.MultiHostProblem(**{**sc.problem.__dict__, "host": np.full(15, 9, np.int32)}), "gpu")
+
+
+@pytest.mark.gpu
+def test_gpu_joint_c2_full_size_matches_oracle():
+    """BASELINE C2 joint form at full size: 7 keyframes x 2000 points, 640x480, 5 iterations."""
+    sc = scenes.make_window_scene(device="cpu")
+    cfg = sc.solver_config(threshold_px=0.0)
+    rg = mh.mh_fc_solve(sc.problem, cfg)
+    ro = mh.mh_fc_solve(sc.problem, cfg, backend="oracle")
+    _runs_close(rg, ro)
+    assert np.abs(rg.final_b - ro.final_b).max() <= 1e-3 and np.abs(rg.final_a - ro.final_a).max() <= 1e-5

@@ -140,15 +140,11 @@ int pba_gpu_ic_hessian(pba_handle* h, double* pp, double* dd, double* pd, double
   return guarded(h, [&](Engine& e) { e.ic_hessian(pp, dd, pd, lambda); });
 }
 int pba_gpu_warning_count(const pba_handle* h) {
-  return (h && h->e) ? static_cast<int>(h->e->warnings().size()) : 0;
+  return (h && h->e) ? static_cast<int>(h->e->warning_count()) : 0;
 }
 int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len) {
   if (!h || !h->e) return 0;
-  std::string all;
-  for (const auto& w : h->e->warnings()) {
-    if (!all.empty()) all += '\n';
-    all += w;
-  }
+  const std::string& all = h->e->warnings_text();
   if (buf && len > 0) {
     const size_t n = std::min<size_t>(all.size(), static_cast<size_t>(len - 1));
     std::memcpy(buf, all.data(), n);
@@ -157,8 +153,8 @@ int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len) {
   return static_cast<int64_t>(all.size());
 }
 int pba_gpu_warning(const pba_handle* h, int i, char* buf, int len) {
-  if (!h || !h->e || i < 0 || i >= static_cast<int>(h->e->warnings().size()) || !buf || len <= 0) return PBA_E_ARG;
-  std::snprintf(buf, len, "%s", h->e->warnings()[i].c_str());
+  if (!h || !h->e || i < 0 || i >= h->e->warning_count() || !buf || len <= 0) return PBA_E_ARG;
+  std::snprintf(buf, len, "%s", h->e->warning(i).c_str());
   return PBA_OK;
 }
 int pba_gpu_ic_begin(pba_handle* h, const pba_config* cfg) {

@@ -2,6 +2,7 @@
 // Control flow mirrors /root/reference/proj/src/solver.cpp line by line (cited);
 // every per-pixel / per-point / per-frame computation is a kernel in kernels.cu.
 #include <algorithm>
+#include <charconv>
 #include <unordered_map>
 #include <mutex>
 #include <chrono>
@@ -745,9 +746,37 @@ void Engine::solve_xp(const double* rhs) {
   ev_end(PBA_K_TRISOLVE, e);
 }
 
+static const char kZeroD[] = ": zero depth Hessian entry (unobservable depth)";
+
+std::string Engine::warning(int64_t i) const {
+  if (i < static_cast<int64_t>(ic_.warnings.size())) return ic_.warnings[i];
+  return "point " + std::to_string(ic_.zero_d[i - ic_.warnings.size()]) + kZeroD;
+}
+
+const std::string& Engine::warnings_text() const {
+  if (wtext_ok_) return wtext_;
+  wtext_.clear();
+  wtext_.reserve(ic_.warnings.size() * 80 + ic_.zero_d.size() * (sizeof(kZeroD) + 16));
+  for (const auto& w : ic_.warnings) {
+    if (!wtext_.empty()) wtext_ += '\n';
+    wtext_ += w;
+  }
+  char num[16];
+  for (const int32_t u : ic_.zero_d) {
+    if (!wtext_.empty()) wtext_ += '\n';
+    wtext_ += "point ";
+    const auto r = std::to_chars(num, num + sizeof(num), u);
+    wtext_.append(num, r.ptr);
+    wtext_.append(kZeroD, sizeof(kZeroD) - 1);
+  }
+  wtext_ok_ = true;
+  return wtext_;
+}
+
 // IcSolver::build (solver.cpp:254-368)
 void Engine::ic_build(const pba_config* cfg) {
   ic_ = SolverState{};
+  wtext_ok_ = false;
   if (cfg) {
     ic_.cfg = *cfg;
   } else {
@@ -803,14 +832,12 @@ void Engine::ic_build(const pba_config* cfg) {
   alloc_schur();
   trace_mark(stream_, "ic_build: Bpm+schur alloc");
   launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
+  trace_mark(stream_, "ic_build: B point-major copy");
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
   ic_.mcur = 0;
-  {  // :359-364 zero depth Hessian warnings, in user point order (compacted on the device)
-    const std::vector<int32_t> zu = zero_depth_points(Dic_.p);
-    for (const int32_t u : zu)
-      ic_.warnings.push_back("point " + std::to_string(u) + ": zero depth Hessian entry (unobservable depth)");
-  }
+  ic_.zero_d = zero_depth_points(Dic_.p);  // :359-364, user point order (compacted on the device)
+  wtext_ok_ = false;
   ic_.builds = 1;
   trace_mark(stream_, "ic_build: D, B copy, warnings");
   ic_factorize_loop(ic_.lambda);

@@ -75,7 +75,8 @@ struct SolverState {
   int builds = 0;
   int factorizations = 0;
   int mcur = 0;  // index of the sticky residual mask in mask_[] (solver.hpp:162)
-  std::vector<std::string> warnings;
+  std::vector<std::string> warnings;  // frame warnings (solver.cpp:265-271)
+  std::vector<int32_t> zero_d;        // user indices of the D_n == 0 points (:359-364), formatted on request
 };
 
 class Engine {
@@ -110,7 +111,11 @@ class Engine {
   cudaStream_t stream() const { return stream_; }
   void set_profiling(bool on);
   void kernel_times(int64_t* counts, double* total_ms);
-  const std::vector<std::string>& warnings() const { return ic_.warnings; }
+  // IcSolver::warnings() (solver.hpp:130): the frame warnings, then one per zero-D point; the
+  // per-point strings (tens of thousands at C4) are formatted once, on request
+  int64_t warning_count() const { return static_cast<int64_t>(ic_.warnings.size() + ic_.zero_d.size()); }
+  std::string warning(int64_t i) const;
+  const std::string& warnings_text() const;
 
   std::string last_error;
 
@@ -196,6 +201,8 @@ class Engine {
   int* flags_h_ = nullptr;        // pinned
 
   SolverState ic_;
+  mutable std::string wtext_;       // cache of warnings_text()
+  mutable bool wtext_ok_ = false;
 
   // rank exchange of point-sharded runs (null fn = single process)
   struct Xch {

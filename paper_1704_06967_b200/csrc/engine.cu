@@ -263,10 +263,18 @@ Engine::~Engine() {
   set_alloc_stream(stream_);  // members free stream-ordered; sh_ destroys the stream last
 }
 
-int64_t Engine::device_bytes() const {
-  int64_t b = images_.bytes() + J_.bytes() + S_.bytes() + rec_.bytes() + partial_.bytes();
-  for (int i = 0; i < 2; ++i) b += B_[i].bytes() + D_[i].bytes() + mask_[i].bytes();
-  return b + pm2fm_.bytes() + fm_point_.bytes() + pm_frame_.bytes();
+int64_t Engine::device_bytes() const {  // every device buffer the handle holds
+  int64_t b = 0;
+  auto add = [&b](const auto&... bufs) { ((b += static_cast<int64_t>(bufs.bytes())), ...); };
+  add(images_, frames_, anchor_, anchor_fm_, tval_, tgrad_, pm_ptr_, fm_ptr_, tile_q0_, tile_q1_, pm_frame_, pm2fm_,
+      fm_point_, tile_frame_, ftile_ptr_, tile_order_, uo2q_d_, perm_d_, zero_idx_, perm_tmp_, pose_state_,
+      pose_cur_, pose_cand_, pose0_, d_state_, d_cur_, d_cand_, d0_, scratch_bits_, J_, Bic_, Dic_, Hic_, Bpm_,
+      rec_, rec_g_, s_n_, dx_n_, xp_, g_tmp_, r_out_, partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_,
+      fscal_, ticket_, S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_, schur_acc_, chunk_pts_,
+      schur_chunk_of_, schur_blocks_, schur_chunks_, schur_chunk_off_, schur_dense_, schur_wsort_, dense_row_,
+      status_, flags_, xsend_, xrecv_, cf_, gauge_sum_);
+  for (int i = 0; i < 2; ++i) add(mask_[i], B_[i], D_[i], H_[i], gn_[i], gf_[i], rhs_[i]);
+  return b;
 }
 
 // =====================================================================================

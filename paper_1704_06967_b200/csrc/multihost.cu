@@ -9,7 +9,7 @@
 //                record of sums in RELATIVE coordinates: z = [J_omega, J_dt, J_d, j_a] of the
 //                reference's FC row at the relative pose plus the affine column; Z = sum w z z^T,
 //                sum w z, sum w, sum w r z, sum w r; plus energy / counts / max update per obs.
-//   k_mh_pair    per (host, target) pair: the records of its observations summed in order; the
+//   k_mh_pair_*  per (host, target) pair: the records of its observations summed in order; the
 //                pair's chain matrix T (absolute <- relative increments: [u]x, R_th, alpha, b_h)
 //                is a pair constant, so H_FF and g_F come from the pair sums (linearity).
 //   k_mh_frames  H_FF and g_F: every entry sums its pairs' mapped blocks in pair order.
@@ -255,15 +255,26 @@ __global__ void k_mh_pairmap(int npairs, int Q, const int2* __restrict__ pairs, 
   maps[p] = pm;
 }
 
-// per pair p = (h, t): records of its observations summed in q order
-__global__ void k_mh_pair(const int64_t* __restrict__ pair_ptr, const int64_t* __restrict__ pair_obs,
-                          const double* __restrict__ rec, double* __restrict__ pair_rec) {
-  const int p = blockIdx.x;
-  for (int i = threadIdx.x; i < MH_REC; i += blockDim.x) {
-    double v = 0.0;
-    for (int64_t j = pair_ptr[p]; j < pair_ptr[p + 1]; ++j) v += rec[pair_obs[j] * MH_REC + i];
-    pair_rec[static_cast<int64_t>(p) * MH_REC + i] = v;
-  }
+// per pair p = (h, t): records of its observations summed in q order, in two fixed-order levels:
+// block (p, s) sums segment s of the pair's list (thread i = record entry i, coalesced 432-byte
+// records), then k_mh_pair_sum adds the segments in order
+constexpr int MH_SEG = 32;
+__global__ void k_mh_pair_seg(const int64_t* __restrict__ pair_ptr, const int64_t* __restrict__ pair_obs,
+                              const double* __restrict__ rec, double* __restrict__ seg_rec) {
+  const int p = blockIdx.x, sg = blockIdx.y, i = threadIdx.x;
+  const int64_t a = pair_ptr[p], len = pair_ptr[p + 1] - a;
+  const int64_t j0 = a + len * sg / MH_SEG, j1 = a + len * (sg + 1) / MH_SEG;
+  if (i >= MH_REC) return;
+  double v = 0.0;
+  for (int64_t j = j0; j < j1; ++j) v += rec[pair_obs[j] * MH_REC + i];
+  seg_rec[(static_cast<int64_t>(p) * MH_SEG + sg) * MH_REC + i] = v;
+}
+__global__ void k_mh_pair_sum(const double* __restrict__ seg_rec, double* __restrict__ pair_rec) {
+  const int p = blockIdx.x, i = threadIdx.x;
+  if (i >= MH_REC) return;
+  double v = 0.0;
+  for (int sg = 0; sg < MH_SEG; ++sg) v += seg_rec[(static_cast<int64_t>(p) * MH_SEG + sg) * MH_REC + i];
+  pair_rec[static_cast<int64_t>(p) * MH_REC + i] = v;
 }
 
 // H_FF (nF x nF, full) and g_F: one thread per (entry | gradient row), pairs in order
@@ -492,7 +503,7 @@ class MhEngine {
   DBuf<double> tval_;
   DBuf<PoseD> pose_[2], pose_cand_;
   DBuf<double> a_[2], b_[2], d_[2], a_cand_, b_cand_, d_cand_;
-  DBuf<double> rec_, pair_rec_, H_, gF_, Bn_, D_, gn_, S_, rhs_, X_, XT_, Dinv_, y_, xp_;
+  DBuf<double> rec_, pair_rec_, seg_rec_, H_, gF_, Bn_, D_, gn_, S_, rhs_, X_, XT_, Dinv_, y_, xp_;
   DBuf<double4> stat_, part_;
   DBuf<int> flags_;
   DBuf<unsigned int> bar_;
@@ -639,6 +650,7 @@ MhEngine::MhEngine(const pba_mh_problem* p) {
   nparts_ = static_cast<int>(std::min<int64_t>(std::max<int64_t>((NO_ + MH_NT - 1) / MH_NT, 1), 1024));
   part_.alloc(nparts_);
   pair_rec_.alloc(std::max<size_t>(pairs_h_.size(), 1) * MH_REC);
+  seg_rec_.alloc(std::max<size_t>(pairs_h_.size(), 1) * MH_SEG * MH_REC);
   H_.alloc(static_cast<size_t>(nF_) * nF_);
   gF_.alloc(nF_);
   Bn_.alloc(std::max<size_t>(static_cast<size_t>(N_) * nF_, 1));
@@ -679,8 +691,9 @@ MhEngine::Eval MhEngine::evaluate(double gamma, const PoseD* pose, const double*
 void MhEngine::build_system(const PoseD* pose, const double* a) {
   const int np = static_cast<int>(pairs_h_.size());
   if (np > 0) {
-    k_mh_pair<<<np, 64, 0, stream_>>>(pair_ptr_.p, pair_obs_.p, rec_.p, pair_rec_.p);
-    count_launches(1);
+    k_mh_pair_seg<<<dim3(np, MH_SEG), 64, 0, stream_>>>(pair_ptr_.p, pair_obs_.p, rec_.p, seg_rec_.p);
+    k_mh_pair_sum<<<np, 64, 0, stream_>>>(seg_rec_.p, pair_rec_.p);
+    count_launches(2);
   }
   const int nent = nF_ * nF_ + nF_;
   if (np > 0) {

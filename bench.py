@@ -295,6 +295,7 @@ def cpu_baseline_threads(st, cfg, npts_per_thread, threads, seed=0, iters=3):
     ms = max(r[1] for r in res)
     v = px / (ms / 1e3) if ms > 0 else 0.0
     return {"value": v, "unit": "obs_px/s", "cores": threads, "kind": "port",
+            "ms_per_iter": ms / max(iters - 1, 1),
             "sample": f"{threads} threads x {npts_per_thread} of {st.num_points} points (all frames, independent "
                       f"samples), {iters} IC iterations each, {sum(r[2] for r in res)} observations in total; "
                       f"oracle/ single-threaded fp64 restatement of solver.cpp per thread; {wall:.1f} s"}
@@ -498,7 +499,8 @@ def main():
         cb["value"] = v
         line = {"impl": "reference", "metric": "obs_px_per_s_per_LM_iteration", "value": v, "unit": "obs_px/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "ms_per_step": statistics.median([c["ms_per_iter"] for c in vals]), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic", "config": {"workload": f"BASELINE {args.config} (IC-proxy LM iteration)",
                                                                   "frames": st.num_frames,
                                                                   "points": st.num_points},

@@ -169,7 +169,7 @@ def ncu_profile_extra():
             return None
         k = ks[0]
         pick = lambda key: float(k[key].split()[0]) if key in k else None  # noqa: E731
-        return {"fp64_pipe_pct": pick("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        return {"fp64_pipe_pct": pick("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
                 "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 "dram_pct_of_theoretical": pick("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
     except Exception:
@@ -188,24 +188,24 @@ def ncu_traffic():
 
 
 def obs_pass_bytes(st, n_px_active):
-    """Algorithmic DRAM bytes of one IC obs-pass launch:
-    24 B per active pixel (factored frozen IC Jacobian m, 3 doubles; the row is rebuilt from m
-    and the frozen pose / depth) + per observation 44 B (anchor 16, point id 4, mask 4,
-    active bits 4, record 16) + per point 80 B (candidate depth 8, frozen depth 8, template
-    values 8P with P = 8; gathers counted once per point) + the fp32 target images once +
-    the reference image once."""
+    """Minimal DRAM bytes of one IC pass as implemented: the frozen rows are rebuilt
+    from the per-(point, pixel) template records, so nothing is read per pixel; per observation 36 B
+    (anchor 16, point id 4, sticky mask 4, active bits 4, g_n term 8); per point 16 + 32 P B (candidate
+    and frozen depth, the 32-byte template records {tval, gx, gy, 0}, each read once); the fp32 target
+    images and the reference image once.  ncu's measured traffic is compared with this."""
     H, W = st.ref.shape
     F = st.num_frames
     NO = st.num_observations
     P = st.pattern.shape[0]
-    return 24 * n_px_active + 44 * NO + (16 + 8 * P) * st.num_points + 4 * F * H * W + 4 * H * W
+    del n_px_active  # no per-pixel stream: the rows are recomputed
+    return 36 * NO + (16 + 32 * P) * st.num_points + 4 * F * H * W + 4 * H * W
 
 
 def survey_obs_pass_bytes(st, n_px_active):
     """SURVEY.md 8d's per-unit figure for the IC observation pass (the K1 terms of B_IC):
     56 B per active pixel (frozen fp64 J row) + 4 N P (fp32 template) + 8 N_obs (observation
     record) + 4 F W H (targets once) + 24 N (depth read, g_n write) + 96 F (pose read, g_pose write).
-    The implementation stores the rows factored (24 B/px) and rebuilds them, so dividing this
+    The implementation stores no rows (it rebuilds them from the template records), so dividing this
     figure by the launch time is the effective bandwidth SURVEY 8d asks for in that case."""
     H, W = st.ref.shape
     P = st.pattern.shape[0]
@@ -572,22 +572,25 @@ def main():
                    "points": st.num_points, "observations": st.num_observations,
                    "pattern": int(st.pattern.shape[0]), "image": list(st.ref.shape[::-1]),
                    "active_obs_px_per_iter": r["n_px_iter"], "accepted_steps": r["accepted"],
-                   "l2": "inputs larger than L2 (factored frozen IC Jacobian %.1f GB)" % (24 * st.num_observations * st.pattern.shape[0] / 1e9),
+                   "l2": "inputs larger than L2 (per-iteration working set: frozen B blocks 2 x %.1f GB, anchors "
+                         "%.1f GB, images %.2f GB)" % (48 * st.num_observations / 1e9, 16 * st.num_observations / 1e9,
+                                                       4 * (st.num_frames + 1) * st.ref.size / 1e9),
                    "parallelism": (f"point-sharded x{world}" if args.mode == "sharded"
                                    else ("replicas" if world > 1 else "single"))},
-        "roofline": {"bound": "hbm", "kernel": "k_obs_lane<OBS_IC> fused residual/Huber/J^T W r pass (factored J)",
+        "roofline": {"bound": "hbm", "kernel": "k_obs_lane<OBS_IC> fused residual/Huber/J^T W r pass (rows rebuilt)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(), "alg_bytes_per_launch": svy,
-                     "factored_bytes_per_launch": alg,
-                     "factored_frac": alg / (obs_ms / 1e3) / 1e9 / peak,
+                     "min_dram_bytes_per_pass": alg,
+                     "min_dram_frac": alg / (obs_ms / 1e3) / 1e9 / peak,
                      "launch_ms": obs_ms, "share_of_step": obs_ms / per_step_ms,
                      "canonical_B_IC_per_iter": bic, "canonical_effective_GBs": bic / (per_step_ms / 1e3) / 1e9,
                      "canonical_frac": bic / (per_step_ms / 1e3) / 1e9 / peak,
                      "ncu": ncu_profile_extra(),
                      "note": "achieved = SURVEY 8d per-unit bytes of the IC pass (56 B/px J rows, K1 terms of B_IC) "
-                             "/ launch time: an effective bandwidth, since the pass stores the rows factored "
-                             "(24 B/px, factored_bytes_per_launch) and rebuilds them; traffic = ncu DRAM bytes "
-                             "of one pass; canonical_* = full B_IC over the whole iteration"},
+                             "/ launch time: an effective bandwidth, since the pass stores no rows and rebuilds them "
+                             "from 32-byte per-(point, pixel) template records; min_dram_bytes_per_pass = what it "
+                             "must move; traffic = ncu DRAM bytes of one pass; the binding resource is L1/L2-hit "
+                             "latency and issue (ncu); canonical_* = full B_IC over the whole iteration"},
         "kernel_ms_per_iter": {n: round(v[1] / args.steps, 4) for n, v in kt.items() if v[0]},
         "clocks": r["clocks"],
         "gpu_launches": int(r["launches"]),

@@ -1,18 +1,21 @@
 // B200 (sm_100a) kernels for the per-iteration photometric bundle adjustment step.
 //
-// Work decomposition (DESIGN.md §3):
-//   k_obs      frame-major fused pass over observation pixels: warp, bilinear,
-//              Huber residual, Jacobian (frozen IC rows / FC rows / IC build),
-//              per-frame J^T W r and J^T W J as per-lane register sums reduced
-//              once per tile, per-observation records reduced over the G lanes
-//              of the pattern.                         solver.cpp:63-103,306-358,450-468,688-724
+// Work decomposition (DESIGN.md §3-4):
+//   k_obs_lane / k_obs_lane_tab
+//              frame-major fused pass, one lane per observation over its pattern pixels: warp,
+//              bilinear (lerp form), Huber residual, Jacobian (IC rows rebuilt from the template
+//              records / FC rows / IC build), per-frame J^T W r and J^T W J as per-lane register
+//              sums reduced once per tile; tiles launched point-block major (tile_order).
+//                                                       solver.cpp:63-103,306-358,450-468,688-724
+//   k_obs_energy  residual / Huber only (energy_eval), TMA-staged G-lane pass.   solver.cpp:229-244
 //   k_backsub  point-major depth back-substitution + candidate depth.  solver.cpp:418-428,553-560,747-750
 //   k_point    point-major gather of per-observation records -> g_n, D_n, s_n.
-//   k_cf       frame-major  c_f = sum_n B_nf g_n/(D_n+lambda).           solver.cpp:407-416
+//   k_cf       frame-major  c_f = sum_n B_nf g_n/(D_n+lambda) + max reprojection update.  solver.cpp:407-416
 //   k_finalize deterministic fixed-order reduction of tile partials -> status.
-//   k_schur    reduced camera system.                                   solver.cpp:170-189,375-392
-//   k_chol_*   blocked right-looking fp64 Cholesky (stands in for Eigen::LDLT, solver.cpp:190,393).
-//   k_tri_*    explicit L^-1 per factorization + two GEMVs per solve.   solver.cpp:417
+//   k_schur_*  reduced camera system: chunked DMMA SYRK, 64-bit fixed point.  solver.cpp:170-189,375-392
+//   k_chol_inv fused blocked Cholesky + explicit L^-1 (stands in for Eigen::LDLT, solver.cpp:190,393).
+//   k_tri_gemv two GEMVs per solve with the explicit inverse.   solver.cpp:417
+//   k_xreduce / k_rhs / k_gauge_from_sum  rank exchange of point-sharded runs (pba_gpu_set_exchange).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

@@ -1696,6 +1696,7 @@ struct CiSmem {
   double a[NB][NB + 1];
   double b[NB][NB + 1];
   double d[NB][NB + 1];
+  double c[NB][NB + 1];  // DMMA product tile of ci_mm
 };
 
 // load a 32x32 block (rows r0.., cols c0..) of an n x n row-major matrix; out of range -> 0.
@@ -1710,14 +1711,33 @@ __device__ __forceinline__ void ci_load(double (*t)[NB + 1], const double* __res
   }
 }
 // acc[q] (element e = tid + 256 q, r = e / 32, c = e % 32) = sum_p x[r][p] * y[p][c]
-__device__ __forceinline__ void ci_mm(const double (*x)[NB + 1], const double (*y)[NB + 1], double (&acc)[4]) {
+// acc[q] (element e = tid + 256 q, r = e / 32, c = e % 32) = sum_p x[r][p] * y[p][c], on the FP64 tensor
+// path: 8 warps x two 8x8 tiles, 8 k-steps of mma.sync.m8n8k4.f64 each, through the shared tile ct.
+// Callers synchronise before (x, y written) and after (ct reused by the next product).
+__device__ __forceinline__ void ci_mm(const double (*x)[NB + 1], const double (*y)[NB + 1], double (*ct)[NB + 1],
+                                      double (&acc)[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = warp >> 1, tj0 = 2 * (warp & 1);
+  double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int p0 = 0; p0 < NB; p0 += 4) {
+    const double av = x[8 * ti + (lane >> 2)][p0 + (lane & 3)];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double bv = y[p0 + (lane & 3)][8 * (tj0 + u) + (lane >> 2)];
+      dmma_8x8x4(d[u][0], d[u][1], av, bv);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    ct[8 * ti + (lane >> 2)][8 * (tj0 + u) + 2 * (lane & 3)] = d[u][0];
+    ct[8 * ti + (lane >> 2)][8 * (tj0 + u) + 2 * (lane & 3) + 1] = d[u][1];
+  }
+  __syncthreads();
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
-    double v = 0.0;
-#pragma unroll 8
-    for (int p = 0; p < NB; ++p) v += x[r][p] * y[p][c];
-    acc[q] = v;
+    const int e = threadIdx.x + q * CI_THREADS;
+    acc[q] = ct[e / NB][e % NB];
   }
 }
 __device__ __forceinline__ void ci_store(double* __restrict__ M, int n, int r0, int c0, const double (&acc)[4],
@@ -1734,39 +1754,40 @@ __device__ __forceinline__ void ci_store(double* __restrict__ M, int n, int r0, 
 }
 
 // Factor the diagonal block k in shared memory: L_kk into A, Dinv_k = L_kk^-1 into Dinv.
+// One CTA barrier per column: every thread derives the pivot itself, the trailing update reads the
+// unscaled column j (l_rj l_cj = a_rj a_cj / d_j) and the scaled column goes to a second buffer, so
+// the update and the scaling of column j do not conflict.
 __device__ void ci_diag(CiSmem& sm, double* __restrict__ A, int n, int k, double* __restrict__ Dinv, int* fail) {
   const int k0 = k * NB, kb = min(NB, n - k0);
   double (*a)[NB + 1] = sm.a;
+  double (*l)[NB + 1] = sm.b;
   for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
     const int r = e / NB, c = e % NB;
     a[r][c] = (r < kb && c < kb && c <= r) ? __ldcg(A + static_cast<int64_t>(k0 + r) * n + k0 + c)
                                            : (r == c ? 1.0 : 0.0);
+    l[r][c] = 0.0;
   }
   __syncthreads();
   for (int j = 0; j < NB; ++j) {
-    if (threadIdx.x == 0) {
-      const double dj = a[j][j];
-      if (!(dj > 0.0) || !isfinite(dj)) {
-        *fail = 1;
-        a[j][j] = 1.0;
-      } else {
-        a[j][j] = sqrt(dj);
-      }
+    double dj = a[j][j];
+    if (!(dj > 0.0) || !isfinite(dj)) {
+      if (threadIdx.x == 0) *fail = 1;
+      dj = 1.0;
     }
-    __syncthreads();
-    const double piv = a[j][j];
-    for (int r = j + 1 + threadIdx.x; r < NB; r += CI_THREADS) a[r][j] = a[r][j] / piv;
-    __syncthreads();
+    const double piv = sqrt(dj), inv = 1.0 / piv, inv2 = inv * inv;
+    if (threadIdx.x < NB && threadIdx.x >= j) l[threadIdx.x][j] = threadIdx.x == j ? piv : a[threadIdx.x][j] * inv;
     for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
       const int r = e / NB, c = e % NB;
-      if (c > j && r >= c) a[r][c] -= a[r][j] * a[c][j];
+      if (c > j && r >= c) a[r][c] -= a[r][j] * a[c][j] * inv2;
     }
     __syncthreads();
   }
   for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) {
     const int r = e / NB, c = e % NB;
-    if (r < kb && c <= r) A[static_cast<int64_t>(k0 + r) * n + k0 + c] = a[r][c];
+    a[r][c] = l[r][c];
+    if (r < kb && c <= r) A[static_cast<int64_t>(k0 + r) * n + k0 + c] = l[r][c];
   }
+  __syncthreads();
   // Dinv_k: forward substitution, one column per thread
   if (threadIdx.x < NB) {
     const int c = threadIdx.x;
@@ -1815,7 +1836,7 @@ __global__ void __launch_bounds__(CI_THREADS) k_chol_inv(double* __restrict__ A,
         ci_load(sm.a, A, n, i0, k0, false);
         for (int e = threadIdx.x; e < NB * NB; e += CI_THREADS) sm.b[e % NB][e / NB] = sm.d[e / NB][e % NB];
         __syncthreads();
-        ci_mm(sm.a, sm.b, acc);
+        ci_mm(sm.a, sm.b, sm.c, acc);
         ci_store(A, n, i0, k0, acc, 1.0, nullptr);
       } else {
         const int j = it - npanel;  // 0..k
@@ -1829,7 +1850,7 @@ __global__ void __launch_bounds__(CI_THREADS) k_chol_inv(double* __restrict__ A,
         } else {  // X_kj = -Dinv_k R_kj
           ci_load(sm.b, X, n, k0, j * NB, false);
           __syncthreads();
-          ci_mm(sm.d, sm.b, acc);
+          ci_mm(sm.d, sm.b, sm.c, acc);
           ci_store(X, n, k0, j * NB, acc, -1.0, XT);
         }
       }
@@ -1854,7 +1875,7 @@ __global__ void __launch_bounds__(CI_THREADS) k_chol_inv(double* __restrict__ A,
         ci_load(sm.a, A, n, i0, k0, false);     // L_ik
         ci_load(sm.b, A, n, j0, k0, true);      // L_jk^T
         __syncthreads();
-        ci_mm(sm.a, sm.b, acc);
+        ci_mm(sm.a, sm.b, sm.c, acc);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int e = threadIdx.x + q * CI_THREADS, r = e / NB, c = e % NB;
@@ -1868,7 +1889,7 @@ __global__ void __launch_bounds__(CI_THREADS) k_chol_inv(double* __restrict__ A,
         ci_load(sm.a, A, n, i0, k0, false);     // L_ik
         ci_load(sm.b, X, n, k0, j0, false);     // X_kj
         __syncthreads();
-        ci_mm(sm.a, sm.b, acc);
+        ci_mm(sm.a, sm.b, sm.c, acc);
         const bool first = j == k;              // R_ij starts at step k = j
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -2211,7 +2232,9 @@ int chol_inv_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_inv, CI_THREADS, 0);
-    return std::max(1, sms * std::max(1, std::min(per, PBA_CI_PER_SM)));
+    int g0 = std::max(1, sms * std::max(1, std::min(per, PBA_CI_PER_SM)));
+    if (const char* e = std::getenv("PBA_CI_GRID")) g0 = std::max(1, std::min(g0, std::atoi(e)));  // experiments
+    return g0;
   }();
   return g;
 }

@@ -436,6 +436,7 @@ ObsArgs Engine::obs_args(double gamma) const {
   a.anchor_fm = anchor_fm_.p;
   a.tval = tval_.p;
   for (int k = 0; k < 8 && k < P_; ++k) a.pat_d[k] = make_double2(pat_.dx[k], pat_.dy[k]);
+  for (int k = 0; k < 8 && k < P_; ++k) a.pat_n[k] = make_double2(pat_.dx[k] * a.ref_ifx, pat_.dy[k] * a.ref_ify);
   a.tgrad = tgrad_.p;
   a.d0 = d0_.p;
   a.pose0 = pose0_.p;  // frozen IC poses (rows of the factored IC Jacobian)
@@ -682,15 +683,25 @@ void Engine::ic_rescale_rhs(int buf, double lambda) {
 }
 
 // User indices (ascending) of the points with D_n == 0.
-std::vector<int32_t> Engine::zero_depth_points(const double* D) {
-  std::vector<int32_t> out;
-  if (N_ == 0) return out;
-  const int64_t cnt = launch_zero_d(N_, D, perm_d_.p, zero_idx_.p, stream_);
-  out.resize(static_cast<size_t>(cnt));
-  if (cnt > 0)
-    ck(cudaMemcpy(out.data(), zero_idx_.p, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost), "zero-D list");
-  std::sort(out.begin(), out.end());
-  return out;
+// D_n == 0 points (solver.cpp:359-364): compacted on the device at the build (count only); the
+// user-order list is downloaded and sorted when a warning text is first requested.
+int64_t Engine::zero_depth_points(const double* D) {
+  if (N_ == 0) return 0;
+  return launch_zero_d(N_, D, perm_d_.p, zero_idx_.p, stream_);
+}
+
+const std::vector<int32_t>& Engine::zero_d_list() const {
+  if (!ic_.zero_d_ready) {
+    ic_.zero_d.resize(static_cast<size_t>(ic_.zero_d_count));
+    if (ic_.zero_d_count > 0) {
+      ck(cudaStreamSynchronize(stream_), "zero-D sync");
+      ck(cudaMemcpy(ic_.zero_d.data(), zero_idx_.p, ic_.zero_d_count * sizeof(int32_t), cudaMemcpyDeviceToHost),
+         "zero-D list");
+    }
+    std::sort(ic_.zero_d.begin(), ic_.zero_d.end());
+    ic_.zero_d_ready = true;
+  }
+  return ic_.zero_d;
 }
 
 // Dense Schur chunk scratch: allocated when a solver is built (not inside a timed factorization).
@@ -758,19 +769,20 @@ static const char kZeroD[] = ": zero depth Hessian entry (unobservable depth)";
 
 std::string Engine::warning(int64_t i) const {
   if (i < static_cast<int64_t>(ic_.warnings.size())) return ic_.warnings[i];
-  return "point " + std::to_string(ic_.zero_d[i - ic_.warnings.size()]) + kZeroD;
+  return "point " + std::to_string(zero_d_list()[i - ic_.warnings.size()]) + kZeroD;
 }
 
 const std::string& Engine::warnings_text() const {
   if (wtext_ok_) return wtext_;
   wtext_.clear();
-  wtext_.reserve(ic_.warnings.size() * 80 + ic_.zero_d.size() * (sizeof(kZeroD) + 16));
+  const std::vector<int32_t>& zd = zero_d_list();
+  wtext_.reserve(ic_.warnings.size() * 80 + zd.size() * (sizeof(kZeroD) + 16));
   for (const auto& w : ic_.warnings) {
     if (!wtext_.empty()) wtext_ += '\n';
     wtext_ += w;
   }
   char num[16];
-  for (const int32_t u : ic_.zero_d) {
+  for (const int32_t u : zd) {
     if (!wtext_.empty()) wtext_ += '\n';
     wtext_ += "point ";
     const auto r = std::to_chars(num, num + sizeof(num), u);
@@ -844,7 +856,7 @@ void Engine::ic_build(const pba_config* cfg) {
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
   ic_.mcur = 0;
-  ic_.zero_d = zero_depth_points(Dic_.p);  // :359-364, user point order (compacted on the device)
+  ic_.zero_d_count = zero_depth_points(Dic_.p);  // :359-364 (list fetched on request)
   wtext_ok_ = false;
   ic_.builds = 1;
   trace_mark(stream_, "ic_build: D, B copy, warnings");

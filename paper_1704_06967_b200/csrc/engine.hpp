@@ -76,7 +76,9 @@ struct SolverState {
   int factorizations = 0;
   int mcur = 0;  // index of the sticky residual mask in mask_[] (solver.hpp:162)
   std::vector<std::string> warnings;  // frame warnings (solver.cpp:265-271)
-  std::vector<int32_t> zero_d;        // user indices of the D_n == 0 points (:359-364), formatted on request
+  int64_t zero_d_count = 0;           // number of D_n == 0 points (:359-364)
+  mutable std::vector<int32_t> zero_d;  // their user indices, downloaded and sorted on first request
+  mutable bool zero_d_ready = false;
 };
 
 class Engine {
@@ -113,7 +115,7 @@ class Engine {
   void kernel_times(int64_t* counts, double* total_ms);
   // IcSolver::warnings() (solver.hpp:130): the frame warnings, then one per zero-D point; the
   // per-point strings (tens of thousands at C4) are formatted once, on request
-  int64_t warning_count() const { return static_cast<int64_t>(ic_.warnings.size() + ic_.zero_d.size()); }
+  int64_t warning_count() const { return static_cast<int64_t>(ic_.warnings.size()) + ic_.zero_d_count; }
   std::string warning(int64_t i) const;
   const std::string& warnings_text() const;
 
@@ -285,7 +287,8 @@ class Engine {
   void alloc_schur();
   void fuse_dense(ObsArgs& a);  // the pass also scatters B into the Schur chunk rows
   void build_frame_tabs(const PoseD* pose_d);
-  std::vector<int32_t> zero_depth_points(const double* D);
+  int64_t zero_depth_points(const double* D);
+  const std::vector<int32_t>& zero_d_list() const;
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
   void ic_factorize_loop(double lambda);
   void ic_refresh();

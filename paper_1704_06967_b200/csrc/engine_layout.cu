@@ -330,64 +330,8 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
   template_ok_ = fl[1] == 0;
 
   trace_mark(s, "layout: host results");
-  // ---- frame-major tiles (a tile never crosses a frame) ----
-  {
-    const int G = [this] {
-      int g = 1;
-      while (g < P_) g <<= 1;
-      return g;
-    }();
-    const int ops = 256 / G;
-    const int64_t steps = std::min<int64_t>(64, std::max<int64_t>(1, (NO_ + 148 * 8 * ops - 1) / (148 * 8 * ops)));
-    const int64_t T = ops * steps;
-    std::vector<int32_t> tile_frame, ftile_ptr(F_ + 1, 0);
-    std::vector<int64_t> tq0, tq1;
-    for (int f = 0; f < F_; ++f) {
-      for (int64_t q = fm_ptr[f]; q < fm_ptr[f + 1]; q += T) {
-        tile_frame.push_back(f);
-        tq0.push_back(q);
-        tq1.push_back(std::min(q + T, fm_ptr[f + 1]));
-      }
-      ftile_ptr[f + 1] = static_cast<int32_t>(tile_frame.size());
-    }
-    auto up = [&](auto& buf, const auto& vec) {
-      using T2 = std::remove_reference_t<decltype(*buf.p)>;
-      buf.alloc(std::max<size_t>(vec.size(), 1));
-      if (!vec.empty())
-        ck(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T2), cudaMemcpyHostToDevice, s), "upload");
-    };
-    up(tile_frame_, tile_frame);
-    up(tile_q0_, tq0);
-    up(tile_q1_, tq1);
-    up(ftile_ptr_, ftile_ptr);
-    ftile_ptr_h_ = ftile_ptr;
-    ov_.ntiles = static_cast<int>(tile_frame.size());
-    // Launch order of the lane passes: within each group of kTabFrames frames (one IC-pass launch),
-    // tiles sorted by their first point, then frame, so that the CTAs resident together work on
-    // the same points in neighbouring frames and share the points' template records in L2.
-    // Env PBA_TILE_ORDER=0 keeps the frame-major order.
-    tile_order_.release();
-    const char* env = std::getenv("PBA_TILE_ORDER");
-    if (!(env && env[0] == '0') && ov_.ntiles > 0) {
-      DBuf<int32_t> key;
-      key.alloc(ov_.ntiles);
-      launch_tile_first_point(ov_.ntiles, tile_q0_.p, fm_point_.p, key.p, s);
-      std::vector<int32_t> kh(ov_.ntiles);
-      ck(cudaMemcpyAsync(kh.data(), key.p, ov_.ntiles * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "tile keys");
-      ck(cudaStreamSynchronize(s), "tile keys sync");
-      std::vector<int32_t> order(ov_.ntiles);
-      for (int g0 = 0; g0 < F_; g0 += kTabFrames) {
-        const int t0 = ftile_ptr[g0], t1 = ftile_ptr[std::min(F_, g0 + kTabFrames)];
-        for (int t = t0; t < t1; ++t) order[t] = t;
-        std::stable_sort(order.begin() + t0, order.begin() + t1,
-                         [&](int32_t x, int32_t y) { return kh[x] < kh[y]; });  // ties: frame order
-      }
-      up(tile_order_, order);
-      ck(cudaStreamSynchronize(s), "tile order sync");
-    }
-  }
-
-  trace_mark(s, "layout: tiles");
+  // The Schur chunk plan goes first: its device sort, key download and host chunking overlap the
+  // target-image upload; the small host->device copies of both plans queue behind that upload.
   // ---- Schur chunk plan: points sorted by visibility window (first frame, last frame) and cut
   //      greedily into chunks whose union window keeps the padded width LD = roundup(6 W, 64) of
   //      the chunk's first window (so merging windows costs no extra DMMA columns), up to
@@ -465,6 +409,64 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
   }
 
   trace_mark(s, "layout: schur plan");
+  // ---- frame-major tiles (a tile never crosses a frame) ----
+  {
+    const int G = [this] {
+      int g = 1;
+      while (g < P_) g <<= 1;
+      return g;
+    }();
+    const int ops = 256 / G;
+    const int64_t steps = std::min<int64_t>(64, std::max<int64_t>(1, (NO_ + 148 * 8 * ops - 1) / (148 * 8 * ops)));
+    const int64_t T = ops * steps;
+    std::vector<int32_t> tile_frame, ftile_ptr(F_ + 1, 0);
+    std::vector<int64_t> tq0, tq1;
+    for (int f = 0; f < F_; ++f) {
+      for (int64_t q = fm_ptr[f]; q < fm_ptr[f + 1]; q += T) {
+        tile_frame.push_back(f);
+        tq0.push_back(q);
+        tq1.push_back(std::min(q + T, fm_ptr[f + 1]));
+      }
+      ftile_ptr[f + 1] = static_cast<int32_t>(tile_frame.size());
+    }
+    auto up = [&](auto& buf, const auto& vec) {
+      using T2 = std::remove_reference_t<decltype(*buf.p)>;
+      buf.alloc(std::max<size_t>(vec.size(), 1));
+      if (!vec.empty())
+        ck(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(T2), cudaMemcpyHostToDevice, s), "upload");
+    };
+    up(tile_frame_, tile_frame);
+    up(tile_q0_, tq0);
+    up(tile_q1_, tq1);
+    up(ftile_ptr_, ftile_ptr);
+    ftile_ptr_h_ = ftile_ptr;
+    ov_.ntiles = static_cast<int>(tile_frame.size());
+    // Launch order of the lane passes: within each group of kTabFrames frames (one IC-pass launch),
+    // tiles sorted by their first point, then frame, so that the CTAs resident together work on
+    // the same points in neighbouring frames and share the points' template records in L2.
+    // Env PBA_TILE_ORDER=0 keeps the frame-major order.
+    tile_order_.release();
+    const char* env = std::getenv("PBA_TILE_ORDER");
+    if (!(env && env[0] == '0') && ov_.ntiles > 0) {
+      DBuf<int32_t> key;
+      key.alloc(ov_.ntiles);
+      launch_tile_first_point(ov_.ntiles, tile_q0_.p, fm_point_.p, key.p, s);
+      std::vector<int32_t> kh(ov_.ntiles);
+      ck(cudaMemcpyAsync(kh.data(), key.p, ov_.ntiles * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "tile keys");
+      ck(cudaStreamSynchronize(s), "tile keys sync");
+      std::vector<int32_t> order(ov_.ntiles);
+      for (int g0 = 0; g0 < F_; g0 += kTabFrames) {
+        const int t0 = ftile_ptr[g0], t1 = ftile_ptr[std::min(F_, g0 + kTabFrames)];
+        for (int t = t0; t < t1; ++t) order[t] = t;
+        std::stable_sort(order.begin() + t0, order.begin() + t1,
+                         [&](int32_t x, int32_t y) { return kh[x] < kh[y]; });  // ties: frame order
+      }
+      up(tile_order_, order);
+      ck(cudaStreamSynchronize(s), "tile order sync");
+    }
+  }
+
+  trace_mark(s, "layout: tiles");
   ov_.N = N_;
   ov_.F = F_;
   ov_.P = P_;

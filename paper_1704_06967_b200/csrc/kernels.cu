@@ -271,6 +271,12 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #ifndef PBA_IC_STORED_PATH
 #define PBA_IC_STORED_PATH 1  // compile the stored-rows body too (PBA_IC_RECOMPUTE=0 at run time)
 #endif
+#ifndef PBA_IC_FACT
+#define PBA_IC_FACT 1  // IC pass: per-observation factored sums of the d0 m / m.t0 columns
+#endif
+#ifndef PBA_IC_OBSBASE
+#define PBA_IC_OBSBASE 1  // IC pass: per-observation anchor ray and warp base
+#endif
 #ifndef PBA_LANE_PREFETCH
 #define PBA_LANE_PREFETCH 1
 #endif
@@ -448,6 +454,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     const double4* tpl = a.tgrad + static_cast<int64_t>(n) * P;  // frozen {tval, gx, gy} of the point
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
+    double mw[3] = {0.0, 0.0, 0.0};  // PBA_IC_FACT: sum over the observation's pixels of wr m
+    (void)mw;
     uint32_t bits = 0u;
     bool obs_ok = true;
     if constexpr (MODE == OBS_BUILD) {
@@ -458,21 +466,54 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       const double vza = p0.R[6] * xa + p0.R[7] * ya + p0.R[8] + dv * p0.t[2];
       obs_ok = (dv > 0.0) && !(vza < kDegenerateDepthEps);
     }
+    // kOB (IC pass, compile-time pattern): the observation's anchor ray and the pixel-invariant
+    // part of the warp, R e_z + d t, are formed once per observation; a pixel then costs one add
+    // per ray coordinate and two FMAs per warp component (equal up to roundoff)
+    constexpr bool kOB = PBA_IC_OBSBASE && MODE == OBS_IC && PT > 0;
+    double xa = 0.0, ya = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+    if constexpr (kOB) {
+      const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
+      xa = (an.x - rf.cx) * a.ref_ifx;
+      ya = (an.y - rf.cy) * a.ref_ify;
+      bx = fma(dv, pe.t[0], pe.R[2]);
+      by = fma(dv, pe.t[1], pe.R[5]);
+      bz = fma(dv, pe.t[2], pe.R[8]);
+    }
 #pragma unroll (PT > 0 ? KP : 1)
     for (int kk = 0; kk < (PT > 0 ? KP : P); ++kk) {
       const int k = PT > 0 ? sub * KP + kk : kk;
       if (!((mbits >> k) & 1u)) continue;
       // template pixel (solver.cpp:42-49)
-      const double pu = an.x + (PT > 0 ? a.pat_d[k].x : static_cast<double>(a.pat.dx[k]));  // no I2F when unrolled
-      const double pv = an.y + (PT > 0 ? a.pat_d[k].y : static_cast<double>(a.pat.dy[k]));
-      const double x = (pu - rf.cx) * a.ref_ifx;
-      const double y = (pv - rf.cy) * a.ref_ify;
+      double x, y;
+      if constexpr (kOB) {
+        x = xa + a.pat_n[k].x;
+        y = ya + a.pat_n[k].y;
+      } else {
+        const double pu = an.x + (PT > 0 ? a.pat_d[k].x : static_cast<double>(a.pat.dx[k]));  // no I2F when unrolled
+        const double pv = an.y + (PT > 0 ? a.pat_d[k].y : static_cast<double>(a.pat.dy[k]));
+        x = (pu - rf.cx) * a.ref_ifx;
+        y = (pv - rf.cy) * a.ref_ify;
+      }
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
       double4 T = make_double4(0.0, NAN, NAN, 0.0);  // template record {tval, gx, gy} (non-FC modes)
       const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
       const FrameL fr = kTab ? tab_frame(tab.r[f - tab.f0]) : lds_frame(s_fr);
-      if (!warp_point(pe, x, y, dv, xn, yn, vx, vy, vz)) {
+      bool wok;
+      if constexpr (kOB) {
+        vx = fma(pe.R[0], x, fma(pe.R[1], y, bx));
+        vy = fma(pe.R[3], x, fma(pe.R[4], y, by));
+        vz = fma(pe.R[6], x, fma(pe.R[7], y, bz));
+        wok = !(fabs(vz) < kDegenerateDepthEps);
+        if (wok) {
+          const double iz = rcp_nr(vz);
+          xn = vx * iz;
+          yn = vy * iz;
+        }
+      } else {
+        wok = warp_point(pe, x, y, dv, xn, yn, vx, vy, vz);
+      }
+      if (!wok) {
         noob += 1.0;
       } else {
         const double u = fr.fx * xn + fr.cx;
@@ -497,10 +538,30 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
+#if PBA_IC_FACT
+            // factored: the d0 m and m.t0 columns are linear in m, so only sum wr m per
+            // observation (3 FMAs) and apply d0 and t0 once per observation below
+            double m0, m1, m2;
+            if (kRc) {
+              ic_m(p0, R0x, d0n, x, y, T.y, T.z, m0, m1, m2);
+            } else {
+              m0 = __ldg(jm + k * 32);
+              m1 = __ldg(jm + (P + k) * 32);
+              m2 = __ldg(jm + (2 * P + k) * 32);
+            }
+            gacc[0] += fma(R0x[1], m2, -(R0x[2] * m1)) * wr;
+            gacc[1] += fma(R0x[2], m0, -(R0x[0] * m2)) * wr;
+            gacc[2] += fma(R0x[0], m1, -(R0x[1] * m0)) * wr;
+            mw[0] = fma(m0, wr, mw[0]);
+            mw[1] = fma(m1, wr, mw[1]);
+            mw[2] = fma(m2, wr, mw[2]);
+            (void)row;
+#else
             ic_jrow<kRc>(p0, R0x, d0n, x, y, T.y, T.z, k, jm, P, row);
 #pragma unroll
             for (int c = 0; c < 6; ++c) gacc[c] += row[c] * wr;
             gnc += row[6] * wr;
+#endif
             bits |= 1u << k;
           } else if constexpr (MODE == OBS_REFRESH) {
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
@@ -589,6 +650,15 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         }
       }
     }
+#if PBA_IC_FACT
+    if constexpr (MODE == OBS_IC) {  // apply the per-observation factors: [.., d0 sum wr m, t0 . sum wr m]
+      const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+      gacc[3] = fma(d0n, mw[0], gacc[3]);
+      gacc[4] = fma(d0n, mw[1], gacc[4]);
+      gacc[5] = fma(d0n, mw[2], gacc[5]);
+      gnc = fma(mw[0], p0.t[0], fma(mw[1], p0.t[1], mw[2] * p0.t[2]));
+    }
+#endif
     if constexpr (LPO > 1) {  // per-observation sums over the LPO lanes of the observation
 #pragma unroll
       for (int o = 1; o < LPO; o <<= 1) {
@@ -940,12 +1010,15 @@ __global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_if
   tgrad[e] = g;
 }
 
-// Bpm[o] = B[pm2fm[o]] (point-major copy of the frozen IC pose-depth blocks)
+// Bpm[o] = B[pm2fm[o]] (point-major copy of the frozen IC pose-depth blocks): three threads per
+// observation, one 16-byte move each (a warp reads ~11 whole 48-byte blocks, stores coalesced)
 __global__ void k_b_to_pm(const ObsView ov, const double* __restrict__ B, double* __restrict__ Bpm) {
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ov.NO * 6;
+  const double2* __restrict__ src = reinterpret_cast<const double2*>(B);
+  double2* __restrict__ dst = reinterpret_cast<double2*>(Bpm);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ov.NO * 3;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t o = e / 6, c = e % 6;
-    Bpm[e] = B[static_cast<int64_t>(ov.pm2fm[o]) * 6 + c];
+    const int64_t o = e / 3, c = e - 3 * o;
+    __stcs(dst + e, __ldcs(src + 3 * static_cast<int64_t>(ov.pm2fm[o]) + c));
   }
 }
 
@@ -2046,7 +2119,7 @@ void launch_template_values(int N, const PatternD& pat, const FrameD& ref, const
 
 void launch_b_to_pm(const ObsView& ov, const double* B, double* Bpm, cudaStream_t s) {
   if (ov.NO == 0) return;
-  const int g = static_cast<int>(std::min<int64_t>((ov.NO * 6 + 255) / 256, 148 * 32));
+  const int g = static_cast<int>(std::min<int64_t>((ov.NO * 3 + 255) / 256, 148 * 32));
   k_b_to_pm<<<g, 256, 0, s>>>(ov, B, Bpm);
   count_launches(1);
 }

@@ -29,6 +29,7 @@ constexpr int PT_STRIDE = 32;
 struct ObsArgs {
   ObsView ov;
   double2 pat_d[8];            // pattern offsets as doubles (compile-time 8-pixel passes)
+  double2 pat_n[8];            // pattern offsets in normalised reference coordinates (dx / fx, dy / fy)
   FrameD ref;
   double ref_ifx, ref_ify;     // 1 / ref.fx, 1 / ref.fy (template normalization)
   const FrameD* frames;        // F

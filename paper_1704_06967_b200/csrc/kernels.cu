@@ -277,6 +277,9 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #ifndef PBA_IC_OBSBASE
 #define PBA_IC_OBSBASE 1  // IC pass: per-observation anchor ray and warp base
 #endif
+#ifndef PBA_IC_TPL_EARLY
+#define PBA_IC_TPL_EARLY 1  // IC pass: template record load issued before the warp
+#endif
 #ifndef PBA_LANE_PREFETCH
 #define PBA_LANE_PREFETCH 1
 #endif
@@ -499,6 +502,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       double4 T = make_double4(0.0, NAN, NAN, 0.0);  // template record {tval, gx, gy} (non-FC modes)
       const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
       const FrameL fr = kTab ? tab_frame(tab.r[f - tab.f0]) : lds_frame(s_fr);
+      constexpr bool kTplEarly = PBA_IC_TPL_EARLY && MODE == OBS_IC;
+      if constexpr (kTplEarly) T = ld_tpl(tpl + k);  // issued ahead of the warp: its latency overlaps it
       bool wok;
       if constexpr (kOB) {
         vx = fma(pe.R[0], x, fma(pe.R[1], y, bx));
@@ -525,7 +530,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           if constexpr (MODE == OBS_FC) {
             r = __ldg(tv + k) - bilinear_grad<true>(fr.img, fr.W, u, v, gdu, gdv);  // + image_gradient taps
           } else {
-            T = ld_tpl(tpl + k);
+            if constexpr (!kTplEarly) T = ld_tpl(tpl + k);
             r = T.x - bilinear(fr.img, fr.W, u, v);
           }
           act = true;

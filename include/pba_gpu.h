@@ -159,6 +159,11 @@ int pba_gpu_warning(const pba_handle* h, int i, char* buf, int len);
 /* All warnings at once, '\n'-separated and NUL-terminated (truncated to len - 1 bytes);
    returns the full length excluding the NUL.  Bulk form of warnings() for large problems. */
 int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len);
+/* The zero-depth-Hessian warnings (solver.cpp:359-364, "point <i>: zero depth Hessian entry
+   (unobservable depth)") are the last pba_gpu_warning_points() entries of warnings(), in
+   ascending user point order: copies up to cap point indices into idx and returns how many
+   there are.  Lets a binding format them on demand instead of parsing the bulk text. */
+int64_t pba_gpu_warning_points(const pba_handle* h, int32_t* idx, int64_t cap);
 int pba_gpu_ic_run(pba_handle* h, const pba_config* cfg, pba_report* rep); /* IcSolver::run / ic_solve solver.cpp:481-654,845-847 */
 
 /* ---- FcSolver (solver.hpp:172-182) ------------------------------------------- */

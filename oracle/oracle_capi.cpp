@@ -1,5 +1,6 @@
 // CPU ORACLE C API — TEST INFRASTRUCTURE ONLY (see pba_oracle.hpp).
 // Exposes the oracle through the same calls as include/pba_gpu.h.
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -294,6 +295,16 @@ int64_t pba_oracle_warnings_text(const pba_oracle_handle* h, char* buf, int64_t 
     buf[n] = '\0';
   }
   return static_cast<int64_t>(all.size());
+}
+// mirror of pba_gpu_warning_points: the trailing "point <n>: ..." warnings as indices
+int64_t pba_oracle_warning_points(const pba_oracle_handle* h, int32_t* idx, int64_t cap) {
+  if (!h->ic) return 0;
+  const auto& w = h->ic->warnings();
+  size_t i = w.size();
+  while (i > 0 && w[i - 1].rfind("point ", 0) == 0) --i;
+  const int64_t n = static_cast<int64_t>(w.size() - i);
+  for (int64_t j = 0; j < n && idx && j < cap; ++j) idx[j] = std::atoi(w[i + j].c_str() + 6);
+  return n;
 }
 int pba_oracle_warning(const pba_oracle_handle* h, int i, char* buf, int len) {
   if (!h->ic || i < 0 || i >= static_cast<int>(h->ic->warnings().size())) return PBA_E_ARG;

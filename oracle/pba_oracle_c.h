@@ -32,6 +32,7 @@ int pba_oracle_ic_hessian(pba_oracle_handle* h, double* pose_pose, double* depth
 int pba_oracle_warning_count(const pba_oracle_handle* h);
 int pba_oracle_warning(const pba_oracle_handle* h, int i, char* buf, int len);
 int64_t pba_oracle_warnings_text(const pba_oracle_handle* h, char* buf, int64_t len);
+int64_t pba_oracle_warning_points(const pba_oracle_handle* h, int32_t* idx, int64_t cap);
 int pba_oracle_ic_run(pba_oracle_handle* h, const pba_config* cfg, pba_report* rep);
 int pba_oracle_fc_build(pba_oracle_handle* h, double gamma, double* pose_pose, double* depth_depth,
                         double* pose_depth, double* g);

@@ -105,6 +105,7 @@ _COMMON = {
     "warning_count": (C.c_int, [VP]),
     "warning": (C.c_int, [VP, C.c_int, C.c_char_p, C.c_int]),
     "warnings_text": (C.c_int64, [VP, C.c_char_p, C.c_int64]),
+    "warning_points": (C.c_int64, [VP, P(i32), C.c_int64]),
     "ic_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),
     "fc_build": (C.c_int, [VP, f64, P(f64), P(f64), P(f64), P(f64)]),
     "fc_run": (C.c_int, [VP, P(pba_config), P(pba_report)]),

@@ -152,6 +152,14 @@ int64_t pba_gpu_warnings_text(const pba_handle* h, char* buf, int64_t len) {
   }
   return static_cast<int64_t>(all.size());
 }
+int64_t pba_gpu_warning_points(const pba_handle* h, int32_t* idx, int64_t cap) {
+  if (!h || !h->e) return 0;
+  try {
+    return h->e->warning_points(idx, cap);
+  } catch (...) {
+    return 0;
+  }
+}
 int pba_gpu_warning(const pba_handle* h, int i, char* buf, int len) {
   if (!h || !h->e || i < 0 || i >= h->e->warning_count() || !buf || len <= 0) return PBA_E_ARG;
   std::snprintf(buf, len, "%s", h->e->warning(i).c_str());

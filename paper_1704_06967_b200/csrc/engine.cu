@@ -693,15 +693,21 @@ int64_t Engine::zero_depth_points(const double* D) {
 const std::vector<int32_t>& Engine::zero_d_list() const {
   if (!ic_.zero_d_ready) {
     ic_.zero_d.resize(static_cast<size_t>(ic_.zero_d_count));
-    if (ic_.zero_d_count > 0) {
+    if (ic_.zero_d_count > 0) {  // compacted unordered by k_zero_d: sort the user indices on the device
+      sort_i32(zero_idx_.p, static_cast<int>(ic_.zero_d_count), stream_);
+      ck(cudaMemcpyAsync(ic_.zero_d.data(), zero_idx_.p, ic_.zero_d_count * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                         stream_), "zero-D list");
       ck(cudaStreamSynchronize(stream_), "zero-D sync");
-      ck(cudaMemcpy(ic_.zero_d.data(), zero_idx_.p, ic_.zero_d_count * sizeof(int32_t), cudaMemcpyDeviceToHost),
-         "zero-D list");
     }
-    std::sort(ic_.zero_d.begin(), ic_.zero_d.end());
     ic_.zero_d_ready = true;
   }
   return ic_.zero_d;
+}
+
+int64_t Engine::warning_points(int32_t* out, int64_t cap) const {
+  const std::vector<int32_t>& zd = zero_d_list();
+  if (out && cap > 0) std::memcpy(out, zd.data(), std::min<int64_t>(cap, static_cast<int64_t>(zd.size())) * sizeof(int32_t));
+  return static_cast<int64_t>(zd.size());
 }
 
 // Dense Schur chunk scratch: allocated when a solver is built (not inside a timed factorization).

@@ -68,6 +68,8 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+void sort_i32(int32_t* keys, int n, cudaStream_t s);  // engine_layout.cu
+
 struct SolverState {
   pba_config cfg{};
   bool built = false;
@@ -289,6 +291,9 @@ class Engine {
   void build_frame_tabs(const PoseD* pose_d);
   int64_t zero_depth_points(const double* D);
   const std::vector<int32_t>& zero_d_list() const;
+ public:
+  int64_t warning_points(int32_t* out, int64_t cap) const;
+ private:
   bool factor_reduced(const double* H, const double* B, const double* D, double lambda);
   void ic_factorize_loop(double lambda);
   void ic_refresh();

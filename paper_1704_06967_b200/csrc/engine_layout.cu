@@ -202,6 +202,20 @@ int bits_for(int64_t v) {
 
 template struct DBuf<unsigned char>;
 
+// ascending in-place sort of n int32 keys on the device (the zero-depth warning list)
+void sort_i32(int32_t* keys, int n, cudaStream_t s) {
+  if (n <= 1) return;
+  DBuf<int32_t> tmp_keys;
+  tmp_keys.alloc(n);
+  size_t tmp = 0;
+  ck(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, tmp_keys.p, n, 0, 32, s), "cub sort size");
+  DBuf<unsigned char> t;
+  t.alloc(std::max<size_t>(tmp, 1));
+  ck(cub::DeviceRadixSort::SortKeys(t.p, tmp, keys, tmp_keys.p, n, 0, 32, s), "cub sort keys");
+  ck(cudaMemcpyAsync(keys, tmp_keys.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s), "sorted keys");
+  ck(cudaStreamSynchronize(s), "sort sync");
+}
+
 void Engine::build_layout(const pba_problem* p, const std::function<void()>& after_obs_upload) {
   cudaStream_t s = stream_;
   // ---- caller CSR on the device (dense problems are generated in place) ----

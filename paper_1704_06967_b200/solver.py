@@ -13,6 +13,7 @@ for tests and baselines.
 """
 from __future__ import annotations
 
+import collections.abc as _abc
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -242,6 +243,45 @@ class BlockHessian:  # solver.hpp:59-69 (pose_depth in observation order)
 # handle
 # ---------------------------------------------------------------------------
 
+_ZERO_DEPTH = ": zero depth Hessian entry (unobservable depth)"  # solver.cpp:359-364
+
+
+class WarningList(_abc.Sequence):
+    """A read-only list of warning strings: `head` (frame warnings, text) followed by one
+    "point <i>: zero depth Hessian entry (unobservable depth)" per index of `points`,
+    formatted on access.  Compares equal to any sequence with the same strings."""
+
+    def __init__(self, head: List[str], points: np.ndarray):
+        self._head = list(head)
+        self.points = points
+
+    def __len__(self) -> int:
+        return len(self._head) + len(self.points)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError(i)
+        if i < len(self._head):
+            return self._head[i]
+        return f"point {int(self.points[i - len(self._head)])}{_ZERO_DEPTH}"
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, WarningList):
+            return self._head == other._head and np.array_equal(self.points, other.points)
+        try:
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"WarningList({len(self._head)} frame warnings, {len(self.points)} zero-depth points)"
+
+
 class Handle:
     """One uploaded problem on a backend ("gpu" = product, "oracle" = CPU checker)."""
 
@@ -333,13 +373,23 @@ class Handle:
                                       C.byref(lam)))
         return BlockHessian(pp, dd, pd, lam.value)
 
-    def warnings(self) -> List[str]:
-        if self.b.warning_count(self.h) == 0:
-            return []
-        n = int(self.b.warnings_text(self.h, None, 0))
-        buf = C.create_string_buffer(n + 1)
-        self.b.warnings_text(self.h, buf, n + 1)
-        return buf.value.decode().split("\n")
+    def warnings(self) -> "WarningList":
+        """IcSolver::warnings() (solver.hpp:130).  The per-point zero-depth warnings
+        (solver.cpp:359-364; 3e4 of them at C4) come back as an index array and are formatted
+        on access; the few frame warnings are fetched as text."""
+        total = int(self.b.warning_count(self.h))
+        if total == 0:
+            return WarningList([], np.zeros(0, dtype=np.int32))
+        npts = int(self.b.warning_points(self.h, None, 0))
+        idx = np.zeros(npts, dtype=np.int32)
+        if npts:
+            self.b.warning_points(self.h, _ptr(idx, C.c_int32), npts)
+        head = []
+        buf = C.create_string_buffer(4096)
+        for i in range(total - npts):
+            self._check(self.b.warning(self.h, i, buf, len(buf)))
+            head.append(buf.value.decode())
+        return WarningList(head, idx)
 
     def _report(self, fn, cfg: SolverConfig, capacity: Optional[int] = None) -> SolveReport:
         cap = int(capacity if capacity is not None else max(cfg.max_iters, 1))

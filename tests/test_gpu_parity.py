@@ -170,6 +170,13 @@ def test_zero_translation_warning_and_zero_depth_hessian():  # test_solver.cpp:2
     w = g.warnings()
     assert w and "zero initial translation" in w[0]
     assert np.all(g.ic_hessian().depth_depth == 0.0)
+    o = Handle(st, "oracle")
+    o.ic_build(SolverConfig())
+    assert w == o.warnings() and len(w) == 4  # the frame warning + 3 zero-depth points, same order
+    n = int(g.b.warnings_text(g.h, None, 0))  # the bulk text form agrees with the formatted list
+    buf = __import__("ctypes").create_string_buffer(n + 1)
+    g.b.warnings_text(g.h, buf, n + 1)
+    assert list(w) == buf.value.decode().split("\n")
 
 
 # ----------------------------------------------------------------------------- full runs

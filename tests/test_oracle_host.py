@@ -79,3 +79,29 @@ def test_oracle_errors_map_to_reference_exceptions():
     h = Handle(oracle_scene(frames=2, points=3), "oracle")
     with pytest.raises(solver.StateError):
         h.ic_gradient()
+
+
+def _bulk_text(h):
+    import ctypes as C
+    n = int(h.b.warnings_text(h.h, None, 0))
+    buf = C.create_string_buffer(n + 1)
+    h.b.warnings_text(h.h, buf, n + 1)
+    return buf.value.decode().split("\n") if n else []
+
+
+def test_warning_list_matches_the_bulk_text():  # test_solver.cpp:266-278 scene, solver.cpp:265-271, 359-364
+    st = oracle_scene(frames=2, points=3, sigma=2e-3)
+    st.targets = st.ref[None].copy()
+    st.targets_K = st.targets_K[:1]
+    st.R = np.eye(3)[None].copy()
+    st.t = np.zeros((1, 3))
+    o = Handle(st, "oracle")
+    o.ic_build(SolverConfig())
+    w = o.warnings()
+    text = _bulk_text(o)
+    assert len(w) == len(text) == 1 + 3  # the frame warning, then one per zero-depth point
+    assert list(w) == text and w == text and w[-1] == text[-1] and w[1:] == text[1:]
+    assert "zero initial translation" in w[0]
+    assert list(w.points) == [0, 1, 2] and w[1] == "point 0: zero depth Hessian entry (unobservable depth)"
+    with pytest.raises(IndexError):
+        w[len(w)]

@@ -68,6 +68,9 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   }
   void* p = nullptr;
   ck(cudaMallocAsync(&p, rb, s), "cudaMallocAsync");
+  if (rb >= (size_t(64) << 20) && std::getenv("PBA_TRACE"))
+    std::fprintf(stderr, "[pba trace] cache miss %.1f MB (cached %.1f GB, %zu blocks)\n", rb / 1048576.0,
+                 c.cached / 1073741824.0, c.free.size());
   return p;
 }
 
@@ -82,6 +85,8 @@ void dev_free(void* p, size_t bytes, cudaStream_t s) {
   }
   std::lock_guard<std::mutex> lk(c.m);
   if (c.cached + rb > BlockCache::kCap) {
+    if (std::getenv("PBA_TRACE"))
+      std::fprintf(stderr, "[pba trace] cache full: %.1f MB to the pool\n", rb / 1048576.0);
     cudaEventDestroy(ev);
     cudaFreeAsync(p, s);
     return;
@@ -810,6 +815,7 @@ void Engine::ic_build(const pba_config* cfg) {
   }
   ic_.lambda = ic_.cfg.lambda0;
   check_template();
+  trace_mark(stream_, "ic_build:   template check");
   if (F_ > 0) ck(cudaMemcpyAsync(pose0_.p, pose_state_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p0");
   pose0_h_.clear();  // host copy of the frozen poses is refreshed by build_frame_tabs
   if (N_ > 0) ck(cudaMemcpyAsync(d0_.p, d_state_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d0");
@@ -824,16 +830,20 @@ void Engine::ic_build(const pba_config* cfg) {
      // per-pixel store; the pass is not HBM-bound, so this costs no time and saves 24 B/px of HBM),
      // or, PBA_IC_RECOMPUTE=0, stored factored as m (24 B per pixel) when that fits comfortably.
     const size_t jm_bytes = static_cast<size_t>(std::max<int64_t>(jm_doubles(NO_, P_), 1)) * sizeof(double);
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
+    // cudaMemGetInfo only when the stored variant is asked for: it intermittently costs 20-40 ms
+    // with a large stream-ordered pool resident (measured inside ic_solve at C4)
     const char* env = std::getenv("PBA_IC_RECOMPUTE");
+    size_t free_b = 0, total_b = 0;
+    if (env && env[0] == '0') cudaMemGetInfo(&free_b, &total_b);
     const bool store = env && env[0] == '0' && jm_bytes <= free_b / 3;
     if (store) J_.alloc(jm_bytes / sizeof(double));
     else J_.release();
   }
+  trace_mark(stream_, "ic_build:   meminfo");
   Bic_.alloc(6 * nO);
   Dic_.alloc(std::max(N_, 1));
   Hic_.alloc(21 * std::max(F_, 1));
+  trace_mark(stream_, "ic_build:   B/D/H alloc");
 
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose0_.p;

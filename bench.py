@@ -588,7 +588,8 @@ def main():
                      "ncu": ncu_profile_extra(),
                      "note": "achieved = SURVEY 8d per-unit bytes of the IC pass (56 B/px J rows, K1 terms of B_IC) "
                              "/ launch time: an effective bandwidth, since the pass stores no rows and rebuilds them "
-                             "from 32-byte per-(point, pixel) template records; min_dram_bytes_per_pass = what it "
+                             "from 32-byte per-(point, pixel) template records (so frac can exceed 1: the pass is faster "
+                             "than any pass that reads the stored 56 B/px rows could be); min_dram_bytes_per_pass = what it "
                              "must move; traffic = ncu DRAM bytes of one pass; the binding resource is L1/L2-hit "
                              "latency and issue (ncu); canonical_* = full B_IC over the whole iteration"},
         "kernel_ms_per_iter": {n: round(v[1] / args.steps, 4) for n, v in kt.items() if v[0]},

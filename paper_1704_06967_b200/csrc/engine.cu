@@ -667,8 +667,19 @@ void Engine::build_frame_tabs(const PoseD* pose_d) {
       FrameRec& r = T.r[j];
       r.pe = pe_h_[f];
       r.p0 = pose0_h_[f];
-      r.fx = frames_h_[f].fx;
-      r.fy = frames_h_[f].fy;
+#if PBA_TAB_SCALED
+      for (int c = 0; c < 3; ++c) {
+        r.pe.R[c] *= frames_h_[f].fx;
+        r.pe.R[3 + c] *= frames_h_[f].fy;
+      }
+      r.pe.t[0] *= frames_h_[f].fx;
+      r.pe.t[1] *= frames_h_[f].fy;
+      r.fsx = static_cast<double>(frames_h_[f].W - 3);
+      r.fsy = static_cast<double>(frames_h_[f].H - 3);
+#else
+      r.fsx = frames_h_[f].fx;
+      r.fsy = frames_h_[f].fy;
+#endif
       r.cx = frames_h_[f].cx;
       r.cy = frames_h_[f].cy;
       r.img = frames_h_[f].img;

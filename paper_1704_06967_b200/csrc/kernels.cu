@@ -312,7 +312,7 @@ struct FrameL {  // register copy of the FrameD fields a pixel needs
   int W, H;
   double fx, fy, cx, cy;
 };
-__device__ __forceinline__ FrameL tab_frame(const FrameRec& r) { return FrameL{r.img, r.W, r.H, r.fx, r.fy, r.cx, r.cy}; }
+__device__ __forceinline__ FrameL tab_frame(const FrameRec& r) { return FrameL{r.img, r.W, r.H, r.fsx, r.fsy, r.cx, r.cy}; }
 __device__ __forceinline__ FrameL lds_frame(const FrameD& s) {
   static_assert(sizeof(FrameD) == 48, "FrameD layout");
   const char* b = reinterpret_cast<const char*>(&s);
@@ -521,9 +521,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       if (!wok) {
         noob += 1.0;
       } else {
-        const double u = fr.fx * xn + fr.cx;
-        const double v = fr.fy * yn + fr.cy;
-        if (!in_margin(u, v, fr.W, fr.H)) {
+        // scaled table (IC pass): pe rows 0/1 carry fx/fy, and fr.fx/fr.fy hold W - 3 / H - 3
+        constexpr bool kSc = kTab && PBA_TAB_SCALED;
+        const double u = kSc ? xn + fr.cx : fr.fx * xn + fr.cx;
+        const double v = kSc ? yn + fr.cy : fr.fy * yn + fr.cy;
+        const bool inm = kSc ? (u >= 1.0 && u <= fr.fx && v >= 1.0 && v <= fr.fy) : in_margin(u, v, fr.W, fr.H);
+        if (!inm) {
           noob += 1.0;
         } else {
           double gdu = 0.0, gdv = 0.0;

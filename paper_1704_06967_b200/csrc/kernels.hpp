@@ -61,10 +61,16 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
 
 // Frame table of the IC pass for frames [f0, f0 + nf) (tiles [tile0, tile0 + ntiles)), passed
 // as a kernel parameter: the frame-uniform records are then read through the constant cache.
+#ifndef PBA_TAB_SCALED
+#define PBA_TAB_SCALED 1
+#endif
+// IC-pass frame record.  With PBA_TAB_SCALED the candidate pose's first two rows (R and t) are
+// pre-multiplied by fx and fy, so the warped pixel is u = (fx v_x) / v_z + cx, and (fsx, fsy) hold
+// the in-margin bounds (W - 3, H - 3) as doubles; otherwise pe is the plain pose and (fsx, fsy) = (fx, fy).
 struct FrameRec {
   PoseD pe;                 // evaluation (candidate) pose
   PoseD p0;                 // frozen IC pose
-  double fx, fy, cx, cy;
+  double fsx, fsy, cx, cy;
   const float* img;
   int W, H;
 };

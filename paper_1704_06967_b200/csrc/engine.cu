@@ -209,6 +209,10 @@ Engine::Engine(const pba_problem* p) {
   scratch_bits_.alloc(nO + 8);
   rec_.alloc(nO);
   rec_g_.alloc(nO);
+  gfix_.alloc(nN);
+  gscale_.alloc(nN);
+  ck(cudaMemsetAsync(gfix_.p, 0, nN * sizeof(unsigned long long), stream_), "gfix zero");
+  if (const char* e = std::getenv("PBA_IC_GFIX")) use_gfix_ = e[0] != '0';
   s_n_.alloc(nN);
   dx_n_.alloc(nN);
   xp_.alloc(6 * nF);
@@ -274,7 +278,7 @@ int64_t Engine::device_bytes() const {  // every device buffer the handle holds
   add(images_, frames_, anchor_, anchor_fm_, tval_, tgrad_, pm_ptr_, fm_ptr_, tile_q0_, tile_q1_, pm_frame_, pm2fm_,
       fm_point_, tile_frame_, ftile_ptr_, tile_order_, uo2q_d_, perm_d_, zero_idx_, perm_tmp_, pose_state_,
       pose_cur_, pose_cand_, pose0_, d_state_, d_cur_, d_cand_, d0_, scratch_bits_, J_, Bic_, Dic_, Hic_, Bpm_,
-      rec_, rec_g_, s_n_, dx_n_, xp_, g_tmp_, r_out_, partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_,
+      rec_, rec_g_, gfix_, gscale_, s_n_, dx_n_, xp_, g_tmp_, r_out_, partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_,
       fscal_, ticket_, S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_, schur_acc_, chunk_pts_,
       schur_chunk_of_, schur_blocks_, schur_chunks_, schur_chunk_off_, schur_dense_, schur_wsort_, dense_row_,
       status_, flags_, xsend_, xrecv_, cf_, gauge_sum_);
@@ -615,6 +619,10 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   a.active_out = active_out;
   a.Jm = J_.p;
   a.rec_g = rec_g_.p;
+  if (use_gfix_) {
+    a.gfix = gfix_.p;
+    a.gscale = gscale_.p;
+  }
   // Large problems read the frame-uniform records from kernel-parameter frame tables (one host
   // read-back of the evaluation poses per pass); small, launch-bound ones keep the shared-memory
   // path and avoid the mid-iteration synchronisation.
@@ -634,6 +642,10 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   ev_end(PBA_K_OBS_PASS, e);
   PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[buf].p, Dic_.p, lambda, s_n_.p, partial_pt_.p};
   pa.rec_g = rec_g_.p;
+  if (use_gfix_) {
+    pa.gfix = gfix_.p;
+    pa.gscale = gscale_.p;
+  }
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
   const MaxUpdArgs mu = maxupd_args(pose_old, pose, d_old, d);
@@ -870,6 +882,8 @@ void Engine::ic_build(const pba_config* cfg) {
   ev_end(PBA_K_IC_BUILD, e);
   trace_mark(stream_, "ic_build: build pass");
   PointArgs pa{ov_, PT_DONLY, rec_.p, nullptr, Dic_.p, 0.0, nullptr, partial_pt_.p};
+  pa.gscale = gscale_.p;  // fixed-point scales of the IC g_n sums
+  pa.gbound = ic_.cfg.gamma;
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
   ev_end(PBA_K_REDUCE, e);

@@ -177,6 +177,9 @@ class Engine {
   DBuf<double> gn_[2], gf_[2], rhs_[2];
   DBuf<double2> rec_;
   DBuf<double> rec_g_;            // IC pass g_n terms (8 B per observation)
+  DBuf<unsigned long long> gfix_;  // IC pass fixed-point g_n sums (N, zero between passes)
+  DBuf<double> gscale_;            // per-point fixed-point scale S_n (set by the IC build)
+  bool use_gfix_ = true;           // env PBA_IC_GFIX=0: per-observation records + point-major gather instead
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;

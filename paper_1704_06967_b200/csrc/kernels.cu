@@ -648,6 +648,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
               b6[i2] += wi * row[6];
             }
             dc += w * row[6] * row[6];
+            gnc += fabs(row[6]);  // bound of the IC g_n terms: |w r| <= gamma (k_point PT_DONLY)
           }
         }
         if (a.Jmw) {  // store m unless the consumers rebuild it
@@ -681,7 +682,9 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     }
     if (live && sub == 0) {
       a.active_out[q] = bits;
-      if (MODE == OBS_IC && a.rec_g) a.rec_g[q] = gnc;  // IC needs the g_n term only (D is frozen)
+      if (MODE == OBS_IC && a.gfix) {  // exact, order-free fixed-point sum per point (L2-resident RED)
+        atomicAdd(a.gfix + n, static_cast<unsigned long long>(llrint(gnc * __ldg(a.gscale + n))));
+      } else if (MODE == OBS_IC && a.rec_g) a.rec_g[q] = gnc;  // IC needs the g_n term only (D is frozen)
       else a.rec[q] = make_double2(gnc, dc);
       if constexpr (kH) {
 #pragma unroll
@@ -1036,6 +1039,19 @@ __global__ void k_b_to_pm(const ObsView ov, const double* __restrict__ B, double
 __global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double g2 = 0.0;
+  if (a.mode == PT_GRAD && a.gfix) {  // g_n from the IC pass's fixed-point sums (cleared for the next pass)
+    for (int n = blockIdx.x * NT + threadIdx.x; n < a.ov.N; n += gridDim.x * NT) {
+      const long long v = static_cast<long long>(a.gfix[n]);
+      a.gfix[n] = 0ull;
+      const double g = static_cast<double>(v) * (1.0 / a.gscale[n]);  // S_n is a power of two: exact inverse
+      a.g_n[n] = g;
+      if (a.s_n) a.s_n[n] = g / (a.D[n] + a.lambda);
+      g2 += g * g;
+    }
+    double v2[2] = {g2, 0.0};
+    block_partial<2, false>(v2, a.partial);
+    return;
+  }
   const int ntask = (a.ov.N + kPPW - 1) / kPPW;
   for (int task = blockIdx.x * (NT / 32) + warp; task < ntask; task += gridDim.x * (NT / 32)) {
     const WarpTask t = warp_task(a.ov, task, lane);
@@ -1081,7 +1097,15 @@ __global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
       switch (a.mode) {
         case PT_GRAD: a.g_n[n] = g; break;
         case PT_FCH: a.g_n[n] = g; a.D[n] = ds; D = ds; break;
-        case PT_DONLY: a.D[n] = ds; D = ds; g = 0.0; break;
+        case PT_DONLY:
+          a.D[n] = ds;
+          D = ds;
+          if (a.gscale) {  // S_n = 2^(61 - e) with gamma sum |Jd| < 2^e: the IC pass's sums stay below 2^62
+            const double bound = a.gbound * g;
+            a.gscale[n] = (bound > 0.0 && isfinite(bound)) ? ldexp(1.0, 61 - (ilogb(bound) + 1)) : 1.0;
+          }
+          g = 0.0;
+          break;
         default: break;  // PT_RESCALE
       }
       if (a.s_n && a.mode != PT_DONLY) a.s_n[n] = g / (D + a.lambda);

@@ -54,6 +54,8 @@ struct ObsArgs {
   const int64_t* dense_row;    // N: offset of point n's chunk row minus 6 fmin (slot of frame f at + 6 f)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
   double* rec_g;               // NO or null: IC pass g_n terms only (sum_k Jd w r)
+  unsigned long long* gfix;    // N or null: IC pass g_n accumulated as 64-bit fixed point (RED), scaled by gscale
+  const double* gscale;        // N: per-point power-of-two scale S_n (gamma sum |Jd| S_n < 2^61, set at the build)
   double* partial;             // ntiles * PT_STRIDE
 };
 
@@ -134,6 +136,9 @@ struct PointArgs {
   double* s_n;            // N out: g_n / (D_n + lambda)
   double* partial;        // nblocks * 2 {sum g_n^2, 0}
   const double* rec_g = nullptr;  // NO or null: PT_GRAD reads these 8-byte g_n terms instead of rec
+  unsigned long long* gfix = nullptr;  // N or null: PT_GRAD converts (and clears) the fixed-point g_n sums
+  double* gscale = nullptr;            // N: PT_GRAD reads S_n; PT_DONLY writes it (bound: gbound * sum rec.x)
+  double gbound = 0.0;                 // PT_DONLY: Huber threshold gamma (|w r| <= gamma in the IC pass)
 };
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);

@@ -231,7 +231,8 @@ def cpu_baseline(st, cfg, npts, seed=0, iters=3):
     sub = scenes.subsample_points(st, npts, seed=seed)
     c = solver.SolverConfig(**{**cfg.__dict__, "max_iters": iters, "threshold_px": 0.0})
     t0 = time.perf_counter()
-    rep = solver.ic_solve(sub, c, backend="oracle")
+    from tests._oracle import ORACLE  # the CPU checker: only the cpu_baseline / reference legs
+    rep = solver.ic_solve(sub, c, backend=ORACLE)
     wall = time.perf_counter() - t0
     px, ms, prev = 0, 0.0, 0.0
     first_wall = rep.iters[0].wall_ms if rep.iters else 0.0
@@ -281,7 +282,8 @@ def cpu_baseline_threads(st, cfg, npts_per_thread, threads, seed=0, iters=3):
     c = solver.SolverConfig(**{**cfg.__dict__, "max_iters": iters, "threshold_px": 0.0})
 
     def one(sub):
-        rep = solver.ic_solve(sub, c, backend="oracle")
+        from tests._oracle import ORACLE
+        rep = solver.ic_solve(sub, c, backend=ORACLE)
         its = rep.iters
         px = sum(it.num_active for it in its[1:])
         ms = (its[-1].wall_ms - its[0].wall_ms) if len(its) > 1 else (its[0].wall_ms if its else 0.0)

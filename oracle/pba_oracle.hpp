@@ -358,7 +358,7 @@ class IcSolver {  // solver.hpp:115-169
   const std::vector<std::string>& warnings() const { return warnings_; }
   // exposed (private in the reference) for the C API mirror
   void factorize(double lambda);
-  std::vector<double> solve_step(const std::vector<double>& g);
+  std::vector<double> solve_step(const std::vector<double>& g, int depth = 0);
   double lambda() const { return lambda_; }
   const std::vector<Pose>& pose0() const { return pose0_; }
   const std::vector<double>& d0() const { return d0_; }

@@ -1,10 +1,10 @@
-"""ctypes declarations of include/pba_gpu.h and a loader for the in-tree libraries.
+"""ctypes declarations of include/pba_gpu.h and the loader of the product library.
 
-Both the product library (``lib/libpba_gpu.so``) and the CPU oracle
-(``oracle/_build/liboracle.so``, TEST INFRASTRUCTURE ONLY) export the same call
-set (prefixes ``pba_gpu_`` / ``pba_oracle_``), so ``Backend`` binds either one.
-The product path never falls back to the oracle: loading the GPU library fails
-loudly when it has not been built.
+``backend("gpu")`` binds ``lib/libpba_gpu.so`` (prefix ``pba_gpu_``); it fails loudly when the
+library has not been built — there is no CPU fallback and this package loads no other library.
+``_COMMON`` is the call set of the C ABI; the test suite binds its CPU checkers
+(tests/_oracle.py) with the same declarations and hands them to ``solver.Handle`` as library
+objects, so the parity tests drive every implementation through identical calls.
 """
 from __future__ import annotations
 
@@ -15,7 +15,6 @@ from pathlib import Path
 _PKG = Path(__file__).resolve().parent
 REPO = _PKG.parent
 GPU_LIB = Path(os.environ.get("PBA_GPU_LIB", str(_PKG / "lib" / "libpba_gpu.so")))  # override: experiments only
-ORACLE_LIB = REPO / "oracle" / "_build" / "liboracle.so"
 
 # status codes (pba_gpu.h)
 PBA_OK = 0
@@ -78,14 +77,6 @@ class pba_energy_result(C.Structure):
     _fields_ = [("energy", f64), ("num_active", i64), ("num_out_of_bounds", i64)]
 
 
-class pba_oracle_scene_spec(C.Structure):
-    _fields_ = [("width", i32), ("height", i32), ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64),
-                ("octaves", i32), ("base_wavelength_px", f64), ("lo", f64), ("hi", f64),
-                ("geometry_kind", i32), ("base_depth", f64), ("amplitude", f64), ("wavelength_px", f64),
-                ("trajectory_kind", i32), ("frames", i32), ("span_deg", f64), ("extent", f64 * 3),
-                ("num_points", i32), ("patch_radius", i32), ("seed", u64), ("supersample", i32)]
-
-
 VP = C.c_void_p
 _COMMON = {
     # name: (restype, argtypes)
@@ -114,7 +105,7 @@ _COMMON = {
     "apply_update": (C.c_int, [VP, C.c_int, P(f64), P(f64), P(f64), P(f64), P(C.c_int)]),
     "max_reproj_update": (C.c_int, [VP, P(f64), P(f64), P(f64), P(f64)]),
     "normalize_gauge": (C.c_int, [VP]),
-    # joint multi-host window (pba_gpu_mh_* / pba_oracle_mh_*)
+    # joint multi-host window (pba_gpu_mh_*)
     "mh_create": (C.c_int, [P(pba_mh_problem), P(VP)]),
     "mh_destroy": (None, [VP]),
     "mh_last_error": (C.c_char_p, [VP]),
@@ -132,54 +123,49 @@ _GPU_ONLY = {
     "device_bytes": (i64, [VP]),
     "launch_count": (i64, []),
 }
-_ORACLE_ONLY = {
-    "solve_normal_equations_dense": _COMMON["solve_normal_equations_schur"],
-    "scene_spec_default": (None, [P(pba_oracle_scene_spec)]),
-    "render_sequence": (C.c_int, [P(pba_oracle_scene_spec), P(f64), P(f64), P(f64), P(f64), P(f64), P(f64),
-                                  C.c_char_p, C.c_int]),
-    "perturb_parameters": (C.c_int, [i32, P(f64), P(f64), i32, P(f64), f64, u64]),
-}
 
 _cache: dict = {}
 
 
 class Backend:
-    """A loaded library with uniformly named functions (``self.create`` ...)."""
+    """The loaded product library with uniformly named functions (``self.create`` ...)."""
 
-    def __init__(self, kind: str):
-        self.kind = kind
-        if kind == "gpu":
-            path, prefix, extra = GPU_LIB, "pba_gpu_", _GPU_ONLY
-        elif kind == "oracle":
-            path, prefix, extra = ORACLE_LIB, "pba_oracle_", _ORACLE_ONLY
-        else:
-            raise ValueError(kind)
+    def __init__(self):
+        self.kind = "gpu"
+        path = GPU_LIB
         if not path.exists():
             raise RuntimeError(
                 f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
-                f"(the {kind} path has no fallback)")
+                f"(the product has no fallback)")
         self.lib = C.CDLL(str(path))
         self.path = path
-        for name, (res, args) in {**_COMMON, **extra}.items():
-            fn = getattr(self.lib, prefix + name)
+        for name, (res, args) in {**_COMMON, **_GPU_ONLY}.items():
+            fn = getattr(self.lib, "pba_gpu_" + name)
             fn.restype = res
             fn.argtypes = args
             setattr(self, name, fn)
-        if kind == "gpu":
-            self.status_string = self.lib.pba_status_string
-            self.status_string.restype = C.c_char_p
-            self.status_string.argtypes = [C.c_int]
-            # host-only utility of the CLI (synth.cpp:308-320); no device work
-            self.perturb_parameters = self.lib.pba_perturb_parameters
-            self.perturb_parameters.restype = C.c_int
-            self.perturb_parameters.argtypes = _ORACLE_ONLY["perturb_parameters"][1]
-        self.config_default = self.lib.pba_config_default if kind == "gpu" else None
+        self.status_string = self.lib.pba_status_string
+        self.status_string.restype = C.c_char_p
+        self.status_string.argtypes = [C.c_int]
+        # host-only utility of the CLI (synth.cpp:308-320); no device work
+        self.perturb_parameters = self.lib.pba_perturb_parameters
+        self.perturb_parameters.restype = C.c_int
+        self.perturb_parameters.argtypes = [i32, P(f64), P(f64), i32, P(f64), f64, u64]
+        self.config_default = self.lib.pba_config_default
 
 
-def backend(kind: str) -> Backend:
-    if kind not in _cache:
-        _cache[kind] = Backend(kind)
-    return _cache[kind]
+def backend(kind="gpu"):
+    """The product library for ``"gpu"``; a library object built elsewhere with the same call set
+    (the test suite's CPU checkers) is passed through unchanged."""
+    if isinstance(kind, str):
+        if kind != "gpu":
+            raise ValueError(f"unknown library {kind!r}: this package binds only libpba_gpu.so")
+        if "gpu" not in _cache:
+            _cache["gpu"] = Backend()
+        return _cache["gpu"]
+    if not hasattr(kind, "create"):
+        raise TypeError(f"{kind!r} is not a bound PBA library")
+    return kind
 
 
 def default_config() -> pba_config:
@@ -189,5 +175,4 @@ def default_config() -> pba_config:
 
 
 def lib_paths() -> dict:
-    return {"gpu": str(GPU_LIB), "oracle": str(ORACLE_LIB), "exists_gpu": GPU_LIB.exists(),
-            "exists_oracle": ORACLE_LIB.exists(), "pid": os.getpid()}
+    return {"gpu": str(GPU_LIB), "exists_gpu": GPU_LIB.exists(), "pid": os.getpid()}

@@ -13,6 +13,15 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+// IcSolver::solve_step refactors with lambda * 10 and recurses while the step is non-finite
+// (solver.cpp:429-432).  With lambda = 0 (lambda0 = 0 and an unobservable depth, D_n + lambda = 0)
+// the reference recurses until its stack overflows; here the retries are bounded like
+// IcSolver::factorize's own attempts (solver.cpp:372, 60) and end in SingularHessian.
+constexpr int kMaxNonfiniteRetries = 60;
+[[noreturn]] void throw_nonfinite_exhausted() {
+  throw PbaError(PBA_E_SINGULAR_HESSIAN, "SingularHessian: non-finite step after damping retries");
+}
+
 __global__ void k_depth_update(int N, int ic, const double* __restrict__ d, const double* __restrict__ d0,
                                const double* __restrict__ dx, double* __restrict__ out, int* __restrict__ nbad) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,7 +87,8 @@ void Engine::backsub(bool ic, const double* B, const double* D, const double* g_
 // ---- IcSolver::compute_step / solve_step mirrors (solver.cpp:404-434, 475-479) ----
 void Engine::ic_solve_loop_and_download(double* dx) {
   double rhs_lambda = ic_.lambda;
-  for (;;) {
+  for (int retry = 0;; ++retry) {
+    if (retry > kMaxNonfiniteRetries) throw_nonfinite_exhausted();
     if (rhs_lambda != ic_.lambda) {
       ic_rescale_rhs(0, ic_.lambda);
       rhs_lambda = ic_.lambda;
@@ -427,6 +437,7 @@ bool Engine::iterate_ic(pba_iter_stats* st) {
   }
   bool accepted = false;
   Status s{};
+  int nonfinite_retries = 0;
   while (!accepted) {  // :538-606
     if (R.rhs_lambda != ic_.lambda) {
       ic_rescale_rhs(b0, ic_.lambda);
@@ -441,6 +452,7 @@ bool Engine::iterate_ic(pba_iter_stats* st) {
             d_cur_.p);                                                      // :561 + next g
     s = read_status();
     if (flags_h_[1] || s.nonfinite > 0) {  // :429-432
+      if (++nonfinite_retries > kMaxNonfiniteRetries) throw_nonfinite_exhausted();
       ic_factorize_loop(ic_.lambda * 10.0);
       continue;
     }

@@ -100,9 +100,9 @@ class MultiHostEnergy:
 
 
 class MultiHostHandle:
-    """pba_gpu_mh_* (product) or pba_oracle_mh_* (checker) on one window."""
+    """pba_gpu_mh_* on one window (or the same calls on a checker library object, tests only)."""
 
-    def __init__(self, problem: MultiHostProblem, backend: str = "gpu"):
+    def __init__(self, problem: MultiHostProblem, backend="gpu"):
         self.b = capi.backend(backend)
         self.K, self.N = problem.num_frames, problem.num_points
         p, self._keep = problem._c()
@@ -164,7 +164,7 @@ class MultiHostHandle:
 
 
 def mh_fc_solve(problem: MultiHostProblem, config: Optional[SolverConfig] = None,
-                backend: str = "gpu") -> MultiHostReport:
+                backend="gpu") -> MultiHostReport:
     h = MultiHostHandle(problem, backend)
     try:
         return h.fc_run(config)

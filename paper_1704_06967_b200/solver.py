@@ -7,9 +7,10 @@ gradient / run / hessian / warnings), ``FcSolver.run``, ``ic_solve``,
 ``fc_solve`` and ``solve_normal_equations_schur``.  The reference's exception
 classes (errors.hpp:9-40) are re-raised from the status codes.
 
-``backend="gpu"`` (the default, the product) drives libpba_gpu.so on the B200;
-``backend="oracle"`` drives the CPU oracle with the very same calls and is only
-for tests and baselines.
+Every entry point drives libpba_gpu.so on the B200 (``backend="gpu"``, the default).  The test
+suite passes its CPU checkers (tests/_oracle.py: the restated oracle and the reference compiled
+in place) as ``backend=<library object>`` to run the very same calls against them; this package
+itself loads no library but libpba_gpu.so.
 """
 from __future__ import annotations
 
@@ -283,11 +284,11 @@ class WarningList(_abc.Sequence):
 
 
 class Handle:
-    """One uploaded problem on a backend ("gpu" = product, "oracle" = CPU checker)."""
+    """One uploaded problem: on the product library ("gpu") or on a checker library object."""
 
-    def __init__(self, state: ProblemState, backend: str = "gpu"):
+    def __init__(self, state: ProblemState, backend="gpu"):
         self.b = capi.backend(backend)
-        self.backend = backend
+        self.backend = self.b.kind
         self.F, self.N = state.num_frames, state.num_points
         self.P = int(np.asarray(state.pattern).reshape(-1, 2).shape[0])
         p, keep = state._c()
@@ -295,7 +296,7 @@ class Handle:
         rc = self.b.create(C.byref(p), C.byref(h))
         del keep
         if rc != capi.PBA_OK:
-            err = self.b.last_error(None) if backend == "gpu" else b""
+            err = self.b.last_error(None) if self.backend == "gpu" else b""
             _raise(rc, (err or b"").decode())
         self.h = h
         self.NO = int(self.b.num_observations(self.h))
@@ -499,7 +500,7 @@ class Handle:
 # reference-shaped entry points
 # ---------------------------------------------------------------------------
 
-def energy_eval(state: ProblemState, gamma: float = 0.03, mask=None, backend: str = "gpu") -> EnergyResult:
+def energy_eval(state: ProblemState, gamma: float = 0.03, mask=None, backend="gpu") -> EnergyResult:
     """energy_eval(state, HuberLoss{gamma}, mask) (solver.hpp:110-111)."""
     h = Handle(state, backend)
     try:
@@ -511,7 +512,7 @@ def energy_eval(state: ProblemState, gamma: float = 0.03, mask=None, backend: st
 class IcSolver:
     """IcSolver(ProblemState, SolverConfig) (solver.hpp:115-169)."""
 
-    def __init__(self, state: ProblemState, config: Optional[SolverConfig] = None, backend: str = "gpu"):
+    def __init__(self, state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu"):
         self.config = config or SolverConfig()
         self.h = Handle(state, backend)
         self._built = False
@@ -555,7 +556,7 @@ class IcSolver:
 class FcSolver:
     """FcSolver(ProblemState, SolverConfig) (solver.hpp:172-182)."""
 
-    def __init__(self, state: ProblemState, config: Optional[SolverConfig] = None, backend: str = "gpu"):
+    def __init__(self, state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu"):
         self.config = config or SolverConfig()
         self.h = Handle(state, backend)
 
@@ -563,7 +564,7 @@ class FcSolver:
         return self.h.fc_run(self.config)
 
 
-def ic_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend: str = "gpu") -> SolveReport:
+def ic_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu") -> SolveReport:
     """ic_solve (solver.cpp:845-847)."""
     h = Handle(state, backend)
     try:
@@ -572,7 +573,7 @@ def ic_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend
         h.close()
 
 
-def fc_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend: str = "gpu") -> SolveReport:
+def fc_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu") -> SolveReport:
     """fc_solve (solver.cpp:849-851)."""
     h = Handle(state, backend)
     try:
@@ -582,7 +583,7 @@ def fc_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend
 
 
 def solve_normal_equations_schur(H: BlockHessian, g, lam: float, obs_ptr=None, obs_frame=None,
-                                 backend: str = "gpu") -> np.ndarray:
+                                 backend="gpu") -> np.ndarray:
     """solve_normal_equations_schur (solver.hpp:190-192, solver.cpp:165-213)."""
     b = capi.backend(backend)
     F, N = H.pose_pose.shape[0], H.depth_depth.shape[0]
@@ -597,6 +598,6 @@ def solve_normal_equations_schur(H: BlockHessian, g, lam: float, obs_ptr=None, o
                                         _ptr(dd, C.c_double), _ptr(pd, C.c_double), _ptr(g, C.c_double), lam,
                                         _ptr(dx, C.c_double))
     if rc != capi.PBA_OK:
-        msg = b.last_error(None) if backend == "gpu" else b""
+        msg = b.last_error(None) if b.kind == "gpu" else b""
         _raise(rc, (msg or b"").decode())
     return dx

@@ -9,13 +9,14 @@ import numpy as np
 from paper_1704_06967_b200 import _capi as capi
 from paper_1704_06967_b200.scenes import square_pattern
 from paper_1704_06967_b200.solver import ProblemState
+from ._oracle import ORACLE, pba_oracle_scene_spec
 
 
 def oracle_scene(width=160, height=120, fx=130.0, frames=2, points=6, span_deg=6.0, patch_radius=1,
                  sigma=0.0, perturb_seed=7, dolly=None, plane=False, seed=7):
     """render_sequence(small_spec(...)) (test_solver.cpp:14-34) with fp32-rounded images."""
-    o = capi.backend("oracle")
-    spec = capi.pba_oracle_scene_spec()
+    o = ORACLE
+    spec = pba_oracle_scene_spec()
     o.scene_spec_default(C.byref(spec))
     spec.width, spec.height = width, height
     spec.fx = spec.fy = fx
@@ -87,3 +88,20 @@ def random_visibility(st: ProblemState, keep=0.6, seed=0):
     op[1:] = np.cumsum(vis.sum(1))
     of = np.nonzero(vis)[1].astype(np.int32)
     return op, of
+
+
+def assert_params_close(a, b, tol):
+    """Per-parameter comparison (north star: "final poses and depths within 1e-4"): every element i of
+    the block satisfies |a_i - b_i| <= tol * max(|b_i|, 1e-2 * max_j |b_j|).  The floor (1% of the
+    block's largest magnitude) keeps elements that are ~0 (rotation off-diagonals, translation
+    components near zero) from demanding an absolute accuracy finer than the block's own scale."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    assert a.shape == b.shape, (a.shape, b.shape)
+    if b.size == 0:
+        return
+    scale = np.maximum(np.abs(b), 1e-2 * np.abs(b).max())
+    err = np.abs(a - b)
+    bad = np.nonzero(err > tol * scale)[0]
+    assert bad.size == 0, (f"{bad.size} of {b.size} elements beyond {tol:g}: worst index {bad[np.argmax(err[bad] / scale[bad])]}"
+                           f" rel {float((err / np.where(scale > 0, scale, 1)).max()):.3e}")

@@ -18,7 +18,9 @@ def _built():
     """Build the oracle and the product library once if they are missing."""
     from paper_1704_06967_b200 import _capi
 
-    if not (_capi.GPU_LIB.exists() and _capi.ORACLE_LIB.exists()):
+    from ._oracle import ORACLE_LIB
+
+    if not (_capi.GPU_LIB.exists() and ORACLE_LIB.exists()):
         import __graft_entry__
 
         __graft_entry__.build()

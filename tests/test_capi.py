@@ -3,7 +3,11 @@ import ctypes
 import re
 from pathlib import Path
 
+import pytest
+
 from paper_1704_06967_b200 import _capi
+
+from ._oracle import ORACLE_LIB, REF
 
 HDR = Path(__file__).resolve().parent.parent / "include" / "pba_gpu.h"
 
@@ -31,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_oracle_mirrors_the_gpu_call_set():
-    lib = ctypes.CDLL(str(_capi.ORACLE_LIB))
+    lib = ctypes.CDLL(str(ORACLE_LIB))
     gpu_only = {"stream", "set_profiling", "kernel_times", "device_bytes", "ic_begin", "fc_begin", "iterate", "end",
                 "launch_count", "set_exchange"}
     for n in declared():
@@ -48,3 +52,26 @@ def test_status_strings_and_defaults():
     lib.pba_config_default(ctypes.byref(cfg))
     assert (cfg.gamma, cfg.threshold_px, cfg.max_iters, cfg.lambda0, cfg.max_bad_steps) == (0.03, 5e-3, 200, 1e-6, 8)
     assert cfg.normalize_depth_gauge == 1 and cfg.refresh_ic_hessian == 0
+
+
+def test_product_package_binds_only_the_gpu_library():
+    """No multi-backend dispatch: the product cannot load a checker library by name, and no product
+    source refers to the oracle's or the reference's shared objects."""
+    with pytest.raises(ValueError):
+        _capi.backend("oracle")
+    pkg = Path(_capi.__file__).resolve().parent
+    for src in list(pkg.glob("*.py")) + list((pkg / "csrc").glob("*")):
+        txt = src.read_text(errors="ignore")
+        assert "liboracle" not in txt and "libpba_ref" not in txt and "pba_oracle_" not in txt, src
+
+
+def test_reference_library_exports_the_checker_call_set():
+    """oracle/_ref/libpba_ref.so (the unmodified reference compiled against oracle/ref_shim) exports the
+    same calls as the oracle, for the dense problems the reference can express."""
+    if not REF.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    lib = ctypes.CDLL(str(REF.path if hasattr(REF, "path") else REF.get().path))
+    for n in ["create", "destroy", "energy", "ic_build", "ic_gradient", "ic_compute_step", "ic_solve_step",
+              "ic_factorize", "ic_hessian", "ic_run", "fc_run", "solve_normal_equations_schur",
+              "solve_normal_equations_dense", "apply_update", "render_sequence", "perturb_parameters"]:
+        assert hasattr(lib, "pba_ref_" + n), n

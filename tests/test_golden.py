@@ -1,16 +1,28 @@
-"""Committed golden fixtures (tests/golden/make_golden.py, from the pinned oracle):
-the oracle must reproduce them exactly (CPU), the GPU within the north-star tolerances."""
+"""Committed golden fixtures (tests/golden/make_golden.py).
+
+Every dense fixture was produced by the REFERENCE ITSELF (oracle/_ref/libpba_ref.so: the unmodified
+/root/reference/proj sources compiled in place); ``tiny_visibility`` (a visibility list, which the
+reference cannot express) by the restated oracle.
+
+* CPU: the restated oracle reproduces the reference fixtures — the energy pass, residuals, active
+  flags, the IC Hessian blocks and gradient bit-for-bit; the step and the trajectories to roundoff
+  (the reference factors with Eigen's pivoted LDLT, the oracle with Cholesky: SURVEY.md §8c); the same
+  iteration count, accept/reject (factorization-count) sequence, counters and messages.
+* GPU: libpba_gpu.so matches them within the north-star tolerances, per element.
+"""
 from pathlib import Path
 
 import numpy as np
 import pytest
 
-from paper_1704_06967_b200.solver import Handle, ProblemState, SolverConfig
+from paper_1704_06967_b200.solver import Error, Handle, ProblemState, SolverConfig
 
-from ._helpers import gauge_vector, project_out, rel
+from ._helpers import assert_params_close, gauge_vector, project_out, rel
+from ._oracle import ORACLE
 
 GOLD = Path(__file__).resolve().parent / "golden"
-NAMES = ["ref_small", "tiny_dso8", "tiny_visibility"]
+NAMES = ["ref_small", "ref_gn_step", "ref_large_noise", "ref_large_noise_diverge", "ref_flat_fc_fail", "tiny_dso8",
+         "tiny_visibility"]
 
 
 def load(name):
@@ -24,19 +36,58 @@ def load(name):
     return z, st, cfg
 
 
+def check_run(z, kind, rep, energy_rtol, param_tol, energy_floor):
+    """One IcSolver/FcSolver run against the fixture: identical control flow, close numbers.  Energies
+    are compared relatively, with an absolute floor of ``energy_floor`` times the initial energy (runs
+    that converge to ~1e-10 of their starting cost are at the roundoff floor of the residuals)."""
+    atol = energy_floor * abs(float(z["energy"]))
+    assert rep.iterations == int(z[f"{kind}_iters"])
+    assert [s.hessian_factorizations for s in rep.iters] == list(z[f"{kind}_factorizations"])
+    assert [s.hessian_builds for s in rep.iters] == list(z[f"{kind}_builds"])
+    assert [s.accepted for s in rep.iters] == list(z[f"{kind}_accepted"])
+    assert (rep.converged, rep.diverged, rep.rejected_steps) == (
+        bool(z[f"{kind}_converged"]), bool(z[f"{kind}_diverged"]), int(z[f"{kind}_rejected"]))
+    assert rep.hessian_factorizations == int(z[f"{kind}_total_factorizations"])
+    assert rep.message == str(z[f"{kind}_message"])
+    if rep.iters:
+        assert np.allclose([s.energy for s in rep.iters], z[f"{kind}_energies"], rtol=energy_rtol, atol=atol)
+    e_ref = float(z[f"{kind}_final_energy"])
+    assert abs(rep.final_energy - e_ref) <= energy_rtol * abs(e_ref) + atol
+    assert_params_close(rep.final_R, z[f"{kind}_final_R"], param_tol)
+    assert_params_close(rep.final_t, z[f"{kind}_final_t"], param_tol)
+    assert_params_close(rep.final_inv_depths, z[f"{kind}_final_d"], param_tol)
+
+
+def kinds(z):
+    return [k for k in ("ic", "fc") if f"{k}_iters" in z]
+
+
 @pytest.mark.parametrize("name", NAMES)
 def test_oracle_reproduces_golden(name):
     z, st, cfg = load(name)
-    h = Handle(st, "oracle")
+    exact = str(z["source"]) == "oracle"
+    h = Handle(st, ORACLE)
     e = h.energy(cfg.gamma)
+    # the residual pass is the same fp64 arithmetic in the same order: bitwise equal to the reference
     assert e.energy == float(z["energy"]) and e.num_active == int(z["num_active"])
-    assert np.array_equal(e.residuals, z["residuals"])
-    h.ic_build(cfg)
-    assert np.array_equal(h.ic_gradient(), z["ic_gradient"])
-    assert np.array_equal(h.ic_compute_step(), z["ic_step"])
-    ic = Handle(st, "oracle").ic_run(cfg)
-    assert ic.iterations == int(z["ic_iters"]) and ic.final_energy == float(z["ic_final_energy"])
-    assert np.array_equal(ic.final_inv_depths, z["ic_final_d"])
+    assert np.array_equal(e.residuals, z["residuals"]) and np.array_equal(e.active, z["active"])
+    if "H_pose_pose" in z:
+        h.ic_build(cfg)
+        H = h.ic_hessian()
+        assert np.array_equal(H.pose_pose, z["H_pose_pose"]) and np.array_equal(H.pose_depth, z["H_pose_depth"])
+        assert np.array_equal(H.depth_depth, z["H_depth_depth"])
+        assert np.array_equal(h.ic_gradient(), z["ic_gradient"])
+        assert list(h.warnings()) == [str(w) for w in z["warnings"]]
+        step = h.ic_compute_step()
+        if exact:
+            assert np.array_equal(step, z["ic_step"])
+        else:  # LDLT (pivoted) vs Cholesky: roundoff, largest along the scale gauge
+            v = gauge_vector(st.num_frames, st.num_points, st.t, st.inv_depths)
+            assert rel(project_out(step, v), project_out(z["ic_step"], v)) <= 1e-8
+    for kind in kinds(z):
+        rep = getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+        check_run(z, kind, rep, energy_rtol=0 if exact else 1e-7, param_tol=0 if exact else 1e-7,
+                  energy_floor=0 if exact else 1e-12)
 
 
 @pytest.mark.gpu
@@ -47,19 +98,20 @@ def test_gpu_matches_golden(name):
     e = h.energy(cfg.gamma)
     assert e.num_active == int(z["num_active"]) and e.num_out_of_bounds == int(z["num_oob"])
     assert np.array_equal(e.active, z["active"])
-    assert abs(e.energy - float(z["energy"])) <= 1e-5 * float(z["energy"])
+    assert abs(e.energy - float(z["energy"])) <= 1e-5 * abs(float(z["energy"]))
     assert rel(e.residuals, z["residuals"]) <= 1e-5
-    h.ic_build(cfg)
-    H = h.ic_hessian()
-    assert rel(H.pose_pose, z["H_pose_pose"]) <= 1e-9 and rel(H.pose_depth, z["H_pose_depth"]) <= 1e-9
-    assert rel(h.ic_gradient(), z["ic_gradient"]) <= 1e-8
-    v = gauge_vector(st.num_frames, st.num_points, st.t, st.inv_depths)
-    assert rel(project_out(h.ic_compute_step(), v), project_out(z["ic_step"], v)) <= 1e-4
-    for kind in ("ic", "fc"):
-        rep = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
-        assert rep.iterations == int(z[f"{kind}_iters"])
-        assert [s.accepted for s in rep.iters] == list(z[f"{kind}_accepted"])
-        assert np.allclose([s.energy for s in rep.iters], z[f"{kind}_energies"], rtol=1e-4, atol=0)
-        assert rel(rep.final_inv_depths, z[f"{kind}_final_d"]) <= 1e-4
-        assert rel(rep.final_t, z[f"{kind}_final_t"]) <= 1e-4
-        assert rel(rep.final_R, z[f"{kind}_final_R"]) <= 1e-4
+    if "H_pose_pose" in z:
+        h.ic_build(cfg)
+        H = h.ic_hessian()
+        assert rel(H.pose_pose, z["H_pose_pose"]) <= 1e-9 and rel(H.pose_depth, z["H_pose_depth"]) <= 1e-9
+        assert rel(H.depth_depth, z["H_depth_depth"]) <= 1e-9
+        assert rel(h.ic_gradient(), z["ic_gradient"]) <= 1e-8
+        assert list(h.warnings()) == [str(w) for w in z["warnings"]]
+        v = gauge_vector(st.num_frames, st.num_points, st.t, st.inv_depths)
+        assert rel(project_out(h.ic_compute_step(), v), project_out(z["ic_step"], v)) <= 1e-4
+    for kind in kinds(z):
+        try:
+            rep = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
+        except Error as ex:  # pragma: no cover - reported with the fixture's expectation
+            raise AssertionError(f"{kind}_run raised {type(ex).__name__}: {ex}")
+        check_run(z, kind, rep, energy_rtol=1e-5, param_tol=1e-4, energy_floor=1e-9)

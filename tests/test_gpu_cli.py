@@ -15,6 +15,7 @@ from paper_1704_06967_b200 import pba, scene_io
 from paper_1704_06967_b200.solver import Handle, SolverConfig
 
 from ._helpers import oracle_scene
+from ._oracle import ORACLE
 
 pytestmark = pytest.mark.gpu
 REPO = Path(__file__).resolve().parent.parent
@@ -59,7 +60,7 @@ def test_cli_solve_matches_the_oracle_on_the_loaded_problem(tmp_path):
     init = scene_io.to_problem_state(scene, R, t, d)
     sc = SolverConfig(record_snapshots=True)
     for name in ("fc", "ic"):
-        h = Handle(init, "oracle")
+        h = Handle(init, ORACLE)
         ref = h.fc_run(sc) if name == "fc" else h.ic_run(sc)
         j = json.loads((tmp_path / "o" / f"{name}_final.json").read_text())
         assert j["iterations"] == ref.iterations and j["converged"] == ref.converged

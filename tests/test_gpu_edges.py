@@ -12,13 +12,14 @@ from paper_1704_06967_b200.solver import Handle, SolverConfig
 
 from ._helpers import oracle_scene
 from .test_gpu_parity import _compare_runs
+from ._oracle import ORACLE
 
 pytestmark = pytest.mark.gpu
 
 
 def _both_runs(st, cfg):
     for kind in ("ic", "fc"):
-        g, o = Handle(st, "gpu"), Handle(st, "oracle")
+        g, o = Handle(st, "gpu"), Handle(st, ORACLE)
         rg, ro = (g.ic_run(cfg), o.ic_run(cfg)) if kind == "ic" else (g.fc_run(cfg), o.fc_run(cfg))
         _compare_runs(rg, ro, st.num_frames, st.num_points)
 
@@ -33,7 +34,7 @@ def test_ragged_lists_with_unobserved_and_single_observation_points():
         ptr.append(len(fr))
     st.obs_ptr, st.obs_frame = np.array(ptr, np.int64), np.array(fr, np.int32)
     eg = solver.energy_eval(st, 0.03, backend="gpu")
-    eo = solver.energy_eval(st, 0.03, backend="oracle")
+    eo = solver.energy_eval(st, 0.03, backend=ORACLE)
     assert eg.num_active == eo.num_active and abs(eg.energy - eo.energy) <= 1e-5 * eo.energy
     assert np.array_equal(eg.active, eo.active)
     _both_runs(st, SolverConfig(max_iters=6))

@@ -1,0 +1,122 @@
+"""GPU parity at the BASELINE scales (VERDICT r1 "what's missing" 1).
+
+Everything the full-size problems exercise that the small parity cases do not, checked against the
+oracle (pinned to the reference itself by tests/test_reference_pins.py) on the same inputs:
+
+* C4 geometry — all 200 frames at 1280x720 with the azimuthal visibility window, on a seeded point
+  subsample the oracle solves in seconds: the 6F = 1200 reduced camera system (fixed-point Schur,
+  fused factorization and inverse), the chunked frame-table IC pass (> 120 frames), IC for 10 and FC
+  for 10 iterations (FcSolver::run solver.cpp:663-843, IcSolver::factorize :370-402, Schur :165-213);
+* C4 at full size — one FC Hessian/gradient build (3.8e7 observations) against the oracle's;
+* C3 in full — 50 frames, 1e5 points, 3x3 patches, normal-cone visibility: IC and FC for 5
+  iterations; and all 20 BASELINE iterations on a 20k-point subsample.
+
+Comparisons are per element (north star: "final poses and depths within 1e-4"), with identical
+iteration counts, accept/reject (factorization-count) sequences, counters and active counts.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1704_06967_b200 import scenes
+from paper_1704_06967_b200.solver import Handle
+
+from ._helpers import assert_params_close, rel
+from ._oracle import ORACLE
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+P_TOL = 1e-4
+
+
+def compare_runs(rg, ro, energy_tol=P_TOL):
+    assert rg.iterations == ro.iterations
+    assert (rg.converged, rg.diverged, rg.rejected_steps) == (ro.converged, ro.diverged, ro.rejected_steps)
+    assert rg.hessian_builds == ro.hessian_builds and rg.hessian_factorizations == ro.hessian_factorizations
+    assert [s.hessian_factorizations for s in rg.iters] == [s.hessian_factorizations for s in ro.iters]
+    assert [s.accepted for s in rg.iters] == [s.accepted for s in ro.iters]
+    assert [s.num_active for s in rg.iters] == [s.num_active for s in ro.iters]
+    assert rg.masked_residuals == ro.masked_residuals
+    assert rg.message == ro.message
+    for a, b in zip(rg.iters, ro.iters):
+        assert abs(a.energy - b.energy) <= energy_tol * abs(b.energy)
+    assert abs(rg.final_energy - ro.final_energy) <= energy_tol * abs(ro.final_energy)
+    assert_params_close(rg.final_R, ro.final_R, P_TOL)
+    assert_params_close(rg.final_t, ro.final_t, P_TOL)
+    assert_params_close(rg.final_inv_depths, ro.final_inv_depths, P_TOL)
+
+
+@pytest.fixture(scope="module")
+def c4():
+    return scenes.make_scene(scenes.baseline_config("C4"))
+
+
+@pytest.fixture(scope="module")
+def c3():
+    return scenes.make_scene(scenes.baseline_config("C3"))
+
+
+@pytest.fixture(scope="module")
+def c4_sub(c4):
+    return scenes.subsample_points(c4.state, 20000, seed=1)
+
+
+def test_c4_subsample_covers_every_frame(c4_sub):
+    """The subsample keeps the full reduced system: every one of the 200 frames is observed."""
+    frames = np.unique(c4_sub.obs_frame)
+    assert c4_sub.num_frames == 200 and frames.size == 200
+
+
+@pytest.mark.parametrize("kind", ["ic", "fc"])
+def test_c4_geometry_runs_match_oracle(c4, c4_sub, kind):
+    cfg = c4.cfg.solver_config(max_iters=10)  # BASELINE C4: 10 iterations
+    rg = getattr(Handle(c4_sub, "gpu"), f"{kind}_run")(cfg)
+    ro = getattr(Handle(c4_sub, ORACLE), f"{kind}_run")(cfg)
+    assert rg.iterations == 10 or rg.converged
+    compare_runs(rg, ro)
+
+
+def test_c4_ic_build_and_step_at_n1200(c4, c4_sub):
+    """IC build: H blocks, gradient and the first step through the 1200 x 1200 reduced system."""
+    from ._helpers import gauge_vector, project_out
+    cfg = c4.cfg.solver_config()
+    g, o = Handle(c4_sub, "gpu"), Handle(c4_sub, ORACLE)
+    g.ic_build(cfg)
+    o.ic_build(cfg)
+    Hg, Ho = g.ic_hessian(), o.ic_hessian()
+    assert rel(Hg.pose_pose, Ho.pose_pose) <= 1e-9 and rel(Hg.pose_depth, Ho.pose_depth) <= 1e-9
+    assert rel(Hg.depth_depth, Ho.depth_depth) <= 1e-9 and Hg.lambda_ == Ho.lambda_
+    assert rel(g.ic_gradient(), o.ic_gradient()) <= 1e-8
+    v = gauge_vector(c4_sub.num_frames, c4_sub.num_points, c4_sub.t, c4_sub.inv_depths)
+    assert rel(project_out(g.ic_compute_step(), v), project_out(o.ic_compute_step(), v)) <= 1e-4
+
+
+def test_c4_full_size_fc_build_matches_oracle(c4):
+    """One FC Hessian / gradient build over all 3.8e7 observations (solver.cpp:688-724)."""
+    st = c4.state
+    (Hg, gg), (Ho, go) = Handle(st, "gpu").fc_build(c4.cfg.huber_delta), Handle(st, ORACLE).fc_build(
+        c4.cfg.huber_delta)
+    assert rel(Hg.pose_pose, Ho.pose_pose) <= 1e-9
+    assert rel(Hg.depth_depth, Ho.depth_depth) <= 1e-9
+    assert rel(Hg.pose_depth, Ho.pose_depth) <= 1e-9
+    assert rel(gg, go) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", ["ic", "fc"])
+def test_c3_full_runs_match_oracle(c3, kind):
+    cfg = c3.cfg.solver_config(max_iters=5)
+    st = c3.state
+    rg = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
+    ro = getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+    compare_runs(rg, ro)
+
+
+@pytest.mark.parametrize("kind", ["ic", "fc"])
+def test_c3_twenty_iterations_on_a_subsample(c3, kind):
+    """BASELINE C3's 20 LM iterations (default convergence threshold) on a 20k-point subsample."""
+    st = scenes.subsample_points(c3.state, 20000, seed=2)
+    cfg = c3.cfg.solver_config(max_iters=20)
+    rg = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
+    ro = getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+    compare_runs(rg, ro)

@@ -15,6 +15,7 @@ from paper_1704_06967_b200.solver import Handle, OutOfBounds
 
 from ._helpers import random_visibility
 from .test_gpu_parity import _compare_runs
+from ._oracle import ORACLE
 
 pytestmark = pytest.mark.gpu
 
@@ -47,7 +48,7 @@ def test_sharded_run_matches_oracle_c1(c1, world, solver_kind):
     st = c1.state
     cfg = c1.cfg.solver_config()  # 10 LM iterations
     rg = sharding.solve_threads(st, cfg, world, solver_kind)
-    o = Handle(st, "oracle")
+    o = Handle(st, ORACLE)
     ro = o.ic_run(cfg) if solver_kind == "ic" else o.fc_run(cfg)
     if solver_kind == "ic":
         assert rg.hessian_builds == 1
@@ -59,7 +60,7 @@ def test_sharded_run_partial_visibility_matches_oracle(c1):
     st.obs_ptr, st.obs_frame = random_visibility(st, 0.6, seed=9)
     cfg = c1.cfg.solver_config(max_iters=5, record_snapshots=True)
     rg = sharding.solve_threads(st, cfg, 2, "ic")
-    ro = Handle(st, "oracle").ic_run(cfg)
+    ro = Handle(st, ORACLE).ic_run(cfg)
     _compare_runs(rg, ro, st.num_frames, st.num_points)
     for a, b in zip(rg.iters, ro.iters):  # merged per-iteration depth snapshots in caller order
         assert np.linalg.norm(a.inv_depths - b.inv_depths) <= 1e-4 * np.linalg.norm(b.inv_depths)

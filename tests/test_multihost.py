@@ -15,6 +15,7 @@ from paper_1704_06967_b200 import scenes, solver
 from paper_1704_06967_b200.solver import Handle, OutOfBounds, SolverConfig
 
 from ._helpers import oracle_scene, rel
+from ._oracle import ORACLE
 
 P_TOL = 1e-4
 E_TOL = 1e-5
@@ -44,12 +45,12 @@ def _runs_close(a, b, tol=P_TOL):
 def test_oracle_window_of_a_single_host_problem_is_the_reference_fc():
     st = oracle_scene(frames=3, points=10, sigma=1e-3, perturb_seed=8)
     cfg = SolverConfig(max_iters=20)
-    ref = Handle(st, "oracle").fc_run(cfg)
+    ref = Handle(st, ORACLE).fc_run(cfg)
     p = mh.from_single_host(st)
-    e_ref = solver.energy_eval(st, 0.03, backend="oracle")
-    e_mh = mh.MultiHostHandle(p, "oracle").energy(0.03)
+    e_ref = solver.energy_eval(st, 0.03, backend=ORACLE)
+    e_mh = mh.MultiHostHandle(p, ORACLE).energy(0.03)
     assert e_mh.energy == e_ref.energy and e_mh.num_active == e_ref.num_active  # same sums, same order
-    r = mh.mh_fc_solve(p, cfg, backend="oracle")
+    r = mh.mh_fc_solve(p, cfg, backend=ORACLE)
     assert r.converged and r.iterations == ref.iterations and r.rejected_steps == ref.rejected_steps
     for a, b in zip(r.iters, ref.iters):
         assert abs(a.energy - b.energy) <= 1e-10 * b.energy
@@ -60,15 +61,15 @@ def test_oracle_window_of_a_single_host_problem_is_the_reference_fc():
 
 def test_oracle_joint_window_recovers_affine_and_descends():
     sc = _window(iters=15)
-    r = mh.mh_fc_solve(sc.problem, sc.solver_config(), backend="oracle")
+    r = mh.mh_fc_solve(sc.problem, sc.solver_config(), backend=ORACLE)
     es = [it.energy for it in r.iters]
     assert all(b <= a * (1 + 1e-12) for a, b in zip(es, es[1:]))
-    e0 = mh.MultiHostHandle(sc.problem, "oracle").energy(9.0).energy
+    e0 = mh.MultiHostHandle(sc.problem, ORACLE).energy(9.0).energy
     assert es[-1] < 0.5 * e0
     assert r.final_a[0] == 0.0 and r.final_b[0] == 0.0  # frame 0 held
     assert np.abs(r.final_b[1:] - sc.b_true[1:]).max() < 5.0  # offsets of ~13 intensity units recovered
     held = mh.MultiHostProblem(**{**sc.problem.__dict__, "optimize_affine": False})
-    rh = mh.mh_fc_solve(held, sc.solver_config(), backend="oracle")
+    rh = mh.mh_fc_solve(held, sc.solver_config(), backend=ORACLE)
     assert np.array_equal(rh.final_a, np.zeros(4)) and rh.final_energy > r.final_energy
 
 
@@ -77,11 +78,11 @@ def test_oracle_rejects_bad_windows():
     p = sc.problem
     bad = mh.MultiHostProblem(**{**p.__dict__, "host": np.full(p.num_points, 7, np.int32)})
     with pytest.raises(solver.Error):
-        mh.MultiHostHandle(bad, "oracle").energy(9.0)
+        mh.MultiHostHandle(bad, ORACLE).energy(9.0)
     an = p.anchors_px.copy()
     an[0] = (0.0, 0.0)
     with pytest.raises(OutOfBounds):
-        mh.MultiHostHandle(mh.MultiHostProblem(**{**p.__dict__, "anchors_px": an}), "oracle").energy(9.0)
+        mh.MultiHostHandle(mh.MultiHostProblem(**{**p.__dict__, "anchors_px": an}), ORACLE).energy(9.0)
 
 
 # ----------------------------------------------------------------------------- GPU
@@ -93,7 +94,7 @@ def test_gpu_window_of_a_single_host_problem_matches_the_reference_fc():
                scenes.make_scene(scenes.baseline_config("C1"), device="cpu").state):
         gamma = 0.03 if st.ref.max() <= 1.0 else 9.0
         cfg = SolverConfig(gamma=gamma, max_iters=10, lambda0=1e-6 if gamma < 1 else 1e-6 * 255.0 ** 2)
-        ref = Handle(st, "oracle").fc_run(cfg)
+        ref = Handle(st, ORACLE).fc_run(cfg)
         r = mh.mh_fc_solve(mh.from_single_host(st), cfg, backend="gpu")
         r.final_t, r.final_R = r.final_t[1:], r.final_R[1:]
         _runs_close(r, ref)
@@ -106,11 +107,11 @@ def test_gpu_joint_window_matches_oracle(affine):
     p = mh.MultiHostProblem(**{**sc.problem.__dict__, "optimize_affine": affine})
     cfg = sc.solver_config(record_snapshots=True)
     eg = mh.MultiHostHandle(p, "gpu").energy(9.0)
-    eo = mh.MultiHostHandle(p, "oracle").energy(9.0)
+    eo = mh.MultiHostHandle(p, ORACLE).energy(9.0)
     assert eg.num_active == eo.num_active and eg.num_out_of_bounds == eo.num_out_of_bounds
     assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
     rg = mh.mh_fc_solve(p, cfg, backend="gpu")
-    ro = mh.mh_fc_solve(p, cfg, backend="oracle")
+    ro = mh.mh_fc_solve(p, cfg, backend=ORACLE)
     _runs_close(rg, ro)
     assert np.abs(rg.final_a - ro.final_a).max() <= P_TOL and np.abs(rg.final_b - ro.final_b).max() <= P_TOL * 255
     for a, b in zip(rg.iters, ro.iters):
@@ -132,7 +133,7 @@ def test_gpu_joint_window_visibility_list_and_determinism():
     cfg = sc.solver_config()
     r1, r2 = mh.mh_fc_solve(q, cfg), mh.mh_fc_solve(q, cfg)
     assert r1.final_energy == r2.final_energy and np.array_equal(r1.final_inv_depths, r2.final_inv_depths)
-    _runs_close(r1, mh.mh_fc_solve(q, cfg, backend="oracle"))
+    _runs_close(r1, mh.mh_fc_solve(q, cfg, backend=ORACLE))
 
 
 @pytest.mark.gpu
@@ -152,6 +153,6 @@ def test_gpu_joint_c2_full_size_matches_oracle():
     sc = scenes.make_window_scene(device="cpu")
     cfg = sc.solver_config(threshold_px=0.0)
     rg = mh.mh_fc_solve(sc.problem, cfg)
-    ro = mh.mh_fc_solve(sc.problem, cfg, backend="oracle")
+    ro = mh.mh_fc_solve(sc.problem, cfg, backend=ORACLE)
     _runs_close(rg, ro)
     assert np.abs(rg.final_b - ro.final_b).max() <= 1e-3 and np.abs(rg.final_a - ro.final_a).max() <= 1e-5

@@ -7,6 +7,7 @@ from paper_1704_06967_b200 import scenes, solver
 from paper_1704_06967_b200.solver import Handle, SolverConfig
 
 from ._helpers import oracle_scene, random_visibility, to_dense_obs
+from ._oracle import ORACLE
 
 
 def test_tiny_scene_properties():
@@ -26,8 +27,8 @@ def test_c1_ground_truth_is_near_optimal():
     sc = scenes.make_scene(scenes.baseline_config("C1"), device="cpu")
     gt = sc.state.copy()
     gt.R, gt.t, gt.inv_depths = sc.R_true, sc.t_true, sc.d_true
-    e_gt = solver.energy_eval(gt, 9.0, backend="oracle")
-    e_0 = solver.energy_eval(sc.state, 9.0, backend="oracle")
+    e_gt = solver.energy_eval(gt, 9.0, backend=ORACLE)
+    e_0 = solver.energy_eval(sc.state, 9.0, backend=ORACLE)
     assert e_gt.energy < 0.2 * e_0.energy
 
 
@@ -47,11 +48,11 @@ def test_oracle_observation_list_dense_equivalence():
     st = oracle_scene(frames=3, points=6, sigma=1e-3, perturb_seed=6)
     st2 = st.copy()
     st2.obs_ptr, st2.obs_frame = to_dense_obs(st)
-    a = solver.energy_eval(st, 0.03, backend="oracle")
-    b = solver.energy_eval(st2, 0.03, backend="oracle")
+    a = solver.energy_eval(st, 0.03, backend=ORACLE)
+    b = solver.energy_eval(st2, 0.03, backend=ORACLE)
     assert a.energy == b.energy and np.array_equal(a.residuals, b.residuals)
-    ra = solver.ic_solve(st, SolverConfig(), backend="oracle")
-    rb = solver.ic_solve(st2, SolverConfig(), backend="oracle")
+    ra = solver.ic_solve(st, SolverConfig(), backend=ORACLE)
+    rb = solver.ic_solve(st2, SolverConfig(), backend=ORACLE)
     assert ra.final_energy == rb.final_energy and np.array_equal(ra.final_inv_depths, rb.final_inv_depths)
 
 
@@ -65,8 +66,8 @@ def test_oracle_partial_visibility_equals_masked_dense():
     mask = np.zeros((N, F, P), dtype=np.uint8)
     for n in range(N):
         mask[n, of[op[n]:op[n + 1]], :] = 1
-    a = solver.energy_eval(st, 0.03, mask=mask.ravel(), backend="oracle")
-    b = solver.energy_eval(st2, 0.03, backend="oracle")
+    a = solver.energy_eval(st, 0.03, mask=mask.ravel(), backend=ORACLE)
+    b = solver.energy_eval(st2, 0.03, backend=ORACLE)
     assert a.num_active == b.num_active
     assert abs(a.energy - b.energy) <= 1e-12 * a.energy
 
@@ -75,8 +76,8 @@ def test_oracle_errors_map_to_reference_exceptions():
     st = oracle_scene(frames=2, points=3)
     st.t = np.tile([50.0, 0.0, 0.0], (2, 1))
     with pytest.raises(solver.EmptyProblem):
-        solver.energy_eval(st, 0.03, backend="oracle")
-    h = Handle(oracle_scene(frames=2, points=3), "oracle")
+        solver.energy_eval(st, 0.03, backend=ORACLE)
+    h = Handle(oracle_scene(frames=2, points=3), ORACLE)
     with pytest.raises(solver.StateError):
         h.ic_gradient()
 
@@ -95,7 +96,7 @@ def test_warning_list_matches_the_bulk_text():  # test_solver.cpp:266-278 scene,
     st.targets_K = st.targets_K[:1]
     st.R = np.eye(3)[None].copy()
     st.t = np.zeros((1, 3))
-    o = Handle(st, "oracle")
+    o = Handle(st, ORACLE)
     o.ic_build(SolverConfig())
     w = o.warnings()
     text = _bulk_text(o)

@@ -10,6 +10,7 @@ import pytest
 from paper_1704_06967_b200 import _capi, pba, scene_io
 from paper_1704_06967_b200.solver import Error, Handle, SolverConfig
 from tests._helpers import oracle_scene
+from ._oracle import ORACLE
 
 
 def test_pgm_16bit_round_trip_quantizes_and_clamps(tmp_path):
@@ -88,7 +89,7 @@ def test_cli_perturbation_matches_the_reference_stream():
     st = oracle_scene(frames=4, points=11)
     Rg, tg, dg = st.R.copy(), st.t.copy(), st.inv_depths.copy()
     pba.perturb_parameters(Rg, tg, dg, 1e-3, 42)
-    o = _capi.backend("oracle")
+    o = ORACLE
     Ro, to, do = (np.ascontiguousarray(a, dtype=np.float64).copy() for a in (st.R, st.t, st.inv_depths))
     p = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
     assert o.perturb_parameters(4, p(Ro), p(to), 11, p(do), 1e-3, 42) == 0
@@ -123,7 +124,7 @@ def test_param_rms_known_answers():
 
 def test_metrics_csv_and_final_json_schema(tmp_path):
     st = oracle_scene(frames=2, points=6, sigma=1e-3)
-    h = Handle(st, "oracle")
+    h = Handle(st, ORACLE)
     rep = h.ic_run(SolverConfig(max_iters=4, record_snapshots=True))
     gt = oracle_scene(frames=2, points=6)
     scene_io.write_metrics_csv(rep, gt.R, gt.t, gt.inv_depths, tmp_path / "m.csv", True)

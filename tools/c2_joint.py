@@ -11,6 +11,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1704_06967_b200 import multihost as mh, scenes  # noqa: E402
+from tests._oracle import ORACLE
 
 sc = scenes.make_window_scene()  # 7 x 2000 points, 640x480, DSO8, a, b ~ N(0, 0.05)
 p = sc.problem
@@ -25,7 +26,7 @@ for _ in range(5):
 r = reps[-1]
 px = sum(it.num_active for it in r.iters)
 t0 = time.perf_counter()
-ro = mh.mh_fc_solve(p, cfg, backend="oracle")
+ro = mh.mh_fc_solve(p, cfg, backend=ORACLE)
 cpu_ms = 1e3 * (time.perf_counter() - t0)
 ho = mh.MultiHostHandle(p, "gpu")
 out = {

@@ -41,6 +41,8 @@ def check_run(z, kind, rep, energy_rtol, param_tol, energy_floor):
     are compared relatively, with an absolute floor of ``energy_floor`` times the initial energy (runs
     that converge to ~1e-10 of their starting cost are at the roundoff floor of the residuals)."""
     atol = energy_floor * abs(float(z["energy"]))
+    if energy_floor:  # plus fp64 roundoff of the texel scale (flat textures: ~1e-17 residuals vs exact 0)
+        atol += 1e-24 * max(1, int(z["num_active"]))
     assert rep.iterations == int(z[f"{kind}_iters"])
     assert [s.hessian_factorizations for s in rep.iters] == list(z[f"{kind}_factorizations"])
     assert [s.hessian_builds for s in rep.iters] == list(z[f"{kind}_builds"])
@@ -98,8 +100,12 @@ def test_gpu_matches_golden(name):
     e = h.energy(cfg.gamma)
     assert e.num_active == int(z["num_active"]) and e.num_out_of_bounds == int(z["num_oob"])
     assert np.array_equal(e.active, z["active"])
-    assert abs(e.energy - float(z["energy"])) <= 1e-5 * abs(float(z["energy"]))
-    assert rel(e.residuals, z["residuals"]) <= 1e-5
+    # 1e-5 relative, with an absolute floor at fp64 roundoff of the texel scale: on a flat texture the
+    # reference's four-term bilinear blend leaves ~1e-17 residuals where the lerp form gives exact zeros
+    floor = 1e-24 * max(1, int(z["num_active"]))
+    assert abs(e.energy - float(z["energy"])) <= 1e-5 * abs(float(z["energy"])) + floor
+    dr = np.linalg.norm(e.residuals - z["residuals"])
+    assert dr <= 1e-5 * np.linalg.norm(z["residuals"]) + 1e-12
     if "H_pose_pose" in z:
         h.ic_build(cfg)
         H = h.ic_hessian()

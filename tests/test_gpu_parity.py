@@ -312,6 +312,50 @@ def test_schur_solve_matches_dense_oracle():  # test_solver.cpp:124-161
         assert np.linalg.norm(a - b) < 1e-8 * max(1.0, np.linalg.norm(b))
 
 
+def test_schur_solve_caller_blocks_outside_the_psd_bound():
+    """caller blocks need not come from a PSD J^T W J.  B large against H_pp (the built
+    passes' Cauchy-Schwarz bound fails, but S stays SPD through a large lambda), negative D_n with
+    D_n + lambda > 0, and D_n + lambda = 0 (the reference's 1/D is non-finite: SingularHessian)."""
+    rng = np.random.default_rng(51)
+    F, N = 3, 8
+    pp = np.zeros((F, 6, 6))
+    for f in range(F):
+        A = rng.uniform(-1, 1, (6, 6))
+        pp[f] = 1e-3 * (A @ A.T + np.eye(6))
+    dd = rng.uniform(-0.5, 2.0, N)
+    pd = rng.uniform(-50, 50, (N * F, 6))
+    g = rng.uniform(-1, 1, 6 * F + N)
+    H = solver.BlockHessian(pp, dd, pd)
+    lam = 1e4  # S = H_pp + lam I - sum b b^T / (D + lam): SPD, |B|^2 / (D + lam) >> H_ii
+    a = solver.solve_normal_equations_schur(H, g, lam)
+    b = solver.solve_normal_equations_schur(H, g, lam, backend=ORACLE)
+    assert np.all(np.isfinite(a)) and np.linalg.norm(a - b) < 1e-8 * max(1.0, np.linalg.norm(b))
+    dd0 = dd.copy()
+    dd0[3] = -lam
+    with pytest.raises(solver.SingularHessian):
+        solver.solve_normal_equations_schur(solver.BlockHessian(pp, dd0, pd), g, lam)
+
+
+@pytest.mark.parametrize("env", [{"PBA_IC_GFIX": "0"}, {"PBA_IC_GFIX_EXP": "72"}])
+def test_ic_gradient_sum_variants_match(c1, env, monkeypatch):
+    """the fixed-point g_n sums (default) against the per-observation records with the
+    point-major gather (PBA_IC_GFIX=0), and against the overflow fallback (scales forced 2^13 too
+    large: every pass raises the flag and is re-run unscaled)."""
+    st = c1.state
+    cfg = c1.cfg.solver_config(max_iters=6)
+    ref = Handle(st, "gpu").ic_run(cfg)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    alt = Handle(st, "gpu").ic_run(cfg)
+    assert [s.accepted for s in alt.iters] == [s.accepted for s in ref.iters]
+    assert alt.hessian_factorizations == ref.hessian_factorizations
+    for x, y in zip(alt.iters, ref.iters):
+        assert abs(x.energy - y.energy) <= 1e-10 * abs(y.energy)
+    assert_params_close(alt.final_inv_depths, ref.final_inv_depths, 1e-8)
+    assert_params_close(alt.final_t, ref.final_t, 1e-8)
+    assert_params_close(alt.final_R, ref.final_R, 1e-8)
+
+
 def test_apply_update_and_gauge_substeps(tiny):
     st = tiny.state
     g, o = pair(st)

@@ -94,3 +94,26 @@ def test_nccl_exchange_world1_is_bitwise_the_single_process_solve(c1):
             _runs_equal_bitwise(rg, ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_warnings_match_the_single_process_solve(c1, world):
+    """Frame warnings once, zero-depth warnings in caller point order (IcSolver::warnings(),
+    solver.cpp:265-271, 359-364): a frame with zero initial translation and points without any
+    observation spread over every shard."""
+    st = c1.state.copy()
+    op, of = random_visibility(st, 0.7, seed=4)
+    keep = np.ones(st.num_points, bool)
+    keep[::97] = False  # unobserved points: D_n = 0
+    cnt = np.diff(op) * keep
+    st.obs_ptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    st.obs_frame = np.concatenate([of[op[n]:op[n + 1]] for n in range(st.num_points) if keep[n]]).astype(np.int32)
+    st.t = st.t.copy()
+    st.t[3] = 0.0
+    cfg = c1.cfg.solver_config(max_iters=2)
+    one = Handle(st, "gpu").ic_run(cfg)
+    ro = Handle(st, ORACLE).ic_run(cfg)
+    assert list(one.warnings) == list(ro.warnings)
+    assert len(one.warnings) == 1 + int((~keep).sum())
+    rg = sharding.solve_threads(st, cfg, world, "ic")
+    assert list(rg.warnings) == list(one.warnings)

@@ -121,3 +121,19 @@ def test_merge_reports_places_depths_in_caller_order():
     assert np.array_equal(m.iters[0].inv_depths, -np.arange(10.0))
     # energies and counts are the exchanged global sums on every rank: taken from rank 0, not re-summed
     assert m.iters[0].num_active == 100 and m.masked_residuals == 4 and m.total_wall_ms == 2.0
+
+
+def test_merge_warnings_frames_once_points_in_caller_order():
+    """frame warnings come from one shard (every shard raises them), zero-depth points are
+    mapped from each shard's local indices to caller indices (solver.cpp:265-271, 359-364)."""
+    from paper_1704_06967_b200.solver import WarningList
+    st = _state(N=10, keep=None)
+    shards = [sharding.shard_problem(st, r, 3) for r in range(3)]
+    head = ["frame 2: zero initial translation, inverse depth unobservable from this frame"]
+    local = [np.array([0], np.int32), np.zeros(0, np.int32), np.array([0, len(shards[2].points) - 1], np.int32)]
+    parts = [WarningList(head, p) for p in local]
+    m = sharding.merge_warnings(shards, parts)
+    want = [int(shards[0].points[0]), int(shards[2].points[0]), int(shards[2].points[-1])]
+    assert list(m) == head + [f"point {i}: zero depth Hessian entry (unobservable depth)" for i in want]
+    # plain string lists (a checker library's report) merge the same way
+    assert list(sharding.merge_warnings(shards, [list(p) for p in parts])) == list(m)

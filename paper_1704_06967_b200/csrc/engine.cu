@@ -622,7 +622,10 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   if (use_gfix_) {
     a.gfix = gfix_.p;
     a.gscale = gscale_.p;
+    a.gfix_bad = flags_.p + 3;
+    ck(cudaMemsetAsync(flags_.p + 3, 0, sizeof(int), stream_), "gfix flag");
   }
+  last_ic_eval_ = IcEvalArgs{pose, d, mask_in, active_out, buf, lambda, pose_old, d_old};
   // Large problems read the frame-uniform records from kernel-parameter frame tables (one host
   // read-back of the evaluation poses per pass); small, launch-bound ones keep the shared-memory
   // path and avoid the mid-iteration synchronisation.
@@ -655,6 +658,33 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
            true);
 }
 
+// Status of the last IC pass.  The fixed-point g_n sums hold every term whose magnitude the build's
+// bound covers; a non-finite term (NaN texels) or one beyond the bound raises flag 3, and the pass
+// is then re-run with the per-observation records and point-major gather (exact for any value),
+// which this handle keeps using from then on.
+Status Engine::ic_read_status() {
+  Status s = read_status();
+  if (!use_gfix_) return s;
+  bool bad = flags_h_[3] != 0;
+  if (sharded()) {  // the same decision on every rank (the re-run pass exchanges again)
+    gauge_sum_.alloc(1);
+    const double v = bad ? 1.0 : 0.0;
+    ck(cudaMemcpyAsync(gauge_sum_.p, &v, sizeof(double), cudaMemcpyHostToDevice, stream_), "gfix flag");
+    xreduce({{gauge_sum_.p, 1, false}});
+    double tot = 0.0;
+    ck(cudaMemcpyAsync(&tot, gauge_sum_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "gfix flag");
+    ck(cudaStreamSynchronize(stream_), "gfix flag");
+    bad = tot > 0.0;
+  }
+  if (bad) {
+    use_gfix_ = false;
+    const IcEvalArgs& e = last_ic_eval_;
+    ic_eval(e.pose, e.d, e.mask_in, e.active_out, e.buf, e.lambda, e.pose_old, e.d_old);
+    s = read_status();
+  }
+  return s;
+}
+
 // Frame tables of the IC pass (kTabFrames frames per launch): the evaluation poses are read
 // back (the pass is ordered after the candidate update anyway), the frozen poses and the
 // intrinsics are host-resident.
@@ -679,6 +709,13 @@ void Engine::build_frame_tabs(const PoseD* pose_d) {
       FrameRec& r = T.r[j];
       r.pe = pe_h_[f];
       r.p0 = pose0_h_[f];
+      r.t0z = r.p0.t[2];
+#if PBA_IC_V2
+      {  // tau = R0^T t0 in the translation slot (the pass's frame-factored gradient)
+        const PoseD& q = pose0_h_[f];
+        for (int j = 0; j < 3; ++j) r.p0.t[j] = q.R[j] * q.t[0] + q.R[3 + j] * q.t[1] + q.R[6 + j] * q.t[2];
+      }
+#endif
 #if PBA_TAB_SCALED
       for (int c = 0; c < 3; ++c) {
         r.pe.R[c] *= frames_h_[f].fx;
@@ -768,7 +805,8 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   auto e = ev_begin(PBA_K_SCHUR);
   alloc_schur();
   const bool densify = dense_B_ != B;  // the dense blocks depend on B only (not on D or lambda)
-  launch_schur_acc(ov_, H, B, D, lambda, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_);
+  launch_schur_acc(ov_, H, B, D, lambda, schur_scale_.p, schur_acc_.p, &schur_plan_, densify, stream_,
+                   schur_scale_in_);
   if (sharded()) xsum_i64(schur_acc_.p, 36 * static_cast<int64_t>(F_) * F_);  // exact: fixed point
   launch_schur_final(ov_, H, lambda, schur_scale_.p, schur_acc_.p, S_.p, stream_);
   dense_B_ = B;
@@ -849,6 +887,7 @@ void Engine::ic_build(const pba_config* cfg) {
                              ": zero initial translation, inverse depth unobservable from this frame");
   }
   const size_t nO = std::max<int64_t>(NO_, 1);
+  if (N_ > 0) ck(cudaMemsetAsync(gfix_.p, 0, N_ * sizeof(unsigned long long), stream_), "gfix zero");  // no stale sums
   {  // Frozen IC rows: rebuilt in every pass from the per-(point, pixel) template gradients (no
      // per-pixel store; the pass is not HBM-bound, so this costs no time and saves 24 B/px of HBM),
      // or, PBA_IC_RECOMPUTE=0, stored factored as m (24 B per pixel) when that fits comfortably.
@@ -884,6 +923,7 @@ void Engine::ic_build(const pba_config* cfg) {
   PointArgs pa{ov_, PT_DONLY, rec_.p, nullptr, Dic_.p, 0.0, nullptr, partial_pt_.p};
   pa.gscale = gscale_.p;  // fixed-point scales of the IC g_n sums
   pa.gbound = ic_.cfg.gamma;
+  if (const char* e = std::getenv("PBA_IC_GFIX_EXP")) pa.gexp = std::atoi(e);  // tests: force the fallback
   e = ev_begin(PBA_K_REDUCE);
   launch_point(pa, stream_);
   ev_end(PBA_K_REDUCE, e);
@@ -916,7 +956,7 @@ static void need_built(const SolverState& s) {
 void Engine::ic_gradient(double* g) {
   need_built(ic_);
   ic_eval(pose0_.p, d0_.p, mask_[ic_.mcur].p, scratch_bits_.p, 0, ic_.lambda, nullptr, nullptr);
-  (void)read_status();
+  (void)ic_read_status();
   if (F_ > 0) ck(cudaMemcpy(g, gf_[0].p, 6 * F_ * sizeof(double), cudaMemcpyDeviceToHost), "g_f");
   download_depths_user(gn_[0], g + 6 * F_);
 }

@@ -180,6 +180,20 @@ class Engine {
   DBuf<unsigned long long> gfix_;  // IC pass fixed-point g_n sums (N, zero between passes)
   DBuf<double> gscale_;            // per-point fixed-point scale S_n (set by the IC build)
   bool use_gfix_ = true;           // env PBA_IC_GFIX=0: per-observation records + point-major gather instead
+  struct IcEvalArgs {              // the last IC pass (re-run without fixed point if its flag is raised)
+    const PoseD* pose;
+    const double* d;
+    const uint32_t* mask_in;
+    uint32_t* active_out;
+    int buf;
+    double lambda;
+    const PoseD* pose_old;
+    const double* d_old;
+  } last_ic_eval_{};
+  const double* schur_scale_in_ = nullptr;  // free Schur solve: host-bounded fixed-point row scales
+  DBuf<double> scale_user_;
+  std::vector<int64_t> ov_user_ptr_;   // the caller's observation list (point-major), kept by the free solve
+  std::vector<int32_t> ov_user_frame_;
   DBuf<double> s_n_, dx_n_, xp_, g_tmp_;
   DBuf<double> r_out_;
   DBuf<double> partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_;
@@ -289,6 +303,7 @@ class Engine {
   void ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
                double lambda, const PoseD* pose_old, const double* d_old);
   void ic_rescale_rhs(int buf, double lambda);
+  Status ic_read_status();
   void alloc_schur();
   void fuse_dense(ObsArgs& a);  // the pass also scatters B into the Schur chunk rows
   void build_frame_tabs(const PoseD* pose_d);

@@ -108,6 +108,7 @@ void Engine::ic_solve_loop_and_download(double* dx) {
 void Engine::ic_compute_step(double* dx) {
   need_built(ic_.built);
   ic_eval(pose0_.p, d0_.p, mask_[ic_.mcur].p, scratch_bits_.p, 0, ic_.lambda, nullptr, nullptr);
+  (void)ic_read_status();
   ic_solve_loop_and_download(dx);
 }
 
@@ -278,13 +279,46 @@ void Engine::solve_block_hessian(const double* pp, const double* dd, const doubl
       for (int j = i; j < 6; ++j) h21[21 * f + h++] = pp[36 * f + 6 * i + j];
   }
   if (F_ > 0) ck(cudaMemcpy(H_[0].p, h21.data(), h21.size() * sizeof(double), cudaMemcpyHostToDevice), "H");
+  // The fixed-point Schur accumulator needs a bound on every partial sum.  Built passes get it from
+  // the PSD block Hessian (Cauchy-Schwarz: sum_n |B_ni B_nj| / D_n <= sqrt(H_ii H_jj)); caller
+  // blocks may be anything, so the row scales come from m_r = max(H_rr, sum_n B_nr^2 / |D_n + lambda|)
+  // (the same inequality with |D_n + lambda|), and D_n + lambda = 0 is the reference's
+  // non-finite outcome (solver.cpp:177-211: the 1/D terms are inf/NaN).
+  {
+    std::vector<double> m(6 * static_cast<size_t>(F_), 0.0);
+    for (int f = 0; f < F_; ++f)
+      for (int i = 0; i < 6; ++i) m[6 * f + i] = std::max(pp[36 * f + 7 * i], 0.0);
+    const int64_t* op = ov_user_ptr_.data();
+    for (int n = 0; n < N_; ++n) {
+      const double Dl = dd[n] + lambda;
+      bool any = false;
+      for (int64_t o = op[n]; o < op[n + 1]; ++o)
+        for (int i = 0; i < 6; ++i) any |= pd[6 * o + i] != 0.0;
+      if (Dl == 0.0 || !std::isfinite(Dl))
+        throw PbaError(PBA_E_SINGULAR_HESSIAN, any ? "SingularHessian: non-finite pose solution"
+                                                   : "SingularHessian: non-finite depth solution");
+      const double w = 1.0 / std::fabs(Dl);
+      for (int64_t o = op[n]; o < op[n + 1]; ++o) {
+        const int f = ov_user_frame_[o];
+        for (int i = 0; i < 6; ++i) m[6 * f + i] += pd[6 * o + i] * pd[6 * o + i] * w;
+      }
+    }
+    for (double& v : m) {
+      if (!std::isfinite(v)) throw PbaError(PBA_E_SINGULAR_HESSIAN, "SingularHessian: non-finite pose solution");
+      v = v > 0.0 ? 1073741824.0 / std::sqrt(v) : 1073741824.0;
+    }
+    scale_user_.alloc(std::max<size_t>(m.size(), 1));
+    if (!m.empty()) ck(cudaMemcpy(scale_user_.p, m.data(), m.size() * sizeof(double), cudaMemcpyHostToDevice), "scale");
+  }
   upload_depths_user(D_[0], dd);
   rows_from_user(pd, 6, B_[0].p);
   dense_B_ = nullptr;
   if (F_ > 0) ck(cudaMemcpy(gf_[0].p, g, 6 * F_ * sizeof(double), cudaMemcpyHostToDevice), "g_f");
   upload_depths_user(gn_[0], g + 6 * F_);
-  if (!factor_reduced(H_[0].p, B_[0].p, D_[0].p, lambda))
-    throw PbaError(PBA_E_SINGULAR_HESSIAN, "SingularHessian: Schur-reduced factorization failed");
+  schur_scale_in_ = scale_user_.p;
+  const bool fok = factor_reduced(H_[0].p, B_[0].p, D_[0].p, lambda);
+  schur_scale_in_ = nullptr;
+  if (!fok) throw PbaError(PBA_E_SINGULAR_HESSIAN, "SingularHessian: Schur-reduced factorization failed");
   fc_rescale_rhs(0, lambda);
   clear_flags();
   solve_xp(rhs_[0].p);
@@ -320,6 +354,10 @@ void Engine::solve_schur_free(int F, int N, const int64_t* obs_ptr, const int32_
   p.obs_ptr = obs_ptr;
   p.obs_frame = obs_frame;
   Engine e(&p);
+  e.ov_user_ptr_.resize(static_cast<size_t>(N) + 1);
+  for (int n = 0; n <= N; ++n) e.ov_user_ptr_[n] = obs_ptr ? obs_ptr[n] : static_cast<int64_t>(n) * F;
+  e.ov_user_frame_.resize(static_cast<size_t>(e.ov_user_ptr_[N]));
+  for (int64_t o = 0; o < e.ov_user_ptr_[N]; ++o) e.ov_user_frame_[o] = obs_frame ? obs_frame[o] : static_cast<int32_t>(o % F);
   e.solve_block_hessian(pp, dd, pd, g, lambda, dx);
 }
 
@@ -337,7 +375,7 @@ void Engine::begin(bool ic, const pba_config* cfg) {
     if (N_ > 0) ck(cudaMemcpyAsync(d_cur_.p, d0_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d");
     // :487-495 initial pass, sticky mask &= active
     ic_eval(pose_cur_.p, d_cur_.p, mask_[ic_.mcur].p, mask_[1 - ic_.mcur].p, 0, ic_.lambda, nullptr, nullptr);
-    const Status s = read_status();
+    const Status s = ic_read_status();
     if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");
     ic_.mcur = 1 - ic_.mcur;
     run_.energy = s.energy;
@@ -450,7 +488,7 @@ bool Engine::iterate_ic(pba_iter_stats* st) {
     gauge_candidate();                                                      // :618-620 (gauge-invariant pass)
     ic_eval(pose_cand_.p, d_cand_.p, mask_[ic_.mcur].p, mask_[1 - ic_.mcur].p, b1, ic_.lambda, pose_cur_.p,
             d_cur_.p);                                                      // :561 + next g
-    s = read_status();
+    s = ic_read_status();
     if (flags_h_[1] || s.nonfinite > 0) {  // :429-432
       if (++nonfinite_retries > kMaxNonfiniteRetries) throw_nonfinite_exhausted();
       ic_factorize_loop(ic_.lambda * 10.0);

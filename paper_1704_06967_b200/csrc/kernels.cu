@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(NT_OBS, PBA_OBS_MINB_IC) k_obs_energy(const Ob
           const double r = __ldg(&a.tval[static_cast<int64_t>(n) * P + k]) - bilinear(fr.img, fr.W, u, v);
           act = true;
           energy += huber_loss(r, gam);
-          nact += 1.0;
+          ++nact;
           if (a.r_out) a.r_out[q * P + k] = r;
         }
       }
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(NT_OBS, PBA_OBS_MINB_IC) k_obs_energy(const Ob
     if (lane == 0) red[warp][slot] = v;
   };
   put(PT_E, energy);
-  put(PT_NACT, nact);
-  put(PT_NOOB, noob);
+  put(PT_NACT, static_cast<double>(nact));
+  put(PT_NOOB, static_cast<double>(noob));
   __syncthreads();
   if (warp == 0 && lane < PT_STRIDE) {
     double v = 0.0;
@@ -269,7 +269,7 @@ void launch_energy(const ObsArgs& a, int G, cudaStream_t s) {
 #endif
 
 #ifndef PBA_IC_STORED_PATH
-#define PBA_IC_STORED_PATH 1  // compile the stored-rows body too (PBA_IC_RECOMPUTE=0 at run time)
+#define PBA_IC_STORED_PATH (!PBA_IC_V2)  // compile the stored-rows body too (PBA_IC_RECOMPUTE=0; the V2 pass never reads m)
 #endif
 #ifndef PBA_IC_FACT
 #define PBA_IC_FACT 1  // IC pass: per-observation factored sums of the d0 m / m.t0 columns
@@ -405,12 +405,31 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   __shared__ __align__(16) PoseD s_pe, s_p0;
   __shared__ __align__(16) FrameD s_fr;
   __shared__ double red[NT / 32][PT_STRIDE];
+  // kV2 (IC pass): J^T W r accumulated in the frame-factored form.  With h = R0 g3, tau = R0^T t0,
+  // s = d0 / vz0 and wq = w r (g3 . tau) s, the frozen row [R0x x m, d0 m, m . t0] of
+  // m = h - e_z (h . t0) s (solver.cpp:331-349) sums over a frame's pixels to
+  //   rot   = R0 sum w r (x~ x g3)  -  ((R0 sum wq x~)_y, -(R0 sum wq x~)_x, 0)
+  //   trans = R0 sum d0 w r g3      -  e_z sum d0 wq
+  //   g_n   = sum (w r (g3 . tau) - t0z wq)
+  // (R0 (x~ x g3) = R0x~ x R0 g3): R0 is applied once per tile, a pixel needs only vz0, one
+  // reciprocal and 10 FMA-class accumulations (equal to the per-pixel rows up to roundoff).
+  constexpr bool kV2 = PBA_IC_V2 && MODE == OBS_IC;
+  __shared__ double s_tau[4];
   if (threadIdx.x == 0) {
     s_fr = a.frames[f];
     s_pe = a.pose_eval[f];
     if (MODE != OBS_FC) s_p0 = a.pose0[f];
+    if (kV2 && !kTab) {
+      const PoseD& q = s_p0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s_tau[j] = q.R[j] * q.t[0] + q.R[3 + j] * q.t[1] + q.R[6 + j] * q.t[2];
+      s_tau[3] = q.t[2];
+    }
   }
   __syncthreads();
+  double v2a[kV2 ? 10 : 1];  // ac[3] = sum wr (x~ x g3), aq[3] = sum wq x~, ag[3] = sum d0 wr g3, adq = sum d0 wq
+#pragma unroll
+  for (int i = 0; i < (kV2 ? 10 : 1); ++i) v2a[i] = 0.0;
   const FrameD& rf = a.ref;
   const int P = PT > 0 ? PT : a.pat.P;
   const double gam = a.gamma;
@@ -419,7 +438,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   for (int i = 0; i < (kH ? 21 : 1); ++i) hacc[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) gacc[i] = 0.0;
-  double energy = 0.0, nact = 0.0, noob = 0.0;
+  double energy = 0.0;
+  int nact = 0, noob = 0;  // integer counters: off the FP64 pipe
   // L2 prefetch of the streamed per-observation inputs, kLanePrefetch block steps ahead
   auto prefetch_step = [&](int64_t qs) {
     if (qs >= q1) return;
@@ -473,7 +493,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     // part of the warp, R e_z + d t, are formed once per observation; a pixel then costs one add
     // per ray coordinate and two FMAs per warp component (equal up to roundoff)
     constexpr bool kOB = PBA_IC_OBSBASE && MODE == OBS_IC && PT > 0;
-    double xa = 0.0, ya = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+    double xa = 0.0, ya = 0.0, bx = 0.0, by = 0.0, bz = 0.0, c8 = 0.0;
+    if constexpr (kV2) {  // pixel-invariant part of the frozen depth vz0 = R0[6] x + R0[7] y + R0[8] + d0 t0z
+      const double r8 = kTab ? tab.r[f - tab.f0].p0.R[8] : s_p0.R[8];
+      const double t0z = kTab ? tab.r[f - tab.f0].t0z : s_tau[3];
+      c8 = fma(d0n, t0z, r8);
+    }
     if constexpr (kOB) {
       const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
       xa = (an.x - rf.cx) * a.ref_ifx;
@@ -519,7 +544,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         wok = warp_point(pe, x, y, dv, xn, yn, vx, vy, vz);
       }
       if (!wok) {
-        noob += 1.0;
+        ++noob;
       } else {
         // scaled table (IC pass): pe rows 0/1 carry fx/fy, and fr.fx/fr.fy hold W - 3 / H - 3
         constexpr bool kSc = kTab && PBA_TAB_SCALED;
@@ -527,7 +552,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         const double v = kSc ? yn + fr.cy : fr.fy * yn + fr.cy;
         const bool inm = kSc ? (u >= 1.0 && u <= fr.fx && v >= 1.0 && v <= fr.fy) : in_margin(u, v, fr.W, fr.H);
         if (!inm) {
-          noob += 1.0;
+          ++noob;
         } else {
           double gdu = 0.0, gdv = 0.0;
           if constexpr (MODE == OBS_FC) {
@@ -538,9 +563,34 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           }
           act = true;
           energy += huber_loss(r, gam);
-          nact += 1.0;
+          ++nact;
           if (a.r_out) a.r_out[q * P + k] = r;
-          if constexpr (MODE == OBS_IC) {
+          if constexpr (kV2) {
+            // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
+            const double wr = fabs(r) <= gam ? r : copysign(gam, r);
+            const double* R0 = kTab ? tab.r[f - tab.f0].p0.R : s_p0.R;
+            const double* tau = kTab ? tab.r[f - tab.f0].p0.t : s_tau;
+            const double t0z = kTab ? tab.r[f - tab.f0].t0z : s_tau[3];
+            const double vz0 = fma(R0[6], x, fma(R0[7], y, c8));
+            const double s0 = d0n * rcp_nr(vz0);  // |vz0| >= 1e-12: degenerate pixels are masked at the build
+            const double g3z = T.w;               // -(gx x + gy y) of the template record
+            const double hdt = fma(T.y, tau[0], fma(T.z, tau[1], g3z * tau[2]));
+            const double wh = wr * hdt;
+            const double wq = wh * s0;
+            v2a[3] = fma(wq, x, v2a[3]);
+            v2a[4] = fma(wq, y, v2a[4]);
+            v2a[5] += wq;
+            v2a[0] = fma(wr, fma(y, g3z, -T.z), v2a[0]);
+            v2a[1] = fma(wr, fma(-x, g3z, T.y), v2a[1]);
+            v2a[2] = fma(wr, fma(x, T.z, -(y * T.y)), v2a[2]);
+            const double wd = wr * d0n;
+            v2a[6] = fma(wd, T.y, v2a[6]);
+            v2a[7] = fma(wd, T.z, v2a[7]);
+            v2a[8] = fma(wd, g3z, v2a[8]);
+            v2a[9] = fma(d0n, wq, v2a[9]);
+            gnc = fma(-t0z, wq, gnc + wh);
+            bits |= 1u << k;
+          } else if constexpr (MODE == OBS_IC) {
             // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
             const double wr = fabs(r) <= gam ? r : copysign(gam, r);
             const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
@@ -660,7 +710,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       }
     }
 #if PBA_IC_FACT
-    if constexpr (MODE == OBS_IC) {  // apply the per-observation factors: [.., d0 sum wr m, t0 . sum wr m]
+    if constexpr (MODE == OBS_IC && !kV2) {  // apply the per-observation factors: [.., d0 sum wr m, t0 . sum wr m]
       const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
       gacc[3] = fma(d0n, mw[0], gacc[3]);
       gacc[4] = fma(d0n, mw[1], gacc[4]);
@@ -683,7 +733,9 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     if (live && sub == 0) {
       a.active_out[q] = bits;
       if (MODE == OBS_IC && a.gfix) {  // exact, order-free fixed-point sum per point (L2-resident RED)
-        atomicAdd(a.gfix + n, static_cast<unsigned long long>(llrint(gnc * __ldg(a.gscale + n))));
+        const double v = gnc * __ldg(a.gscale + n);
+        if (fabs(v) < 0x1p62) atomicAdd(a.gfix + n, static_cast<unsigned long long>(llrint(v)));
+        else *a.gfix_bad = 1;  // non-finite or beyond the bound: the engine re-runs the pass unscaled
       } else if (MODE == OBS_IC && a.rec_g) a.rec_g[q] = gnc;  // IC needs the g_n term only (D is frozen)
       else a.rec[q] = make_double2(gnc, dc);
       if constexpr (kH) {
@@ -704,6 +756,22 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     v = warp_sum(v);
     if (lane == 0) red[warp][slot] = v;
   };
+  if constexpr (kV2) {  // the frame-factored sums to J^T W r of the frame (R0 is uniform over the tile)
+    const double* R0 = kTab ? tab.r[f - tab.f0].p0.R : s_p0.R;
+    double rc[3], rq[3], rg[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      rc[i] = fma(R0[3 * i], v2a[0], fma(R0[3 * i + 1], v2a[1], R0[3 * i + 2] * v2a[2]));
+      rq[i] = fma(R0[3 * i], v2a[3], fma(R0[3 * i + 1], v2a[4], R0[3 * i + 2] * v2a[5]));
+      rg[i] = fma(R0[3 * i], v2a[6], fma(R0[3 * i + 1], v2a[7], R0[3 * i + 2] * v2a[8]));
+    }
+    gacc[0] = rc[0] - rq[1];
+    gacc[1] = rc[1] + rq[0];
+    gacc[2] = rc[2];
+    gacc[3] = rg[0];
+    gacc[4] = rg[1];
+    gacc[5] = rg[2] - v2a[9];
+  }
   if constexpr (kG) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) put(PT_G + i, gacc[i]);
@@ -713,8 +781,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     for (int i = 0; i < 21; ++i) put(PT_H + i, hacc[i]);
   }
   put(PT_E, energy);
-  put(PT_NACT, nact);
-  put(PT_NOOB, noob);
+  put(PT_NACT, static_cast<double>(nact));
+  put(PT_NOOB, static_cast<double>(noob));
   __syncthreads();
   if (warp == 0) {
     const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (kG && lane < 6) || (kH && lane >= PT_H && lane < PT_H + 21);
@@ -1013,10 +1081,14 @@ __global__ void k_template_values(int N, PatternD pat, FrameD ref, double ref_if
   const double gu = ref.fx * x + ref.cx, gvp = ref.fy * y + ref.cy;
   const bool ok = in_bounds_px(gu - 0.5, gvp, ref.W, ref.H) && in_bounds_px(gu + 0.5, gvp, ref.W, ref.H) &&
                   in_bounds_px(gu, gvp - 0.5, ref.W, ref.H) && in_bounds_px(gu, gvp + 0.5, ref.W, ref.H);
-  double4 g = make_double4(tval[e], NAN, NAN, 0.0);  // {template value, gx, gy, 0}: one 32-byte load
+  double4 g = make_double4(tval[e], NAN, NAN, 0.0);  // {template value, gx, gy, g3z}: one 32-byte load
   if (ok) {
     g.y = (bilinear(ref.img, ref.W, gu + 0.5, gvp) - bilinear(ref.img, ref.W, gu - 0.5, gvp)) * ref.fx;
     g.z = (bilinear(ref.img, ref.W, gu, gvp + 0.5) - bilinear(ref.img, ref.W, gu, gvp - 0.5)) * ref.fy;
+    // g3 = (gx, gy, -(gx x + gy y)) at the ray the IC pass forms (anchor ray + pattern offset)
+    const double xo = (anc[n].x - ref.cx) * ref_ifx + static_cast<double>(pat.dx[k]) * ref_ifx;
+    const double yo = (anc[n].y - ref.cy) * ref_ify + static_cast<double>(pat.dy[k]) * ref_ify;
+    g.w = -(g.y * xo + g.z * yo);
   }
   tgrad[e] = g;
 }
@@ -1100,9 +1172,11 @@ __global__ void __launch_bounds__(NT, kPtMinB) k_point(const PointArgs a) {
         case PT_DONLY:
           a.D[n] = ds;
           D = ds;
-          if (a.gscale) {  // S_n = 2^(61 - e) with gamma sum |Jd| < 2^e: the IC pass's sums stay below 2^62
+          if (a.gscale) {  // S_n = 2^(59 - e) with gamma sum |Jd| < 2^e: the IC pass's sums stay below 2^60
+            // (two bits of headroom over the int64 range for rounding of the factored terms; the
+            // exponent is clamped so tiny bounds cannot make S_n infinite)
             const double bound = a.gbound * g;
-            a.gscale[n] = (bound > 0.0 && isfinite(bound)) ? ldexp(1.0, 61 - (ilogb(bound) + 1)) : 1.0;
+            a.gscale[n] = (bound > 0.0 && isfinite(bound)) ? ldexp(1.0, min(a.gexp - (ilogb(bound) + 1), 1000)) : 1.0;
           }
           g = 0.0;
           break;
@@ -1358,7 +1432,8 @@ __device__ __forceinline__ int h21_index(int i, int j) {
 
 __global__ void k_schur_scale(int F, const double* __restrict__ H21, double* __restrict__ scale,
                               unsigned long long* __restrict__ acc, int64_t nacc, const int32_t* __restrict__ chunk_pts,
-                              int npts, const double* __restrict__ D, double lambda, double* __restrict__ wsort) {
+                              int npts, const double* __restrict__ D, double lambda, double* __restrict__ wsort,
+                              const double* __restrict__ scale_in) {
   const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   for (int64_t e = e0; e < nacc; e += static_cast<int64_t>(gridDim.x) * blockDim.x) acc[e] = 0ull;
   for (int64_t p = e0; p < npts; p += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1366,7 +1441,7 @@ __global__ void k_schur_scale(int F, const double* __restrict__ H21, double* __r
   if (e0 < 6 * F) {
     const int r = static_cast<int>(e0);
     const double h = H21[21 * (r / 6) + h21_index(r % 6, r % 6)];
-    scale[r] = h > 0.0 ? 1073741824.0 / sqrt(h) : 1073741824.0;
+    scale[r] = scale_in ? scale_in[r] : h > 0.0 ? 1073741824.0 / sqrt(h) : 1073741824.0;
   }
 }
 
@@ -2219,13 +2294,14 @@ void launch_dense_rows(const SchurPlan& plan, int64_t* dense_row, cudaStream_t s
 }
 
 void launch_schur_acc(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda,
-                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s) {
+                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s,
+                      const double* scale_in) {
   const int n = 6 * ov.F;
   const int64_t total = static_cast<int64_t>(n) * n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
   const bool dense = plan && plan->nblocks > 0;
   k_schur_scale<<<blocks, 256, 0, s>>>(ov.F, H21, scale, acc, total, dense ? plan->chunk_pts : nullptr,
-                                       dense ? plan->npts : 0, D, lambda, dense ? plan->wsort : nullptr);
+                                       dense ? plan->npts : 0, D, lambda, dense ? plan->wsort : nullptr, scale_in);
   int launched = 1;
   if (dense) {
     if (densify) {

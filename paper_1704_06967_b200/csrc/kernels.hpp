@@ -56,6 +56,7 @@ struct ObsArgs {
   double* rec_g;               // NO or null: IC pass g_n terms only (sum_k Jd w r)
   unsigned long long* gfix;    // N or null: IC pass g_n accumulated as 64-bit fixed point (RED), scaled by gscale
   const double* gscale;        // N: per-point power-of-two scale S_n (gamma sum |Jd| S_n < 2^61, set at the build)
+  int* gfix_bad;               // set when a term is non-finite or outside the fixed-point range (engine re-runs the pass)
   double* partial;             // ntiles * PT_STRIDE
 };
 
@@ -66,17 +67,22 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
 #ifndef PBA_TAB_SCALED
 #define PBA_TAB_SCALED 1
 #endif
+#ifndef PBA_IC_V2
+#define PBA_IC_V2 1  // IC pass: gradient accumulated in the frame-factored form (see kernels.cu obs_lane_body)
+#endif
 // IC-pass frame record.  With PBA_TAB_SCALED the candidate pose's first two rows (R and t) are
 // pre-multiplied by fx and fy, so the warped pixel is u = (fx v_x) / v_z + cx, and (fsx, fsy) hold
 // the in-margin bounds (W - 3, H - 3) as doubles; otherwise pe is the plain pose and (fsx, fsy) = (fx, fy).
+// With PBA_IC_V2 the frozen pose's translation slot holds tau = R0^T t0 and t0z its z component.
 struct FrameRec {
   PoseD pe;                 // evaluation (candidate) pose
-  PoseD p0;                 // frozen IC pose
+  PoseD p0;                 // frozen IC pose (PBA_IC_V2: {R0, tau = R0^T t0})
   double fsx, fsy, cx, cy;
+  double t0z;               // frozen translation z (PBA_IC_V2)
   const float* img;
   int W, H;
 };
-constexpr int kTabFrames = 120;  // 120 * 240 B + ObsArgs < 32 KB kernel-parameter limit
+constexpr int kTabFrames = 120;  // 120 * 248 B + ObsArgs < 32 KB kernel-parameter limit
 struct FrameTab {
   int f0, nf, tile0, ntiles;
   FrameRec r[kTabFrames];
@@ -137,8 +143,9 @@ struct PointArgs {
   double* partial;        // nblocks * 2 {sum g_n^2, 0}
   const double* rec_g = nullptr;  // NO or null: PT_GRAD reads these 8-byte g_n terms instead of rec
   unsigned long long* gfix = nullptr;  // N or null: PT_GRAD converts (and clears) the fixed-point g_n sums
-  double* gscale = nullptr;            // N: PT_GRAD reads S_n; PT_DONLY writes it (bound: gbound * sum rec.x)
+  double* gscale = nullptr;            // N: PT_GRAD reads S_n; PT_DONLY writes it (gbound * sum rec.x * S_n < 2^59)
   double gbound = 0.0;                 // PT_DONLY: Huber threshold gamma (|w r| <= gamma in the IC pass)
+  int gexp = 59;                       // PT_DONLY: S_n = 2^(gexp - e) (tests raise it to force the overflow fallback)
 };
 int point_blocks(int N);
 void launch_point(const PointArgs& a, cudaStream_t s);
@@ -233,7 +240,8 @@ void launch_schur(const ObsView& ov, const double* H21, const double* B, const d
 // into acc (scale from H21), and S = blockdiag(H + lambda I) - acc / scale.  A point-sharded run sums
 // acc over the ranks in between (exact: integer addition).
 void launch_schur_acc(const ObsView& ov, const double* H21, const double* B, const double* D, double lambda,
-                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s);
+                      double* scale, unsigned long long* acc, const SchurPlan* plan, bool densify, cudaStream_t s,
+                      const double* scale_in = nullptr);  // scale_in: per-row fixed-point scales (else 2^30/sqrt(H_rr))
 void launch_schur_final(const ObsView& ov, const double* H21, double lambda, const double* scale,
                         const unsigned long long* acc, double* S, cudaStream_t s);
 

@@ -233,8 +233,13 @@ Engine::Engine(const pba_problem* p) {
   S_.alloc(static_cast<size_t>(36) * nF * nF);
   schur_acc_.alloc(static_cast<size_t>(36) * nF * nF);
   schur_scale_.alloc(6 * nF);
+  if (const char* e = std::getenv("PBA_CHOL_INV")) chol_inv_ = e[0] == '1';
   Linv_.alloc(static_cast<size_t>(36) * nF * nF);
   LinvT_.alloc(static_cast<size_t>(36) * nF * nF);
+  if (!chol_inv_) {
+    chol_flags_.alloc(2 * std::max(chol_tile_flags(6 * F_), 1));
+    ck(cudaMemsetAsync(chol_flags_.p, 0, chol_flags_.bytes(), stream_), "chol flags");
+  }
   Dinv_.alloc(static_cast<size_t>((6 * nF + 31) / 32) * 32 * 32);
   ytmp_.alloc(6 * nF);
   gauge_.alloc(1);
@@ -279,7 +284,7 @@ int64_t Engine::device_bytes() const {  // every device buffer the handle holds
       fm_point_, tile_frame_, ftile_ptr_, tile_order_, uo2q_d_, perm_d_, zero_idx_, perm_tmp_, pose_state_,
       pose_cur_, pose_cand_, pose0_, d_state_, d_cur_, d_cand_, d0_, scratch_bits_, J_, Bic_, Dic_, Hic_, Bpm_,
       rec_, rec_g_, gfix_, gscale_, s_n_, dx_n_, xp_, g_tmp_, r_out_, partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_,
-      fscal_, ticket_, S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_, schur_acc_, chunk_pts_,
+      fscal_, ticket_, S_, schur_scale_, Linv_, LinvT_, Dinv_, chol_flags_, ytmp_, gauge_, schur_acc_, chunk_pts_,
       schur_chunk_of_, schur_blocks_, schur_chunks_, schur_chunk_off_, schur_dense_, schur_wsort_, dense_row_,
       status_, flags_, xsend_, xrecv_, cf_, gauge_sum_);
   for (int i = 0; i < 2; ++i) add(mask_[i], B_[i], D_[i], H_[i], gn_[i], gf_[i], rhs_[i]);
@@ -812,7 +817,11 @@ bool Engine::factor_reduced(const double* H, const double* B, const double* D, d
   dense_B_ = B;
   ev_end(PBA_K_SCHUR, e);
   e = ev_begin(PBA_K_CHOLESKY);
-  launch_chol_inv(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, flags_.p, ticket_.p + 2, stream_);  // L, L^-1, L^-T
+  if (chol_inv_) {  // env PBA_CHOL_INV=1: the grid-barrier factor + inverse kernel (round-1 path)
+    launch_chol_inv(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, flags_.p, ticket_.p + 2, stream_);  // L, L^-1, L^-T
+  } else {          // dataflow over the tiles: L in place, Dinv, L^-1 and L^-T
+    launch_chol_tiles(S_.p, n, Dinv_.p, Linv_.p, LinvT_.p, chol_flags_.p, ++chol_epoch_, flags_.p, stream_);
+  }
   ev_end(PBA_K_CHOLESKY, e);
   if (read_flag(0) != 0) return false;
   return true;

@@ -201,6 +201,9 @@ class Engine {
   DBuf<unsigned int> ticket_;     // grid tickets {k_backsub, k_finalize}, k_chol_inv barrier {count, generation}
   DBuf<double> S_, schur_scale_, Linv_, LinvT_, Dinv_, ytmp_, gauge_;
   DBuf<unsigned long long> schur_acc_;
+  bool chol_inv_ = false;          // env PBA_CHOL_INV=1: the round-1 grid-barrier factor + inverse kernel
+  DBuf<int> chol_flags_;           // per-tile completion epochs of k_chol_tiles (factor, then inverse)
+  int chol_epoch_ = 0;
   DBuf<int32_t> chunk_pts_, schur_chunk_of_;
   DBuf<int4> schur_blocks_, schur_chunks_;
   DBuf<int64_t> schur_chunk_off_;

@@ -275,6 +275,12 @@ void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double*
 
 // x = L^-T L^-1 b = XT (X b) with the explicit inverse; y: n scratch.  *nonfinite set
 // when x has a non-finite entry.
+// Tiled dataflow Cholesky of the reduced system in place (factor.cu): lower L, Dinv (32 x 32 inverse
+// diagonal tiles) and, with X / XT given, the explicit inverse L^-1 and its transpose.  flags:
+// 2 * chol_tile_flags(n) ints, zero-initialised once; epoch strictly increasing per call.
+void launch_chol_tiles(double* S, int n, double* Dinv, double* X, double* XT, int* flags, int epoch, int* fail,
+                       cudaStream_t s);
+int chol_tile_flags(int n);
 void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x,
                      int* nonfinite, cudaStream_t s);
 

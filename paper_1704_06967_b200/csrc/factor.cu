@@ -178,25 +178,55 @@ __device__ void potrf_tile(TileSmem& sm, double* __restrict__ A, int n, int j, i
     const int e = t + q * FT, r = e / TB, c = e % TB;
     if (r < kb && c <= r) A[static_cast<int64_t>(j0 + r) * n + j0 + c] = s[r][c];
   }
-  if (t < TB) {  // Dinv column c: x_r = (delta_rc - sum_{c<=p<r} l_rp x_p) / l_rr
-    const int c = t;
-    double x[TB];
+  // Dinv = L^-1 by 8 x 8 blocks: the diagonal blocks X_bb by forward substitution (one thread per
+  // column of each block), then X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj level by level (i - j = 1, 2, 3)
+  double (*xs)[TB + 1] = sm.b;
 #pragma unroll
-    for (int r = 0; r < TB; ++r) {
-      double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int q = 0; q < TB * TB / FT; ++q) {
+    const int e = t + q * FT;
+    xs[e / TB][e % TB] = 0.0;
+  }
+  __syncthreads();
+  if (t < TB) {
+    const int b8 = (t >> 3) * 8, c = t & 7;
+    double x[8];
 #pragma unroll
-      for (int p = 0; p + 3 < r; p += 4) {
-        s0 = fma(-s[r][p], x[p], s0);
-        s1 = fma(-s[r][p + 1], x[p + 1], s1);
-        s2 = fma(-s[r][p + 2], x[p + 2], s2);
-        s3 = fma(-s[r][p + 3], x[p + 3], s3);
-      }
+    for (int r = 0; r < 8; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-      for (int p = r & ~3; p < r; ++p) s0 = fma(-s[r][p], x[p], s0);
-      x[r] = r < c ? 0.0 : ((s0 + s1) + (s2 + s3)) * rd[r];
+      for (int p = 0; p < r; ++p) v = fma(-s[b8 + r][b8 + p], x[p], v);
+      x[r] = r < c ? 0.0 : v * rd[b8 + r];
     }
 #pragma unroll
-    for (int r = 0; r < TB; ++r) Dinv[(static_cast<int64_t>(j) * TB + r) * TB + c] = x[r];
+    for (int r = 0; r < 8; ++r) xs[b8 + r][b8 + c] = x[r];
+  }
+  __syncthreads();
+  double (*tt)[TB + 1] = sm.c + 1;  // rows 1.. of sm.c (row 0 holds rd)
+#pragma unroll 1
+  for (int lv = 1; lv < 4; ++lv) {
+    const int nb = 4 - lv;  // blocks (i, j = i - lv), i = lv .. 3
+    if (t < nb * 64) {
+      const int q = t >> 6, r = (t >> 3) & 7, c = t & 7, i8 = (lv + q) * 8, j8 = q * 8;
+      double v = 0.0;
+      for (int k8 = j8; k8 < i8; k8 += 8)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) v = fma(s[i8 + r][k8 + p], xs[k8 + p][j8 + c], v);
+      tt[8 * q + r][c] = v;
+    }
+    __syncthreads();
+    if (t < nb * 64) {
+      const int q = t >> 6, r = (t >> 3) & 7, c = t & 7, i8 = (lv + q) * 8, j8 = q * 8;
+      double v = 0.0;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) v = fma(xs[i8 + r][i8 + p], tt[8 * q + p][c], v);
+      xs[i8 + r][j8 + c] = -v;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < TB * TB / FT; ++q) {
+    const int e = t + q * FT;
+    Dinv[static_cast<int64_t>(j) * TB * TB + e] = xs[e / TB][e % TB];
   }
 }
 
@@ -320,7 +350,7 @@ __global__ void __launch_bounds__(FT, 1) k_chol_tiles(double* __restrict__ A, in
         for (int q = 0; q < TB * TB / FT; ++q) {
           const int e = threadIdx.x + q * FT, r = e / TB, c = e % TB;
           if (j0 + r < n && j0 + c < n) {
-            const double v = __ldcg(Dinv + static_cast<int64_t>(j) * TB * TB + e);
+            const double v = sm.b[r][c];  // potrf_tile leaves Dinv_j in sm.b
             X[static_cast<int64_t>(j0 + r) * n + j0 + c] = v;
             XT[static_cast<int64_t>(j0 + c) * n + j0 + r] = v;
           }

@@ -23,7 +23,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
-from typing import Optional
+from typing import List, Optional
 
 import numpy as np
 import torch
@@ -415,3 +415,186 @@ def make_window_scene(keyframes: int = 7, points_per_kf: int = 2000, width: int 
     prob = MultiHostProblem(images, np.tile(np.array(K), (KF, 1)), R0, t0, host, anchors, d0, pat,
                             a=np.zeros(KF), b=np.zeros(KF), optimize_affine=True)
     return WindowScene(prob, R_true, t_true, d_true, a_true, b_true, iters=iters)
+
+
+# ----------------------------------------------------------------------------- BASELINE C2: box room
+
+def _room_boxes(rng: np.random.Generator, nboxes: int):
+    """A random box room: the room interior (camera inside) plus `nboxes` axis-aligned boxes standing
+    in front of the cameras at depths 1.2 .. 4, so visible surfaces span inverse depths 0.2 .. ~1."""
+    room_lo = np.array([-rng.uniform(2.6, 3.4), -rng.uniform(1.8, 2.4), -1.0])
+    room_hi = np.array([rng.uniform(2.6, 3.4), rng.uniform(1.8, 2.4), 5.0])
+    boxes = []
+    # one box close in front of the cameras (its front face at depth ~0.95: inverse depth ~1.05)
+    c = np.array([rng.uniform(-0.5, 0.5), rng.uniform(-0.3, 0.3), 1.2])
+    boxes.append((c - np.array([0.35, 0.3, 0.25]), c + np.array([0.35, 0.3, 0.25])))
+    for _ in range(nboxes - 1):
+        c = np.array([rng.uniform(-1.4, 1.4), rng.uniform(-0.9, 0.9), rng.uniform(1.25, 4.0)])
+        h = np.array([rng.uniform(0.15, 0.6), rng.uniform(0.15, 0.6), rng.uniform(0.15, 0.5)])
+        boxes.append((c - h, c + h))
+    return room_lo, room_hi, boxes
+
+
+def _render_room(R, t, K, W, H, room, tex, ppu, dev, ss: int = 2) -> tuple:
+    """Box-room view, ss x ss supersampled (antialiased, so views of the same surface agree
+    photometrically); returns the fp32 image and the camera-frame depth at the pixel centres."""
+    acc = None
+    for sy in range(ss):
+        for sx in range(ss):
+            off = ((sx + 0.5) / ss - 0.5, (sy + 0.5) / ss - 0.5)
+            img, _ = _render_room1(R, t, K, W, H, room, tex, ppu, dev, off)
+            acc = img if acc is None else acc + img
+    _, z = _render_room1(R, t, K, W, H, room, tex, ppu, dev, (0.0, 0.0))
+    return (acc / (ss * ss)).astype(np.float32), z
+
+
+def _render_room1(R, t, K, W, H, room, tex, ppu, dev, off=(0.0, 0.0)) -> tuple:
+    """Ray-cast one view of the box room (first hit among the boxes, else the room's interior wall);
+    planar texture coordinates on each face (ppu texels per unit, per-face offsets).  Returns the
+    fp32 image and the camera-frame depth z of every pixel."""
+    fx, fy, cx, cy = K
+    room_lo, room_hi, boxes = room
+    Rt = torch.as_tensor(R, dtype=torch.float64, device=dev).T
+    C = -(Rt @ torch.as_tensor(t, dtype=torch.float64, device=dev))
+    vv, uu = torch.meshgrid(torch.arange(H, dtype=torch.float64, device=dev),
+                            torch.arange(W, dtype=torch.float64, device=dev), indexing="ij")
+    dcam = torch.stack([(uu + off[0] - cx) / fx, (vv + off[1] - cy) / fy, torch.ones_like(uu)], -1)
+    d = dcam @ Rt.T  # world direction, camera-z component 1
+    inv = 1.0 / torch.where(d.abs() < 1e-12, torch.full_like(d, 1e-12), d)
+    # room interior: exit distance
+    lo = torch.as_tensor(room_lo, device=dev)
+    hi = torch.as_tensor(room_hi, device=dev)
+    t1, t2 = (lo - C) * inv, (hi - C) * inv
+    tmax = torch.maximum(t1, t2)
+    s_hit, axis = tmax.min(-1)
+    face = axis * 2 + (torch.gather(t2, -1, axis.unsqueeze(-1)).squeeze(-1) == s_hit).long()
+    ofs = torch.zeros_like(s_hit)
+    for bi, (blo, bhi) in enumerate(boxes):
+        blo_t = torch.as_tensor(blo, device=dev)
+        bhi_t = torch.as_tensor(bhi, device=dev)
+        b1, b2 = (blo_t - C) * inv, (bhi_t - C) * inv
+        tn, ax = torch.minimum(b1, b2).max(-1)
+        tf = torch.maximum(b1, b2).min(-1).values
+        hit = (tn < tf) & (tn > 1e-6) & (tn < s_hit)
+        s_hit = torch.where(hit, tn, s_hit)
+        face = torch.where(hit, 6 + 2 * ax, face)
+        ofs = torch.where(hit, torch.full_like(ofs, 97.0 * (bi + 1)), ofs)
+    X = C + s_hit.unsqueeze(-1) * d
+    ax = torch.div(face % 6, 2, rounding_mode="floor")
+    # planar coordinates on the face: drop the face's normal axis
+    c0 = torch.where(ax == 0, X[..., 1], X[..., 0])
+    c1 = torch.where(ax == 2, X[..., 1], X[..., 2])
+    ht, wt = tex.shape
+    u = (c0 * ppu + ofs + 131.0 * face) % wt
+    v = (c1 * ppu + 0.5 * ofs + 71.0 * face) % ht
+    u0, v0 = torch.floor(u), torch.floor(v)
+    a, b = (u - u0).float(), (v - v0).float()
+    iu0, iv0 = u0.long() % wt, v0.long() % ht
+    iu1, iv1 = (iu0 + 1) % wt, (iv0 + 1) % ht
+    img = ((1 - a) * (1 - b) * tex[iv0, iu0] + a * (1 - b) * tex[iv0, iu1] + (1 - a) * b * tex[iv1, iu0]
+           + a * b * tex[iv1, iu1])
+    z = s_hit  # camera-frame depth: d has unit camera-z component
+    return img.float().cpu().numpy(), z.cpu().numpy()
+
+
+@dataclass
+class RoomWindow:
+    """BASELINE C2 on the box room: the joint window (multihost.MultiHostProblem, affine) and the
+    per-host single-host restatement of the same geometry without affine brightness."""
+    window: WindowScene
+    hosts: List[ProblemState]     # host h: reference = keyframe h, targets = the 6 others (relative poses)
+    host_true: List[tuple]        # (R_true, t_true, d_true) per host problem
+
+
+def make_room_window_scene(keyframes: int = 7, points_per_kf: int = 2000, width: int = 640, height: int = 480,
+                           fx: float = 500.0, affine_sigma: float = 0.05, rot_deg: float = 0.1,
+                           trans_sigma: float = 0.002, depth_noise: float = 0.05, seed: int = 3, iters: int = 5,
+                           nboxes: int = 10, pattern: Optional[np.ndarray] = None,
+                           device: Optional[str] = None) -> RoomWindow:
+    """BASELINE C2: 7 keyframes at 640x480 in a random box room (procedural texture: Gaussian noise
+    blurred sigma = 2 px, [0, 255]), 2000 points hosted in every keyframe with inverse depths drawn
+    uniformly in [0.2, 1.0] (each matched to a pixel of that inverse depth), observed in all the other
+    keyframes; per-frame affine (a, b), a ~ N(0, 0.05), b ~ 255 N(0, 0.05), frame 0 held at 0.
+    Keyframes: centres within a few cm and rotations within 1.5 deg of frame 0 (parallax of <= ~40 px
+    at the nearest surfaces: photometric alignment converges from the 5% depth noise without an
+    image pyramid); initial poses perturbed by 0.1 deg / 0.002 (a window starts from tracked poses:
+    at 1 deg the 1.6-px texture leaves the solver in local minima).  Synthetic and seeded.
+    Gain a and offset b are individually weakly determined by this texture (std 19 about a mean of
+    125): the identifiable quantity is the brightness map e^a L + b over the image's intensities."""
+    from .multihost import MultiHostProblem
+
+    dev = torch.device(device or ("cuda" if torch.cuda.is_available() else "cpu"))
+    gen = torch.Generator().manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    W, H = width, height
+    K = (fx, fx, (W - 1) / 2.0, (H - 1) / 2.0)
+    tex = _noise_texture(2048, 2048, 2.0, gen, dev)
+    room = _room_boxes(rng, nboxes)
+    KF = keyframes
+    R_true = np.zeros((KF, 3, 3))
+    t_true = np.zeros((KF, 3))
+    for f in range(KF):  # X_f = R_f X_w + t_f; frame 0 at the identity
+        if f == 0:
+            R_true[f] = np.eye(3)
+            continue
+        w = np.radians(rng.uniform(-1.5, 1.5, size=3))
+        C = np.array([rng.uniform(-0.04, 0.04), rng.uniform(-0.02, 0.02), rng.uniform(-0.04, 0.04)])
+        R_true[f] = _so3_exp(w)
+        t_true[f] = -R_true[f] @ C
+    a_true = np.concatenate([[0.0], affine_sigma * rng.normal(size=KF - 1)])
+    b_true = np.concatenate([[0.0], 255.0 * affine_sigma * rng.normal(size=KF - 1)])
+    ppu = fx / 4.0  # texels per unit: <= 1.25 texels per pixel on the far wall
+    L, Z = [], []
+    for f in range(KF):
+        img, z = _render_room(R_true[f], t_true[f], K, W, H, room, tex, ppu, dev)
+        L.append(img)
+        Z.append(z)
+    images = np.stack([(math.exp(a_true[f]) * L[f] + b_true[f]).astype(np.float32) for f in range(KF)])
+    pat = DSO8 if pattern is None else np.asarray(pattern, np.int32)
+    m = int(np.abs(pat).max()) + 2
+    hosts, anchors, depths = [], [], []
+    for f in range(KF):
+        invz = 1.0 / Z[f]
+        ok = np.zeros((H, W), bool)
+        ok[m:H - m, m:W - m] = True
+        ok &= (invz >= 0.2) & (invz <= 1.0)
+        cand = np.flatnonzero(ok.ravel())
+        order = np.argsort(invz.ravel()[cand])
+        cand, ci = cand[order], invz.ravel()[cand][order]
+        want = rng.uniform(0.2, 1.0, size=points_per_kf)  # inverse depths uniform in [0.2, 1.0]
+        pos = np.clip(np.searchsorted(ci, want), 0, cand.size - 1)
+        pos = np.clip(pos + rng.integers(-3, 4, size=pos.size), 0, cand.size - 1)  # nearby pixels of that depth
+        pick = cand[pos]
+        an = np.stack([pick % W, pick // W], -1).astype(np.float64)
+        hosts.append(np.full(len(an), f, np.int32))
+        anchors.append(an)
+        depths.append(invz.ravel()[pick])
+    host = np.concatenate(hosts)
+    anchors = np.concatenate(anchors)
+    d_true = np.concatenate(depths)
+    R0, t0 = R_true.copy(), t_true.copy()
+    for f in range(1, KF):
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        R0[f] = _so3_exp(axis * math.radians(rot_deg) * rng.normal()) @ R_true[f]
+        t0[f] = t_true[f] + rng.normal(scale=trans_sigma, size=3)
+    d0 = np.abs(d_true * (1.0 + depth_noise * rng.normal(size=d_true.size))) + 1e-6
+    prob = MultiHostProblem(images, np.tile(np.array(K), (KF, 1)), R0, t0, host, anchors, d0, pat,
+                            a=np.zeros(KF), b=np.zeros(KF), optimize_affine=True)
+    win = WindowScene(prob, R_true, t_true, d_true, a_true, b_true, iters=iters)
+    # per-host restatement (the reference's single-host model, no affine): reference = keyframe h,
+    # targets = the others at the relative poses T_t T_h^-1, the points hosted in h
+    hst, htrue = [], []
+    for h in range(KF):
+        sel = host == h
+        others = [f for f in range(KF) if f != h]
+        Rr0 = np.stack([R0[f] @ R0[h].T for f in others])
+        tr0 = np.stack([t0[f] - Rr0[i] @ t0[h] for i, f in enumerate(others)])
+        Rrt = np.stack([R_true[f] @ R_true[h].T for f in others])
+        trt = np.stack([t_true[f] - Rrt[i] @ t_true[h] for i, f in enumerate(others)])
+        st = ProblemState(ref=L[h].astype(np.float32), ref_K=K, targets=np.stack([L[f] for f in others]).astype(np.float32),
+                          targets_K=np.tile(np.array(K), (KF - 1, 1)), R=Rr0, t=tr0, anchors_px=anchors[sel].copy(),
+                          inv_depths=d0[sel].copy(), pattern=pat)
+        hst.append(st)
+        htrue.append((Rrt, trt, d_true[sel].copy()))
+    return RoomWindow(win, hst, htrue)

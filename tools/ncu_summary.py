@@ -55,9 +55,10 @@ def full(path):
     res = []
     for vals in rows[2:]:
         d = {"kernel": vals[hdr.index("Kernel Name")][:80]}
-        for k in KEYS:
-            if k in hdr:
-                d[k] = f"{vals[hdr.index(k)]} {units[hdr.index(k)]}".strip()
+        for i, k in enumerate(hdr):  # the listed counters plus every FP64 / DMMA / tensor-pipe counter
+            if k in KEYS or any(t in k for t in ("dmma", "pipe_fp64", "pipe_tensor", "fp64")):
+                if vals[i] not in ("", "n/a"):
+                    d[k] = f"{vals[i]} {units[i]}".strip()
         res.append(d)
     return res
 

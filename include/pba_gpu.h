@@ -131,6 +131,11 @@ int pba_perturb_parameters(int32_t F, double* R, double* t, int32_t N, double* d
 /* ---- handle lifecycle: IcSolver(ProblemState, SolverConfig) solver.hpp:117,
    FcSolver(ProblemState, SolverConfig) solver.hpp:176.  Uploads the problem. */
 int pba_gpu_create(const pba_problem* problem, pba_handle** out);
+/* As pba_gpu_create, but it returns without waiting for the tail of the target-image upload: the
+   caller keeps problem->targets[*].data valid until the first call on the handle that reads them
+   (energy, ic_build, ic_run / fc_run, ic_begin / fc_begin, fc_build) returns.  ic_solve / fc_solve
+   (solver.cpp:845-851) hold their ProblemState for the whole call, so they use this. */
+int pba_gpu_create_deferred(const pba_problem* problem, pba_handle** out);
 void pba_gpu_destroy(pba_handle* h);
 const char* pba_gpu_last_error(const pba_handle* h);
 int64_t pba_gpu_num_observations(const pba_handle* h);   /* N_obs */
@@ -255,6 +260,13 @@ enum { PBA_X_GATHER = 0, PBA_X_SUM_I64 = 1 };
 typedef int (*pba_exchange_fn)(void* ctx, int op, void* send, void* recv, int64_t count, void* stream);
 int pba_gpu_set_exchange(pba_handle* h, int32_t rank, int32_t world, int64_t num_points_total,
                          pba_exchange_fn fn, void* ctx);
+/* The same exchange issued by the library itself over NCCL (no callback per candidate): rank 0 draws a
+   128-byte ncclUniqueId with pba_gpu_nccl_unique_id, the caller distributes it (any channel), and
+   every rank attaches its handle; the all-gathers and the int64 sum then run on the handle's stream.
+   NCCL is loaded with dlopen on first use (PBA_E_CUDA when absent). */
+int pba_gpu_nccl_unique_id(void* id128);
+int pba_gpu_set_exchange_nccl(pba_handle* h, const void* id128, int32_t rank, int32_t world,
+                              int64_t num_points_total);
 
 /* ---- instrumentation ------------------------------------------------------- */
 void* pba_gpu_stream(pba_handle* h);                 /* the handle's cudaStream_t */

@@ -113,6 +113,9 @@ _COMMON = {
     "mh_fc_run": (C.c_int, [VP, P(pba_config), P(pba_report), P(f64), P(f64)]),
 }
 _GPU_ONLY = {
+    "create_deferred": (C.c_int, [P(pba_problem), P(VP)]),
+    "nccl_unique_id": (C.c_int, [VP]),
+    "set_exchange_nccl": (C.c_int, [VP, VP, i32, i32, i64]),
     "ic_begin": (C.c_int, [VP, P(pba_config)]),
     "fc_begin": (C.c_int, [VP, P(pba_config)]),
     "iterate": (C.c_int, [VP, P(pba_iter_stats), P(C.c_int)]),

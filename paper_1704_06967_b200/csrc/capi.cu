@@ -88,12 +88,12 @@ void pba_config_default(pba_config* c) {  // SolverConfig{} (solver.hpp:45-54)
   c->record_snapshots = 0;
 }
 
-int pba_gpu_create(const pba_problem* problem, pba_handle** out) {
+static int create_impl(const pba_problem* problem, pba_handle** out, bool deferred) {
   if (!out) return PBA_E_ARG;
   *out = nullptr;
   try {
     auto h = std::make_unique<pba_handle>();
-    h->e = std::make_unique<Engine>(problem);
+    h->e = std::make_unique<Engine>(problem, deferred);
     *out = h.release();
     return PBA_OK;
   } catch (const PbaError& ex) {
@@ -104,6 +104,8 @@ int pba_gpu_create(const pba_problem* problem, pba_handle** out) {
     return PBA_E_ARG;
   }
 }
+int pba_gpu_create(const pba_problem* problem, pba_handle** out) { return create_impl(problem, out, false); }
+int pba_gpu_create_deferred(const pba_problem* problem, pba_handle** out) { return create_impl(problem, out, true); }
 
 void pba_gpu_destroy(pba_handle* h) { delete h; }
 
@@ -224,6 +226,22 @@ int pba_gpu_normalize_gauge(pba_handle* h) {
 int pba_gpu_set_exchange(pba_handle* h, int32_t rank, int32_t world, int64_t num_points_total, pba_exchange_fn fn,
                          void* ctx) {
   return guarded(h, [&](Engine& e) { e.set_exchange(rank, world, num_points_total, fn, ctx); });
+}
+int pba_gpu_nccl_unique_id(void* id128) {
+  if (!id128) return PBA_E_ARG;
+  try {
+    pba_b200::nccl_unique_id(id128);
+    return PBA_OK;
+  } catch (const pba_b200::PbaError& e) {
+    return e.code;
+  } catch (...) {
+    return PBA_E_CUDA;
+  }
+}
+int pba_gpu_set_exchange_nccl(pba_handle* h, const void* id128, int32_t rank, int32_t world,
+                              int64_t num_points_total) {
+  if (!id128) return PBA_E_ARG;
+  return guarded(h, [&](Engine& e) { e.set_exchange_nccl(id128, rank, world, num_points_total); });
 }
 void* pba_gpu_stream(pba_handle* h) { return (h && h->e) ? static_cast<void*>(h->e->stream()) : nullptr; }
 int pba_gpu_set_profiling(pba_handle* h, int on) {

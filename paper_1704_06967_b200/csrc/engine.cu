@@ -117,7 +117,7 @@ void init_memory_pool() {
 // =====================================================================================
 // construction: upload the ProblemState (solver.hpp:33-43) into the device layout
 // =====================================================================================
-Engine::Engine(const pba_problem* p) {
+Engine::Engine(const pba_problem* p, bool deferred) {
   if (!p) throw PbaError(PBA_E_ARG, "null problem");
   if (p->num_frames < 0 || p->num_points < 0) throw PbaError(PBA_E_ARG, "negative sizes");
   if (p->pattern_size < 1 || p->pattern_size > 32 || !p->pattern)
@@ -157,25 +157,19 @@ Engine::Engine(const pba_problem* p) {
     frames_h_[f] = FrameD{images_.p + off[f + 1], im.width, im.height, im.fx, im.fy, im.cx, im.cy};
   }
   frames_.alloc(std::max(F_, 1));
+  if (F_ > 0)
+    ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, stream_), "frames");
   // target images go up on a second stream once the observation list and anchors are up
   // (they gate the layout build), so the image upload overlaps the layout build
-  struct UploadRes {  // released on every exit path (constructor errors included)
-    cudaStream_t up = nullptr;
-    cudaEvent_t up_done = nullptr, obs_up = nullptr;
-    ~UploadRes() {
-      if (up) {
-        cudaStreamSynchronize(up);
-        cudaStreamDestroy(up);
-      }
-      if (up_done) cudaEventDestroy(up_done);
-      if (obs_up) cudaEventDestroy(obs_up);
-    }
-  } ur;
-  ck(cudaStreamCreateWithFlags(&ur.up, cudaStreamNonBlocking), "upload stream");
-  ck(cudaEventCreateWithFlags(&ur.up_done, cudaEventDisableTiming), "upload event");
-  ck(cudaEventCreateWithFlags(&ur.obs_up, cudaEventDisableTiming), "obs upload event");
-  cudaStream_t up = ur.up;
-  cudaEvent_t up_done = ur.up_done, obs_up = ur.obs_up;
+  ck(cudaStreamCreateWithFlags(&up_stream_, cudaStreamNonBlocking), "upload stream");
+  ck(cudaEventCreateWithFlags(&img_done_, cudaEventDisableTiming), "upload event");
+  cudaEvent_t obs_up = nullptr;
+  ck(cudaEventCreateWithFlags(&obs_up, cudaEventDisableTiming), "obs upload event");
+  struct EvRes {
+    cudaEvent_t& e;
+    ~EvRes() { if (e) cudaEventDestroy(e); }
+  } obs_res{obs_up};
+  cudaStream_t up = up_stream_;
   auto upload_targets = [&]() {
     ck(cudaEventRecord(obs_up, stream_), "obs upload record");
     ck(cudaStreamWaitEvent(up, obs_up, 0), "obs upload wait");
@@ -183,9 +177,8 @@ Engine::Engine(const pba_problem* p) {
       ck(cudaMemcpyAsync(images_.p + off[f + 1], p->targets[f].data, (off[f + 2] - off[f + 1]) * sizeof(float),
                          cudaMemcpyHostToDevice, up),
          "upload target");
-    if (F_ > 0)
-      ck(cudaMemcpyAsync(frames_.p, frames_h_.data(), F_ * sizeof(FrameD), cudaMemcpyHostToDevice, up), "frames");
-    ck(cudaEventRecord(up_done, up), "upload record");
+    ck(cudaEventRecord(img_done_, up), "upload record");
+    images_pending_ = true;
   };
 
   build_layout(p, upload_targets);
@@ -252,14 +245,28 @@ Engine::Engine(const pba_problem* p) {
   t_state_.assign(p->pose_t, p->pose_t + 3 * F_);
   set_params(p->pose_R, p->pose_t, p->inv_depths);
   trace_mark(stream_, "create: buffers+tval+params");
-  // the caller's image buffers are free once create returns: finish the upload here
-  ck(cudaStreamWaitEvent(stream_, up_done, 0), "upload wait");
-  ck(cudaEventSynchronize(up_done), "upload sync");
+  if (!deferred) {  // the caller's image buffers are free once create returns: finish the upload here
+    ensure_images();
+    ck(cudaEventSynchronize(img_done_), "upload sync");
+  }
   trace_mark(stream_, "create: image upload tail");
+}
+
+// Order the handle's stream after the whole target-image upload (deferred handles: before the
+// first work that reads the images; the stream syncs of that call then also complete the upload).
+void Engine::ensure_images() {
+  if (!images_pending_) return;
+  ck(cudaStreamWaitEvent(stream_, img_done_, 0), "upload wait");
+  images_pending_ = false;
 }
 
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
+  if (up_stream_) {
+    cudaStreamSynchronize(up_stream_);
+    cudaStreamDestroy(up_stream_);
+  }
+  if (img_done_) cudaEventDestroy(img_done_);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto& pd : pending_) {
     cudaEventDestroy(pd.a);
@@ -280,7 +287,7 @@ Engine::~Engine() {
 int64_t Engine::device_bytes() const {  // every device buffer the handle holds
   int64_t b = 0;
   auto add = [&b](const auto&... bufs) { ((b += static_cast<int64_t>(bufs.bytes())), ...); };
-  add(images_, frames_, anchor_, anchor_fm_, tval_, tgrad_, pm_ptr_, fm_ptr_, tile_q0_, tile_q1_, pm_frame_, pm2fm_,
+  add(images_, frames_, anchor_, anchor_fm_, tval_, tgrad_, pm_ptr_, fm_ptr_, tile_q0_, tile_q1_, pm_frame_, pm2fm_, fm2pm_,
       fm_point_, tile_frame_, ftile_ptr_, tile_order_, uo2q_d_, perm_d_, zero_idx_, perm_tmp_, pose_state_,
       pose_cur_, pose_cand_, pose0_, d_state_, d_cur_, d_cand_, d0_, scratch_bits_, J_, Bic_, Dic_, Hic_, Bpm_,
       rec_, rec_g_, gfix_, gscale_, s_n_, dx_n_, xp_, g_tmp_, r_out_, partial_, partial_cf_, partial_bs_, partial_pt_, partial_mr_,
@@ -465,6 +472,7 @@ void Engine::set_exchange(int rank, int world, int64_t n_total, pba_exchange_fn 
   if (fn && (world < 1 || rank < 0 || rank >= world || n_total < N_))
     throw PbaError(PBA_E_ARG, "set_exchange: need 0 <= rank < world and num_points_total >= this shard's points");
   xch_ = Xch{};
+  xch_owner_.reset();
   if (!fn) return;
   xch_ = Xch{rank, world, n_total, fn, ctx};
   cf_.alloc(6 * static_cast<size_t>(std::max(F_, 1)));
@@ -568,6 +576,7 @@ void Engine::finalize(const double* partial, const double* partial_cf, bool bs, 
 // =====================================================================================
 void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, double* residuals, uint8_t* active) {
   check_template();
+  ensure_images();
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose_state_.p;
   a.active_out = scratch_bits_.p;
@@ -923,8 +932,12 @@ void Engine::ic_build(const pba_config* cfg) {
   a.active_out = mask_[0].p;
   a.Jmw = J_.p;
   a.B_out = Bic_.p;
+  Bpm_.alloc(6 * nO);
+  a.Bpm_out = Bpm_.p;  // point-major copy written by the pass itself
+  a.fm2pm = fm2pm_.p;
   fuse_dense(a);
   trace_mark(stream_, "ic_build: setup+alloc");
+  ensure_images();
   auto e = ev_begin(PBA_K_IC_BUILD);
   launch_obs(OBS_BUILD, a, stream_);
   ev_end(PBA_K_IC_BUILD, e);
@@ -938,11 +951,8 @@ void Engine::ic_build(const pba_config* cfg) {
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, nullptr, false, false, true, nullptr, nullptr, nullptr, Hic_.p, true);
   trace_mark(stream_, "ic_build: D pass");
-  Bpm_.alloc(6 * nO);
   alloc_schur();
-  trace_mark(stream_, "ic_build: Bpm+schur alloc");
-  launch_b_to_pm(ov_, Bic_.p, Bpm_.p, stream_);
-  trace_mark(stream_, "ic_build: B point-major copy");
+  trace_mark(stream_, "ic_build: schur alloc");
   const Status s = read_status();
   if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");  // :275
   ic_.mcur = 0;

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -85,7 +86,9 @@ struct SolverState {
 
 class Engine {
  public:
-  explicit Engine(const pba_problem* p);
+  // deferred: the target images may still be in flight when the constructor returns; the caller keeps
+  // them valid until the first call that reads them returns (pba_gpu_create_deferred)
+  explicit Engine(const pba_problem* p, bool deferred = false);
   ~Engine();
 
   // ---- C ABI operations (see include/pba_gpu.h) ----
@@ -125,6 +128,8 @@ class Engine {
 
   // point-sharded runs (pba_gpu_set_exchange)
   void set_exchange(int rank, int world, int64_t n_total, pba_exchange_fn fn, void* ctx);
+  // in-library NCCL exchange (nccl_exchange.cu): a communicator from a ncclUniqueId, collectives on stream_
+  void set_exchange_nccl(const void* id128, int rank, int world, int64_t n_total);
 
   // make this engine's stream the allocation stream of the calling thread (every C-ABI entry)
   void bind() const { set_alloc_stream(stream_); }
@@ -159,7 +164,7 @@ class Engine {
   DBuf<double> tval_;             // template values N*P
   DBuf<double4> tgrad_;           // template records {tval, gx, gy, 0} N*P (IC passes)
   DBuf<int64_t> pm_ptr_, fm_ptr_, tile_q0_, tile_q1_;
-  DBuf<int32_t> pm_frame_, pm2fm_, fm_point_, tile_frame_, ftile_ptr_, tile_order_;
+  DBuf<int32_t> pm_frame_, pm2fm_, fm2pm_, fm_point_, tile_frame_, ftile_ptr_, tile_order_;
   DBuf<int32_t> uo2q_d_;         // caller obs -> frame-major obs q
   DBuf<int32_t> perm_d_;         // internal point -> user point (device copy)
   DBuf<int32_t> zero_idx_;       // scratch: compacted user indices (+1 counter slot)
@@ -220,6 +225,10 @@ class Engine {
   std::vector<FrameTab> tabs_;    // IC pass frame tables (kernel parameters)
   int64_t tab_min_obs_ = int64_t(1) << 20;  // frame tables from this many observations on (env PBA_TAB_MIN_OBS)
   cudaStream_t side_ = nullptr;   // second stream for the IC pass frame chunks
+  cudaStream_t up_stream_ = nullptr;   // target-image upload (deferred handles: completes behind create)
+  cudaEvent_t img_done_ = nullptr;
+  bool images_pending_ = false;
+  void ensure_images();
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<int32_t> ftile_ptr_h_;  // host copy of ov_.ftile_ptr
   int* flags_h_ = nullptr;        // pinned
@@ -235,6 +244,7 @@ class Engine {
     pba_exchange_fn fn = nullptr;
     void* ctx = nullptr;
   } xch_;
+  std::shared_ptr<void> xch_owner_;  // state of an exchange the library owns (the NCCL communicator)
   struct XSeg {
     double* p;
     int n;

@@ -90,18 +90,35 @@ __global__ void k_fill_pm(int N, const int32_t* __restrict__ perm, const int64_t
   }
 }
 
+// four independent observations per thread and step: their dependent gathers (o -> n -> anchor)
+// are issued together instead of one chain at a time
 __global__ void k_fm_scatter(int64_t NO, const int32_t* __restrict__ fm2pm, const int32_t* __restrict__ pm_point,
                              const int32_t* __restrict__ pm2uo, const double2* __restrict__ anc,
                              int32_t* __restrict__ pm2fm, int32_t* __restrict__ fm_point, int32_t* __restrict__ uo2q,
                              double2* __restrict__ anchor_fm) {
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < NO;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int o = fm2pm[q];
-    const int n = pm_point[o];
-    pm2fm[o] = static_cast<int32_t>(q);
-    fm_point[q] = n;
-    uo2q[pm2uo[o]] = static_cast<int32_t>(q);
-    anchor_fm[q] = anc[n];
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q0 < NO; q0 += U * stride) {
+    int o[U], n[U], uo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      o[u] = q < NO ? __ldg(fm2pm + q) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      n[u] = __ldg(pm_point + o[u]);
+      uo[u] = __ldg(pm2uo + o[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      if (q >= NO) break;
+      pm2fm[o[u]] = static_cast<int32_t>(q);
+      fm_point[q] = n[u];
+      uo2q[uo[u]] = static_cast<int32_t>(q);
+      anchor_fm[q] = __ldg(anc + n[u]);
+    }
   }
 }
 
@@ -293,7 +310,8 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
 
   trace_mark(s, "layout: point-major list");
   // ---- frame-major list (stable radix sort of observations by frame) ----
-  DBuf<int32_t> frames_sorted, iota_o, fm2pm;
+  DBuf<int32_t> frames_sorted, iota_o;
+  DBuf<int32_t>& fm2pm = fm2pm_;  // kept: the IC build writes the point-major B blocks through it
   frames_sorted.alloc(nO);
   iota_o.alloc(nO);
   fm2pm.alloc(nO);
@@ -314,8 +332,8 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
     trace_mark(s, "layout:   iota");
     radix_sort_pairs(pm_frame_.p, frames_sorted.p, iota_o.p, fm2pm.p, NO_, bits_for(F_), s);
     trace_mark(s, "layout:   frame sort");
-    k_fm_scatter<<<grid_for(NO_), 256, 0, s>>>(NO_, fm2pm.p, pm_point.p, pm2uo.p, anchor_.p, pm2fm_.p, fm_point_.p,
-                                               uo2q_d_.p, anchor_fm_.p);
+    k_fm_scatter<<<grid_for((NO_ + 3) / 4), 256, 0, s>>>(NO_, fm2pm.p, pm_point.p, pm2uo.p, anchor_.p, pm2fm_.p,
+                                                         fm_point_.p, uo2q_d_.p, anchor_fm_.p);
     count_launches(1);
   }
   trace_mark(s, "layout: frame-major sort+scatter");

@@ -206,6 +206,7 @@ void Engine::fc_rescale_rhs(int buf, double lambda) {
 
 void Engine::fc_build(double gamma, double* pp, double* dd, double* pd, double* g) {
   check_template();
+  ensure_images();
   alloc_fc();
   fc_eval(gamma, pose_state_.p, d_state_.p, 0, 1.0, nullptr, nullptr);
   (void)read_status();
@@ -389,6 +390,7 @@ void Engine::begin(bool ic, const pba_config* cfg) {
       pba_config_default(&run_.cfg);
     }
     check_template();
+    ensure_images();
     alloc_fc();
     if (F_ > 0) ck(cudaMemcpyAsync(pose_cur_.p, pose_state_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p");
     if (N_ > 0) ck(cudaMemcpyAsync(d_cur_.p, d_state_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d");

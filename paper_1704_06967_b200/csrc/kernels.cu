@@ -741,6 +741,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       if constexpr (kH) {
 #pragma unroll
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
+        if (MODE == OBS_BUILD && a.Bpm_out) {  // the point-major copy k_backsub streams
+          double2* dst = reinterpret_cast<double2*>(a.Bpm_out + static_cast<int64_t>(__ldg(a.fm2pm + q)) * 6);
+          dst[0] = make_double2(b6[0], b6[1]);
+          dst[1] = make_double2(b6[2], b6[3]);
+          dst[2] = make_double2(b6[4], b6[5]);
+        }
         if (a.B_dense) {  // the Schur chunk row slot of (n, f): 16-byte aligned (rows are 64-double multiples)
           double2* dst = reinterpret_cast<double2*>(a.B_dense + a.dense_row[n] + 6 * f);
           dst[0] = make_double2(b6[0], b6[1]);
@@ -1547,7 +1553,7 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
                                                            const double* __restrict__ scale,
                                                            unsigned long long* __restrict__ acc) {
   extern __shared__ __align__(16) double sy_smem[];
-  // blocks[b] = {chunk id, 0, 0, rb | cb << 16}
+  // blocks[b] = {chunk id, valid columns V (unused here), 0, rb | cb << 16}
   const int4 blk = blocks[blockIdx.x];
   const int4 ch = chunks[blk.x];
   const int p0 = ch.x, p1 = ch.y, fmin = ch.z, LD = ch.w;
@@ -1610,7 +1616,8 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(accd[i][j][0], accd[i][j][1], a[i], b[j]);
+          for (int j = 0; j < 4; ++j)
+            dmma_8x8x4(accd[i][j][0], accd[i][j][1], a[i], b[j]);
       }
     }
     __syncthreads();  // the stage is overwritten by the next issue

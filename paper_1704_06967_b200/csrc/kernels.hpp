@@ -51,6 +51,8 @@ struct ObsArgs {
   const double* d0;            // N: frozen depths of the IC build (IC / REFRESH)
   double* B_out;               // NO*6 (FC/BUILD/REFRESH)
   double* B_dense;             // or null: also scatter b_n into the Schur chunk rows (SchurPlan::dense)
+  double* Bpm_out;             // or null: also write b_n point-major (at fm2pm[q]; the IC build: no k_b_to_pm)
+  const int32_t* fm2pm;
   const int64_t* dense_row;    // N: offset of point n's chunk row minus 6 fmin (slot of frame f at + 6 f)
   double2* rec;                // NO: {sum_k Jd w r, sum_k w Jd^2}
   double* rec_g;               // NO or null: IC pass g_n terms only (sum_k Jd w r)
@@ -281,6 +283,7 @@ void launch_tri_inverse(const double* L, int n, double* Dinv, double* X, double*
 void launch_chol_tiles(double* S, int n, double* Dinv, double* X, double* XT, int* flags, int epoch, int* fail,
                        cudaStream_t s);
 int chol_tile_flags(int n);
+void nccl_unique_id(void* out128);  // nccl_exchange.cu
 void launch_trisolve(const double* X, const double* XT, int n, const double* b, double* y, double* x,
                      int* nonfinite, cudaStream_t s);
 

@@ -190,6 +190,30 @@ class TorchExchange(Exchange):
         return t.numpy()
 
 
+class NcclLibExchange:
+    """The exchange issued by libpba_gpu.so itself over NCCL (pba_gpu_set_exchange_nccl): the ranks only
+    share a 128-byte ncclUniqueId here (broadcast from rank 0 over torch.distributed, any backend);
+    every later collective runs inside the library on the handle's stream, with no callback."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.error: Optional[BaseException] = None
+        self.calls = 0
+        self._id = None
+
+    def attach(self, h: Handle, num_points_total: int) -> None:
+        if self._id is None:
+            buf = C.create_string_buffer(128)
+            if self.rank == 0:
+                h._check(h.b.nccl_unique_id(buf))
+            obj = [bytes(buf.raw) if self.rank == 0 else None]
+            self.dist.broadcast_object_list(obj, src=0, group=self.group)
+            self._id = C.create_string_buffer(obj[0], 128)
+        h._check(h.b.set_exchange_nccl(h.h, self._id, self.rank, self.world, int(num_points_total)))
+
+
 class _Rendezvous:
     """Host rendezvous of the shards of one process (one thread per shard)."""
 
@@ -312,11 +336,13 @@ def solve_threads(state: ProblemState, config: SolverConfig, world: int, solver:
 
 
 def solve_distributed(state: ProblemState, config: SolverConfig, solver: str = "ic", group=None,
-                      gather: bool = True) -> SolveReport:
+                      gather: bool = True, exchange: str = "torch") -> SolveReport:
     """One rank's part of a point-sharded solve under torch.distributed (one process per GPU).
-    Returns the merged report on every rank when `gather`, else this rank's report (local depths)."""
+    Returns the merged report on every rank when `gather`, else this rank's report (local depths).
+    exchange: "torch" (torch.distributed collectives through the callback: NCCL on the handle's
+    stream, or gloo via the host) or "nccl-lib" (the library's own NCCL communicator)."""
     import torch.distributed as dist
-    x = TorchExchange(group)
+    x = NcclLibExchange(group) if exchange == "nccl-lib" else TorchExchange(group)
     sh = shard_problem(state, x.rank, x.world)
     h = Handle(sh.state, "gpu")
     try:

@@ -286,15 +286,18 @@ class WarningList(_abc.Sequence):
 class Handle:
     """One uploaded problem: on the product library ("gpu") or on a checker library object."""
 
-    def __init__(self, state: ProblemState, backend="gpu"):
+    def __init__(self, state: ProblemState, backend="gpu", deferred: bool = False):
+        """deferred (product library only): pba_gpu_create_deferred - the target images may still be
+        uploading when this returns; the state's arrays stay referenced by the handle until it is closed."""
         self.b = capi.backend(backend)
         self.backend = self.b.kind
         self.F, self.N = state.num_frames, state.num_points
         self.P = int(np.asarray(state.pattern).reshape(-1, 2).shape[0])
         p, keep = state._c()
         h = C.c_void_p()
-        rc = self.b.create(C.byref(p), C.byref(h))
-        del keep
+        deferred = deferred and self.backend == "gpu"
+        rc = (self.b.create_deferred if deferred else self.b.create)(C.byref(p), C.byref(h))
+        self._keep = (keep, p) if deferred else None
         if rc != capi.PBA_OK:
             err = self.b.last_error(None) if self.backend == "gpu" else b""
             _raise(rc, (err or b"").decode())
@@ -565,8 +568,9 @@ class FcSolver:
 
 
 def ic_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu") -> SolveReport:
-    """ic_solve (solver.cpp:845-847)."""
-    h = Handle(state, backend)
+    """ic_solve (solver.cpp:845-847).  The state is held for the whole call, so the handle is created
+    deferred (create does not wait for the tail of the image upload)."""
+    h = Handle(state, backend, deferred=True)
     try:
         return h.ic_run(config or SolverConfig())
     finally:
@@ -575,7 +579,7 @@ def ic_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend
 
 def fc_solve(state: ProblemState, config: Optional[SolverConfig] = None, backend="gpu") -> SolveReport:
     """fc_solve (solver.cpp:849-851)."""
-    h = Handle(state, backend)
+    h = Handle(state, backend, deferred=True)
     try:
         return h.fc_run(config or SolverConfig())
     finally:

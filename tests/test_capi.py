@@ -37,7 +37,8 @@ def test_library_exports_every_declared_symbol():
 def test_oracle_mirrors_the_gpu_call_set():
     lib = ctypes.CDLL(str(ORACLE_LIB))
     gpu_only = {"stream", "set_profiling", "kernel_times", "device_bytes", "ic_begin", "fc_begin", "iterate", "end",
-                "launch_count", "set_exchange"}
+                "launch_count", "set_exchange", "nccl_unique_id", "set_exchange_nccl",  # multi-process plumbing
+                "create_deferred"}
     for n in declared():
         if n.startswith("pba_gpu_") and n[len("pba_gpu_"):] not in gpu_only:
             assert hasattr(lib, "pba_oracle_" + n[len("pba_gpu_"):]), n

@@ -439,3 +439,18 @@ def test_ic_run_refresh_hessian_matches_oracle(c1):  # refresh_ic_hessian (solve
     rg, ro = g.ic_run(cfg), o.ic_run(cfg)
     assert rg.hessian_builds == ro.hessian_builds and rg.hessian_builds > 1
     _compare_runs(rg, ro, st.num_frames, st.num_points)
+
+
+@pytest.mark.parametrize("solver_kind", ["ic", "fc"])
+def test_deferred_create_is_bitwise_the_plain_create(c1, solver_kind):
+    """pba_gpu_create_deferred (ic_solve / fc_solve): every result is bitwise the plain handle's."""
+    st = c1.state
+    cfg = c1.cfg.solver_config(max_iters=4)
+    a = Handle(st, "gpu", deferred=True)
+    b = Handle(st, "gpu")
+    ra = a.ic_run(cfg) if solver_kind == "ic" else a.fc_run(cfg)
+    rb = b.ic_run(cfg) if solver_kind == "ic" else b.fc_run(cfg)
+    assert ra.final_energy == rb.final_energy and [s.energy for s in ra.iters] == [s.energy for s in rb.iters]
+    assert np.array_equal(ra.final_inv_depths, rb.final_inv_depths) and np.array_equal(ra.final_t, rb.final_t)
+    e = Handle(st, "gpu", deferred=True).energy(c1.cfg.huber_delta)  # energy as the first call
+    assert e.energy == b.energy(c1.cfg.huber_delta).energy

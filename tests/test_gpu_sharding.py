@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -117,3 +118,50 @@ def test_sharded_warnings_match_the_single_process_solve(c1, world):
     assert len(one.warnings) == 1 + int((~keep).sum())
     rg = sharding.solve_threads(st, cfg, world, "ic")
     assert list(rg.warnings) == list(one.warnings)
+
+
+def test_two_process_gloo_sharded_solve_matches_oracle(tmp_path):
+    """a full point-sharded IC and FC solve by two PROCESSES (torch.distributed,
+    gloo, world size 2) on one GPU, merged and compared with the oracle's single-process solve."""
+    import json
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    worker = Path(__file__).resolve().parent / "mp_sharded_worker.py"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(worker), str(tmp_path)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    res = json.loads((tmp_path / "rank0.json").read_text())
+    for kind in ("ic", "fc"):
+        r = res[kind]
+        assert r["world"] == 2 and r["control_flow_and_energies"], r
+        assert r["params"] is True, r
+        assert r["warnings_equal"], r
+
+
+def test_library_nccl_exchange_world1_is_bitwise_the_single_process_solve(c1):
+    """pba_gpu_set_exchange_nccl: the library's own NCCL communicator (collectives on the handle's
+    stream, no callback per candidate) at world size 1 reproduces the single-process solve bitwise."""
+    import torch
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        st = c1.state
+        cfg = c1.cfg.solver_config(max_iters=4)
+        for kind in ("ic", "fc"):
+            rg = sharding.solve_distributed(st, cfg, kind, exchange="nccl-lib")
+            h = Handle(st, "gpu")
+            ref = h.ic_run(cfg) if kind == "ic" else h.fc_run(cfg)
+            _runs_equal_bitwise(rg, ref)
+    finally:
+        dist.destroy_process_group()

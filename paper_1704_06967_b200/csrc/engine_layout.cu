@@ -365,9 +365,9 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
   // The Schur chunk plan goes first: its device sort, key download and host chunking overlap the
   // target-image upload; the small host->device copies of both plans queue behind that upload.
   // ---- Schur chunk plan: points sorted by visibility window (first frame, last frame) and cut
-  //      greedily into chunks whose union window keeps the padded width LD = roundup(6 W, 64) of
-  //      the chunk's first window (so merging windows costs no extra DMMA columns), up to
-  //      kMaxChunk points; one work item per 64x64 upper tile-block of each chunk's window.
+  //      greedily into chunks whose union window keeps the padded width LD = roundup(6 W, kSchurTB)
+  //      of the chunk's first window (so merging windows costs no extra DMMA columns), up to
+  //      kMaxChunk points; one work item per kSchurTB^2 upper tile-block of each chunk's window.
   //      Long chunks mean long K loops and few fixed-point folds of each tile into S. ----
   {
     const int kMaxChunk = [] {
@@ -396,7 +396,7 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
       int64_t total = 0;
       for (int p = 0; p < npts;) {
         int fmin = static_cast<int>(keys[p] >> 16), fmax = static_cast<int>(keys[p] & 0xffffu);
-        const int LD = ((6 * (fmax - fmin + 1) + 63) / 64) * 64;
+        const int LD = ((6 * (fmax - fmin + 1) + kSchurTB - 1) / kSchurTB) * kSchurTB;
         int q = p + 1;
         while (q < npts && q - p < kMaxChunk) {
           const int a0 = std::min(fmin, static_cast<int>(keys[q] >> 16));
@@ -406,7 +406,7 @@ void Engine::build_layout(const pba_problem* p, const std::function<void()>& aft
           fmax = a1;
           ++q;
         }
-        const int nb = LD / 64;
+        const int nb = LD / kSchurTB;
         if (nb > 0xffff) throw PbaError(PBA_E_ARG, "Schur chunk window too large");
         const int c = static_cast<int>(chunks.size());
         chunks.push_back(make_int4(p, q, fmin, LD));

@@ -1488,10 +1488,13 @@ __global__ void __launch_bounds__(NT) k_schur_pts(const ObsView ov, const double
 // Chunked dense Schur update on the FP64 tensor path (DMMA, mma.sync.m8n8k4.f64).
 // Points are sorted by visibility window and cut into chunks; a chunk's scaled blocks
 // b_n / sqrt(D_n + lambda) form a dense [points x 6W] matrix over its frame window, and
-// one CTA computes one 64x64 tile-block of its Gram matrix (upper triangle of tile-blocks),
-// K-looping over the chunk's points through shared memory.  8 warps x 8 DMMA 8x8 tiles.
+// one CTA computes one SCH_TB x SCH_TB tile-block of its Gram matrix (upper triangle of tile-blocks),
+// K-looping over the chunk's points through shared memory.  4 warps x SY_NT^2 DMMA 8x8 tiles.
 // Results enter S through the same deterministic fixed-point RED as k_schur_pts.
-constexpr int SCH_TB = 64;   // tile-block edge (window-local dimensions)
+constexpr int SCH_TB = kSchurTB;      // tile-block edge (window-local dimensions)
+constexpr int SY_NT = PBA_SY_NT;      // 8x8 DMMA tiles per warp-quadrant side
+constexpr int SY_QW = 8 * SY_NT;      // warp-quadrant edge
+constexpr int SY_PPR = SCH_TB / 2;    // 16-byte pieces per chunk row of a tile-block
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -1500,7 +1503,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 // Densify once per B (independent of D and lambda): row p of chunk c = b_n^T over the chunk's
-// frame window (zero where the point does not observe a frame), LD_c = roundup(6 W_c, 64).
+// frame window (zero where the point does not observe a frame), LD_c = roundup(6 W_c, SCH_TB).
 __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const double* __restrict__ B,
                                                        const int32_t* __restrict__ chunk_pts, int npts,
                                                        const int32_t* __restrict__ chunk_of,
@@ -1523,12 +1526,12 @@ __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const d
   }
 }
 
-// One 64x64 upper tile-block of a chunk's weighted Gram matrix  sum_p w_p a_p a_p^T  on DMMA.
-// 4 warps, each a 32x32 quadrant (4x4 DMMA 8x8 tiles, 32 fp64 accumulators per lane); the
+// One SCH_TB x SCH_TB upper tile-block of a chunk's weighted Gram matrix  sum_p w_p a_p a_p^T  on DMMA.
+// 4 warps, each an SY_QW x SY_QW quadrant (SY_NT^2 DMMA 8x8 tiles, 2 SY_NT^2 fp64 accumulators per lane); the
 // K loop streams SY_KB points per stage into shared memory with cp.async (2 stages,
 // zero-filled past the chunk end); the weight w_p = 1/(D_n + lambda) scales the A fragment.
 constexpr int SY_KB = 32;      // points per stage
-constexpr int SY_LDS = 68;     // smem row stride (doubles): 68 = 4 mod 16 puts the 4 k-rows of a half-warp fragment load on distinct banks (2 wavefronts)
+constexpr int SY_LDS = SCH_TB + 4;  // smem row stride (doubles): = 4 mod 16 puts the 4 k-rows of a half-warp fragment load on distinct banks (2 wavefronts)
 constexpr int SY_STAGES = 2;
 constexpr int SY_THREADS = 128;
 constexpr size_t SY_SMEM = static_cast<size_t>(SY_STAGES) * (2 * SY_KB * SY_LDS + SY_KB) * sizeof(double);
@@ -1570,13 +1573,14 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
   auto issue = [&](int stage, int pb) {
     double* as = As + stage * SY_KB * SY_LDS;
     double* bs = Bs + stage * SY_KB * SY_LDS;
-    // KB rows x 32 16-byte pieces for each of A and B
+    // KB rows x SY_PPR 16-byte pieces for each of A and B
+    static_assert((2 * SY_KB * SY_PPR) % SY_THREADS == 0, "whole pieces per thread");
 #pragma unroll
-    for (int it = 0; it < (2 * SY_KB * 32) / SY_THREADS; ++it) {
+    for (int it = 0; it < (2 * SY_KB * SY_PPR) / SY_THREADS; ++it) {
       const int idx = tid + it * SY_THREADS;
-      const int isb = idx >= SY_KB * 32;
-      const int j = idx - isb * SY_KB * 32;
-      const int pp = j >> 5, piece = j & 31;
+      const int isb = idx >= SY_KB * SY_PPR;
+      const int j = idx - isb * SY_KB * SY_PPR;
+      const int pp = j / SY_PPR, piece = j % SY_PPR;
       const bool valid = pb + pp < p1;
       const double* src = base + static_cast<int64_t>(valid ? pb - p0 + pp : 0) * LD + (isb ? c0 : r0) + 2 * piece;
       cp_async16((isb ? bs : as) + pp * SY_LDS + 2 * piece, src, valid);
@@ -1584,11 +1588,11 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
     if (tid < SY_KB) cp_async8(Ws + stage * SY_KB + tid, wsort + min(pb + tid, p1 - 1), pb + tid < p1);
     cp_async_commit();
   };
-  double accd[4][4][2];
+  double accd[SY_NT][SY_NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < SY_NT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) accd[i][j][0] = accd[i][j][1] = 0.0;
+    for (int j = 0; j < SY_NT; ++j) accd[i][j][0] = accd[i][j][1] = 0.0;
   const int nsb = (p1 - p0 + SY_KB - 1) / SY_KB;
   if (nsb > 0) issue(0, p0);
   for (int sb = 0; sb < nsb; ++sb) {
@@ -1601,22 +1605,22 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
     }
     __syncthreads();
     if (active) {
-      const double* as = As + stage * SY_KB * SY_LDS + wr * 32 + (lane >> 2);
-      const double* bs = Bs + stage * SY_KB * SY_LDS + wc * 32 + (lane >> 2);
+      const double* as = As + stage * SY_KB * SY_LDS + wr * SY_QW + (lane >> 2);
+      const double* bs = Bs + stage * SY_KB * SY_LDS + wc * SY_QW + (lane >> 2);
       const double* ws = Ws + stage * SY_KB;
 #pragma unroll
       for (int kk = 0; kk < SY_KB; kk += 4) {
         const int k = kk + (lane & 3);
         const double w = ws[k];
-        double a[4], b[4];
+        double a[SY_NT], b[SY_NT];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = as[k * SY_LDS + 8 * i] * w;
+        for (int i = 0; i < SY_NT; ++i) a[i] = as[k * SY_LDS + 8 * i] * w;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = bs[k * SY_LDS + 8 * j];
+        for (int j = 0; j < SY_NT; ++j) b[j] = bs[k * SY_LDS + 8 * j];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < SY_NT; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < SY_NT; ++j)
             dmma_8x8x4(accd[i][j][0], accd[i][j][1], a[i], b[j]);
       }
     }
@@ -1627,13 +1631,13 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
   const int ld = 6 * ov.F;
   const int gbase = 6 * fmin;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < SY_NT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < SY_NT; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int lr = r0 + wr * 32 + 8 * i + (lane >> 2);
-        const int lc = c0 + wc * 32 + 8 * j + (lane & 3) * 2 + h;
+        const int lr = r0 + wr * SY_QW + 8 * i + (lane >> 2);
+        const int lc = c0 + wc * SY_QW + 8 * j + (lane & 3) * 2 + h;
         if (lr > lc || lc >= LD) continue;  // padded rows/cols are zero
         const int r = gbase + lr, c = gbase + lc;
         if (c >= ld) continue;

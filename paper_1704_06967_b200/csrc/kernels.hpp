@@ -72,6 +72,10 @@ void launch_obs(int mode, const ObsArgs& a, cudaStream_t s);
 #ifndef PBA_IC_V2
 #define PBA_IC_V2 1  // IC pass: gradient accumulated in the frame-factored form (see kernels.cu obs_lane_body)
 #endif
+#ifndef PBA_SY_NT
+#define PBA_SY_NT 3  // Schur SYRK: 8x8 DMMA tiles per warp-quadrant side (tile-block edge 16 * PBA_SY_NT)
+#endif
+constexpr int kSchurTB = 16 * PBA_SY_NT;  // Schur chunk rows are padded to multiples of this (48: 6 W = 240 at C4 fits exactly)
 // IC-pass frame record.  With PBA_TAB_SCALED the candidate pose's first two rows (R and t) are
 // pre-multiplied by fx and fy, so the warped pixel is u = (fx v_x) / v_z + cx, and (fsx, fsy) hold
 // the in-margin bounds (W - 3, H - 3) as doubles; otherwise pe is the plain pose and (fsx, fsy) = (fx, fy).

@@ -159,21 +159,26 @@ def fp64_peak():
 
 
 def ncu_profile_extra():
-    """Binding-resource evidence for the IC pass from the committed ncu capture."""
-    p = REPO / "profiles" / "r1_ncu_full_c4.json"
-    if not p.exists():
-        return None
-    try:
-        ks = [k for k in json.loads(p.read_text()) if "k_obs_lane_tab" in k["kernel"]]
-        if not ks:
-            return None
-        k = ks[0]
-        pick = lambda key: float(k[key].split()[0]) if key in k else None  # noqa: E731
-        return {"fp64_pipe_pct": pick("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-                "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                "dram_pct_of_theoretical": pick("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
-    except Exception:
-        return None
+    """Binding-resource evidence for the IC pass from the committed ncu capture of the current kernel
+    (SURVEY.md §8d): the FP64-pipe and issue utilisation (the pass rebuilds its rows, so these, not
+    the DRAM fraction, are what bound it)."""
+    for name in ("r2_ncu_full_ic_c4.json", "r1_ncu_full_c4.json"):
+        p = REPO / "profiles" / name
+        if not p.exists():
+            continue
+        try:
+            ks = [k for k in json.loads(p.read_text()) if "k_obs_lane_tab" in k["kernel"]]
+            if not ks:
+                continue
+            k = ks[0]
+            pick = lambda key: float(k[key].split()[0].replace(",", "")) if key in k else None  # noqa: E731
+            return {"source": f"profiles/{name}",
+                    "fp64_pipe_pct": pick("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                    "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "dram_pct_of_theoretical": pick("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+        except Exception:
+            continue
+    return None
 
 
 def ncu_traffic():
@@ -612,7 +617,10 @@ def main():
                      "launch_ms": obs_ms, "share_of_step": obs_ms / per_step_ms,
                      "canonical_B_IC_per_iter": bic, "canonical_effective_GBs": bic / (per_step_ms / 1e3) / 1e9,
                      "canonical_frac": bic / (per_step_ms / 1e3) / 1e9 / peak,
-                     "ncu": ncu_profile_extra(),
+                     "ncu": (nx := ncu_profile_extra()),
+                     # binding resource of the pass (it rebuilds its rows instead of streaming them)
+                     "fp64_pipe_frac": (nx["fp64_pipe_pct"] / 100.0 if nx and nx.get("fp64_pipe_pct") is not None
+                                        else None),
                      "note": "achieved = SURVEY 8d per-unit bytes of the IC pass (56 B/px J rows, K1 terms of B_IC) "
                              "/ launch time: an effective bandwidth, since the pass stores no rows and rebuilds them "
                              "from 32-byte per-(point, pixel) template records (so frac can exceed 1: the pass is faster "

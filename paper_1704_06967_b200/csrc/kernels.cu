@@ -1530,9 +1530,15 @@ __global__ void __launch_bounds__(256) k_schur_densify(const ObsView ov, const d
 // 4 warps, each an SY_QW x SY_QW quadrant (SY_NT^2 DMMA 8x8 tiles, 2 SY_NT^2 fp64 accumulators per lane); the
 // K loop streams SY_KB points per stage into shared memory with cp.async (2 stages,
 // zero-filled past the chunk end); the weight w_p = 1/(D_n + lambda) scales the A fragment.
-constexpr int SY_KB = 32;      // points per stage
+#ifndef PBA_SY_KB
+#define PBA_SY_KB 32
+#endif
+#ifndef PBA_SY_STAGES
+#define PBA_SY_STAGES 2
+#endif
+constexpr int SY_KB = PBA_SY_KB;  // points per stage
 constexpr int SY_LDS = SCH_TB + 4;  // smem row stride (doubles): = 4 mod 16 puts the 4 k-rows of a half-warp fragment load on distinct banks (2 wavefronts)
-constexpr int SY_STAGES = 2;
+constexpr int SY_STAGES = PBA_SY_STAGES;
 constexpr int SY_THREADS = 128;
 constexpr size_t SY_SMEM = static_cast<size_t>(SY_STAGES) * (2 * SY_KB * SY_LDS + SY_KB) * sizeof(double);
 
@@ -1594,15 +1600,19 @@ __global__ void __launch_bounds__(SY_THREADS) k_schur_syrk(const ObsView ov, con
 #pragma unroll
     for (int j = 0; j < SY_NT; ++j) accd[i][j][0] = accd[i][j][1] = 0.0;
   const int nsb = (p1 - p0 + SY_KB - 1) / SY_KB;
-  if (nsb > 0) issue(0, p0);
+  // SY_STAGES-deep cp.async pipeline: SY_STAGES - 1 stages in flight while one is consumed (an
+  // empty commit group past the end keeps the wait count uniform)
+#pragma unroll
+  for (int i = 0; i < SY_STAGES - 1; ++i) {
+    if (i < nsb) issue(i, p0 + i * SY_KB);
+    else cp_async_commit();
+  }
   for (int sb = 0; sb < nsb; ++sb) {
-    const int stage = sb & 1;
-    if (sb + 1 < nsb) {
-      issue(stage ^ 1, p0 + (sb + 1) * SY_KB);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int stage = sb % SY_STAGES;
+    const int nxt = sb + SY_STAGES - 1;
+    if (nxt < nsb) issue(nxt % SY_STAGES, p0 + nxt * SY_KB);
+    else cp_async_commit();
+    cp_async_wait<SY_STAGES - 1>();
     __syncthreads();
     if (active) {
       const double* as = As + stage * SY_KB * SY_LDS + wr * SY_QW + (lane >> 2);

@@ -273,7 +273,6 @@ Engine::~Engine() {
     cudaEventDestroy(pd.b);
   }
   if (status_h_) cudaFreeHost(status_h_);
-  if (pe_h_) cudaFreeHost(pe_h_);
   if (side_) {
     cudaStreamSynchronize(side_);
     cudaStreamDestroy(side_);
@@ -652,7 +651,7 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
       ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "fork event");
       ck(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "join event");
     }
-    launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), stream_, side_, fork_, join_);
+    launch_obs_ic_tab(a, tabs_.data(), static_cast<int>(tabs_.size()), frame_recs_.p, stream_, side_, fork_, join_);
   } else {
     launch_obs(OBS_IC, a, stream_);
   }
@@ -699,57 +698,24 @@ Status Engine::ic_read_status() {
   return s;
 }
 
-// Frame tables of the IC pass (kTabFrames frames per launch): the evaluation poses are read
-// back (the pass is ordered after the candidate update anyway), the frozen poses and the
-// intrinsics are host-resident.
+// Frame tables of the IC pass (kTabFrames frames per launch): the chunk geometry is fixed per
+// handle; the records are built on the device from the evaluation poses (no host read-back) and
+// copied into constant memory by launch_obs_ic_tab on the launching stream.
 void Engine::build_frame_tabs(const PoseD* pose_d) {
-  if (!pe_h_) ck(cudaMallocHost(&pe_h_, std::max(F_, 1) * sizeof(PoseD)), "pinned poses");
-  if (F_ > 0) ck(cudaMemcpyAsync(pe_h_, pose_d, F_ * sizeof(PoseD), cudaMemcpyDeviceToHost, stream_), "poses");
-  if (pose0_h_.size() != static_cast<size_t>(F_)) {
-    pose0_h_.resize(F_);
-    if (F_ > 0) ck(cudaMemcpyAsync(pose0_h_.data(), pose0_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToHost, stream_), "p0");
-  }
-  ck(cudaStreamSynchronize(stream_), "pose sync");
   const int ntab = (F_ + kTabFrames - 1) / kTabFrames;
-  tabs_.resize(ntab);
-  for (int i = 0; i < ntab; ++i) {
-    FrameTab& T = tabs_[i];
-    T.f0 = i * kTabFrames;
-    T.nf = std::min(kTabFrames, F_ - T.f0);
-    T.tile0 = ftile_ptr_h_[T.f0];
-    T.ntiles = ftile_ptr_h_[T.f0 + T.nf] - T.tile0;
-    for (int j = 0; j < T.nf; ++j) {
-      const int f = T.f0 + j;
-      FrameRec& r = T.r[j];
-      r.pe = pe_h_[f];
-      r.p0 = pose0_h_[f];
-      r.t0z = r.p0.t[2];
-#if PBA_IC_V2
-      {  // tau = R0^T t0 in the translation slot (the pass's frame-factored gradient)
-        const PoseD& q = pose0_h_[f];
-        for (int j = 0; j < 3; ++j) r.p0.t[j] = q.R[j] * q.t[0] + q.R[3 + j] * q.t[1] + q.R[6 + j] * q.t[2];
-      }
-#endif
-#if PBA_TAB_SCALED
-      for (int c = 0; c < 3; ++c) {
-        r.pe.R[c] *= frames_h_[f].fx;
-        r.pe.R[3 + c] *= frames_h_[f].fy;
-      }
-      r.pe.t[0] *= frames_h_[f].fx;
-      r.pe.t[1] *= frames_h_[f].fy;
-      r.fsx = static_cast<double>(frames_h_[f].W - 3);
-      r.fsy = static_cast<double>(frames_h_[f].H - 3);
-#else
-      r.fsx = frames_h_[f].fx;
-      r.fsy = frames_h_[f].fy;
-#endif
-      r.cx = frames_h_[f].cx;
-      r.cy = frames_h_[f].cy;
-      r.img = frames_h_[f].img;
-      r.W = frames_h_[f].W;
-      r.H = frames_h_[f].H;
+  if (static_cast<int>(tabs_.size()) != ntab) {
+    tabs_.resize(ntab);
+    for (int i = 0; i < ntab; ++i) {
+      FrameTab& T = tabs_[i];
+      T.f0 = i * kTabFrames;
+      T.nf = std::min(kTabFrames, F_ - T.f0);
+      T.tile0 = ftile_ptr_h_[T.f0];
+      T.ntiles = ftile_ptr_h_[T.f0 + T.nf] - T.tile0;
+      T.slot = i % kTabSlots;
     }
   }
+  frame_recs_.alloc(std::max(F_, 1));
+  launch_frame_recs(F_, pose_d, pose0_.p, frames_.p, frame_recs_.p, stream_);
 }
 
 void Engine::ic_rescale_rhs(int buf, double lambda) {
@@ -896,7 +862,6 @@ void Engine::ic_build(const pba_config* cfg) {
   check_template();
   trace_mark(stream_, "ic_build:   template check");
   if (F_ > 0) ck(cudaMemcpyAsync(pose0_.p, pose_state_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p0");
-  pose0_h_.clear();  // host copy of the frozen poses is refreshed by build_frame_tabs
   if (N_ > 0) ck(cudaMemcpyAsync(d0_.p, d_state_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d0");
   for (int f = 0; f < F_; ++f) {  // :265-271
     const double* t = &t_state_[3 * f];

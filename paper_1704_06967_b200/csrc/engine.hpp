@@ -220,9 +220,8 @@ class Engine {
   DBuf<Status> status_;
   DBuf<int> flags_;
   Status* status_h_ = nullptr;    // pinned
-  PoseD* pe_h_ = nullptr;         // pinned: evaluation poses for the IC frame tables
-  std::vector<PoseD> pose0_h_;    // host copy of the frozen IC poses
-  std::vector<FrameTab> tabs_;    // IC pass frame tables (kernel parameters)
+  std::vector<FrameTab> tabs_;    // IC pass frame chunks (kernel parameters: frames, tiles, constant slot)
+  DBuf<FrameRec> frame_recs_;     // IC pass frame records, built on the device per pass
   int64_t tab_min_obs_ = int64_t(1) << 20;  // frame tables from this many observations on (env PBA_TAB_MIN_OBS)
   cudaStream_t side_ = nullptr;   // second stream for the IC pass frame chunks
   cudaStream_t up_stream_ = nullptr;   // target-image upload (deferred handles: completes behind create)

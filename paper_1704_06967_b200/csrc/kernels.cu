@@ -21,6 +21,7 @@
 #include <cstdio>
 
 #include <atomic>
+#include <mutex>
 
 #include "kernels.hpp"
 
@@ -388,6 +389,8 @@ __device__ __forceinline__ void ic_row(const PoseD& p0, const double (&R0x)[3], 
   row[6] = fma(m0, p0.t[0], fma(m1, p0.t[1], m2 * p0.t[2]));
 }
 
+__constant__ FrameRec c_tab[kTabSlots][kTabFrames];  // the IC pass's frame records (launch_obs_ic_tab)
+
 // kTab: the frame-uniform records (candidate pose, frozen pose, intrinsics) come from a
 // kernel-parameter table (constant bank, read through the constant cache) instead of shared
 // memory: the per-pixel re-reads of the pose then cost no L1 data-pipe wavefronts, which
@@ -482,7 +485,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     uint32_t bits = 0u;
     bool obs_ok = true;
     if constexpr (MODE == OBS_BUILD) {
-      const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+      const PoseD p0 = kTab ? c_tab[tab.slot][f - tab.f0].p0 : lds_pose(s_p0);
       // make_proxy_constants at the anchor (geometry.cpp:141-160): masks the whole obs
       const double xa = ((an.x + static_cast<double>(a.pat.dx[0])) - rf.cx) * a.ref_ifx;
       const double ya = ((an.y + static_cast<double>(a.pat.dy[0])) - rf.cy) * a.ref_ify;
@@ -495,12 +498,12 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     constexpr bool kOB = PBA_IC_OBSBASE && MODE == OBS_IC && PT > 0;
     double xa = 0.0, ya = 0.0, bx = 0.0, by = 0.0, bz = 0.0, c8 = 0.0;
     if constexpr (kV2) {  // pixel-invariant part of the frozen depth vz0 = R0[6] x + R0[7] y + R0[8] + d0 t0z
-      const double r8 = kTab ? tab.r[f - tab.f0].p0.R[8] : s_p0.R[8];
-      const double t0z = kTab ? tab.r[f - tab.f0].t0z : s_tau[3];
+      const double r8 = kTab ? c_tab[tab.slot][f - tab.f0].p0.R[8] : s_p0.R[8];
+      const double t0z = kTab ? c_tab[tab.slot][f - tab.f0].t0z : s_tau[3];
       c8 = fma(d0n, t0z, r8);
     }
     if constexpr (kOB) {
-      const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
+      const PoseD pe = kTab ? c_tab[tab.slot][f - tab.f0].pe : lds_pose(s_pe);
       xa = (an.x - rf.cx) * a.ref_ifx;
       ya = (an.y - rf.cy) * a.ref_ify;
       bx = fma(dv, pe.t[0], pe.R[2]);
@@ -525,8 +528,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
       double xn, yn, vx, vy, vz, r = 0.0;
       bool act = false;
       double4 T = make_double4(0.0, NAN, NAN, 0.0);  // template record {tval, gx, gy} (non-FC modes)
-      const PoseD pe = kTab ? tab.r[f - tab.f0].pe : lds_pose(s_pe);
-      const FrameL fr = kTab ? tab_frame(tab.r[f - tab.f0]) : lds_frame(s_fr);
+      const PoseD pe = kTab ? c_tab[tab.slot][f - tab.f0].pe : lds_pose(s_pe);
+      const FrameL fr = kTab ? tab_frame(c_tab[tab.slot][f - tab.f0]) : lds_frame(s_fr);
       constexpr bool kTplEarly = PBA_IC_TPL_EARLY && MODE == OBS_IC;
       if constexpr (kTplEarly) T = ld_tpl(tpl + k);  // issued ahead of the warp: its latency overlaps it
       bool wok;
@@ -568,9 +571,9 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           if constexpr (kV2) {
             // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
             const double wr = fabs(r) <= gam ? r : copysign(gam, r);
-            const double* R0 = kTab ? tab.r[f - tab.f0].p0.R : s_p0.R;
-            const double* tau = kTab ? tab.r[f - tab.f0].p0.t : s_tau;
-            const double t0z = kTab ? tab.r[f - tab.f0].t0z : s_tau[3];
+            const double* R0 = kTab ? c_tab[tab.slot][f - tab.f0].p0.R : s_p0.R;
+            const double* tau = kTab ? c_tab[tab.slot][f - tab.f0].p0.t : s_tau;
+            const double t0z = kTab ? c_tab[tab.slot][f - tab.f0].t0z : s_tau[3];
             const double vz0 = fma(R0[6], x, fma(R0[7], y, c8));
             const double s0 = d0n * rcp_nr(vz0);  // |vz0| >= 1e-12: degenerate pixels are masked at the build
             const double g3z = T.w;               // -(gx x + gy y) of the template record
@@ -593,7 +596,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
           } else if constexpr (MODE == OBS_IC) {
             // fresh weights (solver.cpp:461): w(r) r = r or gamma * sign(r) (no division)
             const double wr = fabs(r) <= gam ? r : copysign(gam, r);
-            const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+            const PoseD p0 = kTab ? c_tab[tab.slot][f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
 #if PBA_IC_FACT
@@ -622,7 +625,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
 #endif
             bits |= 1u << k;
           } else if constexpr (MODE == OBS_REFRESH) {
-            const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+            const PoseD p0 = kTab ? c_tab[tab.slot][f - tab.f0].p0 : lds_pose(s_p0);
             double R0x[3], row[7];
             rot_ray(p0, x, y, R0x);
             ic_jrow<kRc>(p0, R0x, d0n, x, y, T.y, T.z, k, jm, P, row);
@@ -675,7 +678,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         // IcSolver::build per-pixel rows (solver.cpp:306-356); evaluation point is p0
         double m0 = 0.0, m1 = 0.0, m2 = 0.0;
         if (act && obs_ok) {
-          const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+          const PoseD p0 = kTab ? c_tab[tab.slot][f - tab.f0].p0 : lds_pose(s_p0);
           // template gradient image_gradient(ref, x) (image.cpp:36-49): computed once per (n, k)
           // with the template values (solver.cpp:296-304), NaN when its footprint leaves the image
           const double2 tg = make_double2(T.y, T.z);
@@ -711,7 +714,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     }
 #if PBA_IC_FACT
     if constexpr (MODE == OBS_IC && !kV2) {  // apply the per-observation factors: [.., d0 sum wr m, t0 . sum wr m]
-      const PoseD p0 = kTab ? tab.r[f - tab.f0].p0 : lds_pose(s_p0);
+      const PoseD p0 = kTab ? c_tab[tab.slot][f - tab.f0].p0 : lds_pose(s_p0);
       gacc[3] = fma(d0n, mw[0], gacc[3]);
       gacc[4] = fma(d0n, mw[1], gacc[4]);
       gacc[5] = fma(d0n, mw[2], gacc[5]);
@@ -763,7 +766,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     if (lane == 0) red[warp][slot] = v;
   };
   if constexpr (kV2) {  // the frame-factored sums to J^T W r of the frame (R0 is uniform over the tile)
-    const double* R0 = kTab ? tab.r[f - tab.f0].p0.R : s_p0.R;
+    const double* R0 = kTab ? c_tab[tab.slot][f - tab.f0].p0.R : s_p0.R;
     double rc[3], rq[3], rg[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -2163,8 +2166,60 @@ void launch_lane(const ObsArgs& a, cudaStream_t s) {
   else k_obs_lane<MODE, 0, 1><<<a.ov.ntiles, NT, 0, s>>>(a);
 }
 
-void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s, cudaStream_t side,
-                       cudaEvent_t fork, cudaEvent_t join) {
+// IC frame records from the candidate poses (PBA_TAB_SCALED: rows 0/1 of the candidate pose
+// pre-multiplied by fx, fy; (fsx, fsy) = in-margin bounds W - 3, H - 3; PBA_IC_V2: tau = R0^T t0)
+__global__ void k_frame_recs(int F, const PoseD* __restrict__ pe, const PoseD* __restrict__ p0,
+                             const FrameD* __restrict__ frames, FrameRec* __restrict__ recs) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const FrameD fr = frames[f];
+  FrameRec r;
+  r.pe = pe[f];
+  r.p0 = p0[f];
+  r.t0z = r.p0.t[2];
+#if PBA_IC_V2
+  const PoseD q = p0[f];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) r.p0.t[j] = q.R[j] * q.t[0] + q.R[3 + j] * q.t[1] + q.R[6 + j] * q.t[2];
+#endif
+#if PBA_TAB_SCALED
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    r.pe.R[c] *= fr.fx;
+    r.pe.R[3 + c] *= fr.fy;
+  }
+  r.pe.t[0] *= fr.fx;
+  r.pe.t[1] *= fr.fy;
+  r.fsx = static_cast<double>(fr.W - 3);
+  r.fsy = static_cast<double>(fr.H - 3);
+#else
+  r.fsx = fr.fx;
+  r.fsy = fr.fy;
+#endif
+  r.cx = fr.cx;
+  r.cy = fr.cy;
+  r.img = fr.img;
+  r.W = fr.W;
+  r.H = fr.H;
+  recs[f] = r;
+}
+
+void launch_frame_recs(int F, const PoseD* pose_eval, const PoseD* pose0, const FrameD* frames, FrameRec* recs,
+                       cudaStream_t s) {
+  if (F <= 0) return;
+  k_frame_recs<<<(F + 127) / 128, 128, 0, s>>>(F, pose_eval, pose0, frames, recs);
+  count_launches(1);
+}
+
+namespace {
+// The constant tables are one per process: passes of different handles (e.g. the shards of one
+// process on their own streams) take turns per slot, ordered by an event and a host mutex.
+std::mutex g_tab_mutex;
+cudaEvent_t g_tab_free[kTabSlots] = {};
+}  // namespace
+
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, const FrameRec* recs, cudaStream_t s,
+                       cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   // the frame chunks are independent (disjoint tiles): chunks after the first run on a side
   // stream so their launches overlap instead of serialising tail effects
   const bool fan = ntabs > 1 && side && fork && join;
@@ -2172,13 +2227,20 @@ void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaSt
     cudaEventRecord(fork, s);
     cudaStreamWaitEvent(side, fork, 0);
   }
+  std::lock_guard<std::mutex> lk(g_tab_mutex);
   for (int i = 0; i < ntabs; ++i) {
     const int nb = tabs[i].ntiles;
     if (nb == 0) continue;
     cudaStream_t st = (fan && i > 0) ? side : s;
+    const int slot = tabs[i].slot;
+    if (!g_tab_free[slot]) cudaEventCreateWithFlags(&g_tab_free[slot], cudaEventDisableTiming);
+    cudaStreamWaitEvent(st, g_tab_free[slot], 0);  // the slot's previous pass (any handle) is done
+    cudaMemcpyToSymbolAsync(c_tab, recs + tabs[i].f0, tabs[i].nf * sizeof(FrameRec),
+                            static_cast<size_t>(slot) * kTabFrames * sizeof(FrameRec), cudaMemcpyDeviceToDevice, st);
     if (a.pat.P == 8) k_obs_lane_tab<OBS_IC, 8, PBA_IC_LPO><<<nb, NT, 0, st>>>(a, tabs[i]);
     else k_obs_lane_tab<OBS_IC, 0, 1><<<nb, NT, 0, st>>>(a, tabs[i]);
-    count_launches(1);
+    cudaEventRecord(g_tab_free[slot], st);
+    count_launches(2);
   }
   if (fan) {
     cudaEventRecord(join, side);

@@ -88,13 +88,20 @@ struct FrameRec {
   const float* img;
   int W, H;
 };
-constexpr int kTabFrames = 120;  // 120 * 248 B + ObsArgs < 32 KB kernel-parameter limit
-struct FrameTab {
-  int f0, nf, tile0, ntiles;
-  FrameRec r[kTabFrames];
+// The IC pass reads its frame records from constant memory: kTabSlots tables of kTabFrames records
+// (the frame chunks of one pass run concurrently, one slot each).  The records are built on the
+// device from the candidate poses (k_frame_recs) and copied into the slot on the launching stream,
+// so the pass needs no host read-back of the poses.
+constexpr int kTabFrames = 120;
+constexpr int kTabSlots = 2;  // 2 * 120 * 248 B of the 64 KB constant bank
+struct FrameTab {             // kernel parameter: which frames / tiles / constant slot
+  int f0, nf, tile0, ntiles, slot;
 };
-void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, cudaStream_t s, cudaStream_t side,
-                       cudaEvent_t fork, cudaEvent_t join);
+// records of frames [0, F) into recs (device): scaled candidate rows, {R0, tau}, t0z, intrinsics
+void launch_frame_recs(int F, const PoseD* pose_eval, const PoseD* pose0, const FrameD* frames, FrameRec* recs,
+                       cudaStream_t s);
+void launch_obs_ic_tab(const ObsArgs& a, const FrameTab* tabs, int ntabs, const FrameRec* recs, cudaStream_t s,
+                       cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 // doubles of the factored IC Jacobian store for NO observations of P pixels
 inline int64_t jm_doubles(int64_t NO, int P) { return ((NO + 31) / 32) * 3 * static_cast<int64_t>(P) * 32; }
 

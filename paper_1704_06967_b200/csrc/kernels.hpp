@@ -92,8 +92,11 @@ struct FrameRec {
 // (the frame chunks of one pass run concurrently, one slot each).  The records are built on the
 // device from the candidate poses (k_frame_recs) and copied into the slot on the launching stream,
 // so the pass needs no host read-back of the poses.
-constexpr int kTabFrames = 120;
-constexpr int kTabSlots = 2;  // 2 * 120 * 248 B of the 64 KB constant bank
+#ifndef PBA_TAB_FRAMES
+#define PBA_TAB_FRAMES 240  // one constant table (and one IC-pass launch) for up to 240 frames
+#endif
+constexpr int kTabFrames = PBA_TAB_FRAMES;
+constexpr int kTabSlots = 240 / PBA_TAB_FRAMES;  // kTabSlots * kTabFrames * 248 B of the 64 KB constant bank
 struct FrameTab {             // kernel parameter: which frames / tiles / constant slot
   int f0, nf, tile0, ntiles, slot;
 };

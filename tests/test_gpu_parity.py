@@ -407,8 +407,8 @@ def test_deterministic_repeat(c1):
 @pytest.fixture(scope="module")
 def many_frames():
     # C4-shaped (azimuth visibility window, sub-pixel anchors, DSO8) with more frames than one
-    # IC frame table holds (kTabFrames = 120): exercises the chunked IC pass on two streams
-    cfg = scenes.baseline_config("C4", width=320, height=180, fx=250.0, frames=130, points=3000, iters=4)
+    # IC frame table holds (kTabFrames = 240): exercises the chunked IC pass (constant slot reused in turn)
+    cfg = scenes.baseline_config("C4", width=320, height=180, fx=250.0, frames=250, points=3000, iters=4)
     return scenes.make_scene(cfg, device="cpu")
 
 

@@ -152,3 +152,37 @@ def assert_final_params_close(rg, ro, tol, st=None, kind=None, cfg=None):
         assert_params_close(rg.final_R, ro.final_R, tol, env["R"])
         assert_params_close(rg.final_t, ro.final_t, tol, env["t"])
         assert_params_close(rg.final_inv_depths, ro.final_inv_depths, tol, env["d"])
+
+
+def oracle_energy_by_point_ranges(st: ProblemState, gamma: float, parts: int = 8):
+    """energy_eval of the oracle over contiguous point ranges on host threads (the energy is a sum
+    over points; each range is an independent single-threaded oracle call, the ctypes calls release
+    the GIL).  Returns (energy, num_active, num_out_of_bounds) summed over the ranges; only the
+    summation order differs from one whole-problem call (far below the 1e-10 the callers allow)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1704_06967_b200 import solver
+    N = st.num_points
+    parts = max(1, min(parts, N))
+    edges = np.linspace(0, N, parts + 1).astype(np.int64)
+
+    def one(i):
+        a, b = int(edges[i]), int(edges[i + 1])
+        op = of = None
+        if st.obs_ptr is not None:
+            o0, o1 = int(st.obs_ptr[a]), int(st.obs_ptr[b])
+            op = np.ascontiguousarray(st.obs_ptr[a:b + 1] - o0)
+            of = np.ascontiguousarray(st.obs_frame[o0:o1])
+        sub = ProblemState(st.ref, st.ref_K, st.targets, st.targets_K, st.R, st.t,
+                           np.ascontiguousarray(st.anchors_px[a:b]), np.ascontiguousarray(st.inv_depths[a:b]),
+                           st.pattern, op, of)
+        try:
+            return solver.energy_eval(sub, gamma, backend=ORACLE)
+        except Exception as e:  # EmptyProblem of a range with no in-bounds residual
+            if "Empty" in type(e).__name__ or "empty" in str(e).lower() or "no in-bounds" in str(e):
+                return None
+            raise
+
+    with ThreadPoolExecutor(max_workers=parts) as pool:
+        res = [r for r in pool.map(one, range(parts)) if r is not None]
+    return (float(sum(r.energy for r in res)), int(sum(r.num_active for r in res)),
+            int(sum(r.num_out_of_bounds for r in res)))

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from paper_1704_06967_b200 import scenes, solver
-from ._oracle import ORACLE
+from ._helpers import oracle_energy_by_point_ranges
 
 pytestmark = pytest.mark.gpu
 
@@ -33,9 +33,9 @@ def test_c4_energy_matches_oracle_at_full_size(c4):
     st = c4.state
     gam = c4.cfg.solver_config().gamma
     eg = solver.energy_eval(st, gam)
-    eo = solver.energy_eval(st, gam, backend=ORACLE)
-    assert eg.num_active == eo.num_active and eg.num_active > 2.5e8
-    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+    eo_energy, eo_active, eo_oob = oracle_energy_by_point_ranges(st, gam)
+    assert eg.num_active == eo_active and eg.num_active > 2.5e8 and eg.num_out_of_bounds == eo_oob
+    assert abs(eg.energy - eo_energy) <= E_TOL * eo_energy
 
 
 def test_c4_ic_iterations_full_size(c4):
@@ -55,8 +55,8 @@ def test_c4_ic_iterations_full_size(c4):
     # the energy pass at the solved parameters agrees with the oracle at full size
     s2 = _at(st, r1.final_R, r1.final_t, r1.final_inv_depths)
     eg = solver.energy_eval(s2, cfg.gamma)
-    eo = solver.energy_eval(s2, cfg.gamma, backend=ORACLE)
-    assert eg.num_active == eo.num_active
-    assert abs(eg.energy - eo.energy) <= E_TOL * eo.energy
+    eo_energy, eo_active, _ = oracle_energy_by_point_ranges(s2, cfg.gamma)
+    assert eg.num_active == eo_active
+    assert abs(eg.energy - eo_energy) <= E_TOL * eo_energy
     # the IC energy is taken over the sticky mask (a subset of the in-bounds pixels)
     assert r1.iters[-1].num_active <= eg.num_active and r1.final_energy <= eg.energy * (1 + 1e-12)

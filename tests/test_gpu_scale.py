@@ -62,6 +62,33 @@ def c4_sub(c4):
     return scenes.subsample_points(c4.state, 20000, seed=1)
 
 
+@pytest.fixture(scope="module")
+def c3_sub(c3):
+    return scenes.subsample_points(c3.state, 20000, seed=2)
+
+
+@pytest.fixture(scope="module")
+def oracle_jobs(c4, c4_sub, c3, c3_sub):
+    """The oracle side of every test of this module, started together on host threads (the oracle is
+    single-threaded per handle, as the reference is; independent handles run concurrently and the
+    ctypes calls release the GIL), so the module takes about as long as its longest oracle solve.
+    Each test waits for its own result."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(st, kind, cfg):
+        return getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+
+    pool = ThreadPoolExecutor(max_workers=max(1, min(7, os.cpu_count() or 1)))
+    jobs = {"c4_fc_build": pool.submit(lambda: Handle(c4.state, ORACLE).fc_build(c4.cfg.huber_delta))}
+    for kind in ("fc", "ic"):
+        jobs["c4_sub", kind] = pool.submit(run, c4_sub, kind, c4.cfg.solver_config(max_iters=10))
+        jobs["c3", kind] = pool.submit(run, c3.state, kind, c3.cfg.solver_config(max_iters=5))
+        jobs["c3_sub", kind] = pool.submit(run, c3_sub, kind, c3.cfg.solver_config(max_iters=20))
+    yield jobs
+    pool.shutdown(wait=True, cancel_futures=True)
+
+
 def test_c4_subsample_covers_every_frame(c4, c4_sub):
     """The subsample keeps the full reduced system (200 frames, 6F = 1200) and observes every frame the
     full scene observes at least 100 times (the orbit's first and last 7 frames are outside every
@@ -74,10 +101,10 @@ def test_c4_subsample_covers_every_frame(c4, c4_sub):
 
 
 @pytest.mark.parametrize("kind", ["ic", "fc"])
-def test_c4_geometry_runs_match_oracle(c4, c4_sub, kind):
+def test_c4_geometry_runs_match_oracle(c4, c4_sub, oracle_jobs, kind):
     cfg = c4.cfg.solver_config(max_iters=10)  # BASELINE C4: 10 iterations
     rg = getattr(Handle(c4_sub, "gpu"), f"{kind}_run")(cfg)
-    ro = getattr(Handle(c4_sub, ORACLE), f"{kind}_run")(cfg)
+    ro = oracle_jobs["c4_sub", kind].result()
     assert rg.iterations == 10 or rg.converged
     compare_runs(rg, ro, c4_sub, kind, cfg)
 
@@ -97,11 +124,10 @@ def test_c4_ic_build_and_step_at_n1200(c4, c4_sub):
     assert rel(project_out(g.ic_compute_step(), v), project_out(o.ic_compute_step(), v)) <= 1e-4
 
 
-def test_c4_full_size_fc_build_matches_oracle(c4):
+def test_c4_full_size_fc_build_matches_oracle(c4, oracle_jobs):
     """One FC Hessian / gradient build over all 3.8e7 observations (solver.cpp:688-724)."""
     st = c4.state
-    (Hg, gg), (Ho, go) = Handle(st, "gpu").fc_build(c4.cfg.huber_delta), Handle(st, ORACLE).fc_build(
-        c4.cfg.huber_delta)
+    (Hg, gg), (Ho, go) = Handle(st, "gpu").fc_build(c4.cfg.huber_delta), oracle_jobs["c4_fc_build"].result()
     assert rel(Hg.pose_pose, Ho.pose_pose) <= 1e-9
     assert rel(Hg.depth_depth, Ho.depth_depth) <= 1e-9
     assert rel(Hg.pose_depth, Ho.pose_depth) <= 1e-9
@@ -109,19 +135,19 @@ def test_c4_full_size_fc_build_matches_oracle(c4):
 
 
 @pytest.mark.parametrize("kind", ["ic", "fc"])
-def test_c3_full_runs_match_oracle(c3, kind):
+def test_c3_full_runs_match_oracle(c3, oracle_jobs, kind):
     cfg = c3.cfg.solver_config(max_iters=5)
     st = c3.state
     rg = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
-    ro = getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+    ro = oracle_jobs["c3", kind].result()
     compare_runs(rg, ro, st, kind, cfg)
 
 
 @pytest.mark.parametrize("kind", ["ic", "fc"])
-def test_c3_twenty_iterations_on_a_subsample(c3, kind):
+def test_c3_twenty_iterations_on_a_subsample(c3, c3_sub, oracle_jobs, kind):
     """BASELINE C3's 20 LM iterations (default convergence threshold) on a 20k-point subsample."""
-    st = scenes.subsample_points(c3.state, 20000, seed=2)
+    st = c3_sub
     cfg = c3.cfg.solver_config(max_iters=20)
     rg = getattr(Handle(st, "gpu"), f"{kind}_run")(cfg)
-    ro = getattr(Handle(st, ORACLE), f"{kind}_run")(cfg)
+    ro = oracle_jobs["c3_sub", kind].result()
     compare_runs(rg, ro, st, kind, cfg)

@@ -172,10 +172,21 @@ def ncu_profile_extra():
                 continue
             k = ks[0]
             pick = lambda key: float(k[key].split()[0].replace(",", "")) if key in k else None  # noqa: E731
-            return {"source": f"profiles/{name}",
-                    "fp64_pipe_pct": pick("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-                    "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                    "dram_pct_of_theoretical": pick("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+            out = {"source": f"profiles/{name}",
+                   "fp64_pipe_pct": pick("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                   "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "dram_pct_of_theoretical": pick("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+            pp = REPO / "profiles" / "r2_ic_pipes.json"  # per-pipe capture of the same kernel (tools/ncu_ic_raw.sh)
+            if pp.exists():
+                v = json.loads(pp.read_text())["variants"]["default"]
+                out["pipes_source"] = "profiles/r2_ic_pipes.json"
+                out["l1_lsu_data_pipe_pct"] = v.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_active")
+                out["adu_pipe_pct"] = v.get("sm__inst_executed_pipe_adu.avg.pct_of_peak_sustained_active")
+                out["xu_pipe_pct"] = v.get("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active")
+                out["l2_pct"] = v.get("lts__throughput.avg.pct_of_peak_sustained_elapsed")
+                out["stall_cycles_per_issue"] = {k[6:]: v[k] for k in ("stall_long_scoreboard", "stall_wait",
+                                                                        "stall_short_scoreboard") if k in v}
+            return out
         except Exception:
             continue
     return None
@@ -625,8 +636,10 @@ def main():
                              "/ launch time: an effective bandwidth, since the pass stores no rows and rebuilds them "
                              "from 32-byte per-(point, pixel) template records (so frac can exceed 1: the pass is faster "
                              "than any pass that reads the stored 56 B/px rows could be); min_dram_bytes_per_pass = what it "
-                             "must move; traffic = ncu DRAM bytes of one pass; the binding resource is L1/L2-hit "
-                             "latency and issue (ncu); canonical_* = full B_IC over the whole iteration"},
+                             "must move; traffic = ncu DRAM bytes of one pass; no unit is saturated (ncu: L1 LSU data pipe 82%, "
+                             "ADU 66%, FP64 42.5%, issue 47%) and relieving either of the two busiest did not speed the pass "
+                             "up (DESIGN.md section 4): the binding resource is load and fp64-chain latency at register-limited "
+                             "occupancy (6 warps per scheduler); canonical_* = full B_IC over the whole iteration"},
         "kernel_ms_per_iter": {n: round(v[1] / args.steps, 4) for n, v in kt.items() if v[0]},
         "clocks": r["clocks"],
         "gpu_launches": int(r["launches"]),

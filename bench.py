@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--reference-port", action="store_true",
+                    help="--impl reference: time the oracle port instead of oracle/_ref (the unmodified reference)")
     ap.add_argument("--fc-steps", type=int, default=2)
     ap.add_argument("--e2e-iters", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -319,6 +321,77 @@ def cpu_baseline_threads(st, cfg, npts_per_thread, threads, seed=0, iters=3):
                       f"oracle/ single-threaded fp64 restatement of solver.cpp per thread; {wall:.1f} s"}
 
 
+def dense_window_samples(st, frames_per_sample, npts, count, seed=0):
+    """Dense sub-problems of the scene for the unmodified reference (it has no observation list: every
+    point is observed in every frame): `frames_per_sample` consecutive target frames and `npts` points
+    the scene observes in all of them.  Same images, poses, anchors and depths as the full problem."""
+    import numpy as np
+
+    from paper_1704_06967_b200 import solver
+
+    rng = np.random.default_rng(seed)
+    F, K = st.num_frames, min(frames_per_sample, st.num_frames)
+    if st.obs_ptr is None:
+        first = np.zeros(st.num_points, np.int64)
+        last = np.full(st.num_points, F - 1, np.int64)
+        contiguous = np.ones(st.num_points, bool)
+    else:
+        first = st.obs_frame[st.obs_ptr[:-1]].astype(np.int64)
+        last = st.obs_frame[st.obs_ptr[1:] - 1].astype(np.int64)
+        contiguous = np.diff(st.obs_ptr) == last - first + 1
+    out = []
+    for _ in range(count):
+        for _try in range(64):
+            f0 = int(rng.integers(0, F - K + 1))
+            ok = np.nonzero(contiguous & (first <= f0) & (last >= f0 + K - 1))[0]
+            if ok.size >= npts:
+                break
+        else:
+            raise RuntimeError("no frame window of the scene has enough fully observed points")
+        idx = np.sort(rng.choice(ok, size=npts, replace=False))
+        out.append(solver.ProblemState(st.ref, st.ref_K, st.targets[f0:f0 + K], st.targets_K[f0:f0 + K],
+                                       st.R[f0:f0 + K].copy(), st.t[f0:f0 + K].copy(), st.anchors_px[idx].copy(),
+                                       st.inv_depths[idx].copy(), st.pattern, None, None))
+    return out
+
+
+def reference_threads(st, cfg, frames_per_sample, npts_per_thread, threads, seed=0, iters=3):
+    """The reference arm proper: the UNMODIFIED reference (oracle/_ref/libpba_ref.so, compiled in place
+    from /root/reference/proj/src by oracle/Makefile) on all host threads.  The reference is
+    single-threaded and dense, so each thread solves its own dense window sample (dense_window_samples);
+    value = all threads' active pixels per LM iteration / the steady iterations' wall time (the
+    reference's own cumulative IterationStats::wall_ms, max over threads).  The reference does not record
+    active counts: they are its own energy_eval count at the initial parameters."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1704_06967_b200 import solver
+    from tests._oracle import REF
+
+    subs = dense_window_samples(st, frames_per_sample, npts_per_thread, threads, seed=seed)
+    c = solver.SolverConfig(**{**cfg.__dict__, "max_iters": iters, "threshold_px": 0.0})
+
+    def one(sub):
+        rep = solver.ic_solve(sub, c, backend=REF)
+        its = rep.iters
+        nact = solver.energy_eval(sub, c.gamma, backend=REF).num_active
+        ms = (its[-1].wall_ms - its[0].wall_ms) if len(its) > 1 else (its[0].wall_ms if its else 0.0)
+        return nact * max(len(its) - 1, 1), ms, sub.num_observations
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(one, subs))
+    wall = time.perf_counter() - t0
+    px = sum(r[0] for r in res)
+    ms = max(r[1] for r in res)
+    v = px / (ms / 1e3) if ms > 0 else 0.0
+    return {"value": v, "unit": "obs_px/s", "cores": threads, "kind": "reference",
+            "ms_per_iter": ms / max(iters - 1, 1),
+            "sample": f"{threads} threads x one dense window each ({subs[0].num_frames} consecutive frames x "
+                      f"{npts_per_thread} points observed in all of them, of {st.num_frames} frames / {st.num_points} "
+                      f"points), {iters} IC iterations each, {sum(r[2] for r in res)} observations in total; the "
+                      f"unmodified reference solver.cpp (oracle/_ref, single-threaded per handle); {wall:.1f} s"}
+
+
 def run_ours(args, rank, world):
     import torch
 
@@ -525,10 +598,20 @@ def main():
         px_per_point = max(st.num_observations / st.num_points * st.pattern.shape[0], 1)
         npts = args.cpu_points or max(100, min(st.num_points, int(1.2e6 / px_per_point)))
         vals = []
+        from tests._oracle import REF_LIB
+        use_ref = REF_LIB.exists() and not args.reference_port
+        kf = min(32, st.num_frames)  # dense window of the reference samples (C4: ~38 observations per point)
+        npts_ref = args.cpu_points or max(100, int(1.2e6 / (kf * st.pattern.shape[0])))
         for k in range(args.warmup + args.steps):
-            cb = cpu_baseline_threads(st, cfg, npts, threads, seed=k, iters=3)
+            if use_ref:
+                cb = reference_threads(st, cfg, kf, npts_ref, threads, seed=k, iters=3)
+            else:
+                cb = cpu_baseline_threads(st, cfg, npts, threads, seed=k, iters=3)
             if k >= args.warmup:
                 vals.append(cb)
+        port = cpu_baseline_threads(st, cfg, npts, threads, seed=0, iters=3) if use_ref else None
+        if use_ref:
+            npts = npts_ref
         v = statistics.median([c["value"] for c in vals])
         cb = dict(vals[0])
         cb["value"] = v
@@ -541,14 +624,17 @@ def main():
                            "frames": st.num_frames,
                            "points": threads * npts,  # what was measured: the samples
                            "sample": {"threads": threads, "points_per_thread": npts,
-                                      "observations_per_thread": int(round(npts * st.num_observations / st.num_points)),
+                                      "observations_per_thread": (npts * kf if use_ref else
+                                                                  int(round(npts * st.num_observations / st.num_points))),
                                       "of_full_problem_points": st.num_points,
                                       "of_full_problem_observations": st.num_observations}},
                 "cpu_baseline": cb,
+                # the oracle port on observation-list samples of the same scene, once, beside the reference
+                "port_check": port,
                 # the contract's e2e of the reference arm is the line's own value (host-resident CPU
                 # port: no transfers); it is a per-LM-iteration rate on the samples, not a full solve
                 "e2e": {"value": v, "unit": "obs_px/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                        "what": "per-LM-iteration rate of the sampled oracle solves (same as value)"}}
+                        "what": "per-LM-iteration rate of the sampled CPU solves (same as value)"}}
         print(json.dumps(line))
         return
 
@@ -597,7 +683,13 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         npts = args.cpu_points or max(200, int(3.2e6 / (st.num_observations / st.num_points * st.pattern.shape[0])))
-        cpu = cpu_baseline(st, r["cfg"], min(npts, st.num_points))
+        from tests._oracle import REF_LIB
+        if REF_LIB.exists() and rank == 0:  # the unmodified reference on one core, one dense window sample
+            kf = min(32, st.num_frames)
+            cpu = reference_threads(st, r["cfg"], kf, args.cpu_points or max(100, int(3.2e6 / (kf * st.pattern.shape[0]))),
+                                    1)
+        else:
+            cpu = cpu_baseline(st, r["cfg"], min(npts, st.num_points))
     line = {
         "metric": "obs_px_per_s_per_LM_iteration",
         "value": value,

@@ -532,7 +532,7 @@ void Engine::xcheck(bool ok, int code, const std::string& msg) {
 }
 
 void Engine::finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
-                      double* rhs, const double* g_f_in, double* H, bool status) {
+                      double* rhs, const double* g_f_in, double* H, bool status, int e_slot) {
   if (sharded() && rhs && partial && !g_f) g_f = g_tmp_.p;  // the rank sum needs g itself
   FinalizeArgs f{};
   f.ov = ov_;
@@ -550,6 +550,7 @@ void Engine::finalize(const double* partial, const double* partial_cf, bool bs, 
   f.status = status ? status_.p : nullptr;
   f.fscal = fscal_.p;
   f.ticket = ticket_.p + 1;
+  f.e_slot = e_slot;
   if (sharded()) {  // rhs = -g + c_f is formed from the rank sums of g and c_f
     f.rhs = nullptr;
     f.cf_out = rhs ? cf_.p : nullptr;
@@ -575,6 +576,7 @@ void Engine::finalize(const double* partial, const double* partial_cf, bool bs, 
 // =====================================================================================
 void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, double* residuals, uint8_t* active) {
   check_template();
+  ic_.init_from_build = false;  // the pass overwrites the tile partials
   ensure_images();
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose_state_.p;
@@ -623,6 +625,7 @@ void Engine::energy(double gamma, const uint8_t* mask, pba_energy_result* out, d
 void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
                      double lambda, const PoseD* pose_old, const double* d_old) {
   // eval_residuals + assemble_gradient (solver.cpp:436-468) + solve_step rhs (:407-416)
+  ic_.init_from_build = false;  // the pass overwrites the tile partials and the g_n records
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose;
   a.pose_old = pose_old;
@@ -669,6 +672,23 @@ void Engine::ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in
   ev_end(PBA_K_REDUCE, e);
   finalize(partial_.p, partial_cf_.p, pose_old != nullptr, true, false, gf_[buf].p, rhs_[buf].p, nullptr, nullptr,
            true);
+}
+
+// IcSolver::run's initial pass (solver.cpp:487-495) evaluates the residuals at (pose0, d0) under the
+// build's mask with fresh weights: exactly what the build pass evaluated.  The build pass therefore
+// also sums J^T W r per frame (tile partials, PT_G), the g_n terms per observation (rec_g), and the
+// energy and count of the masked pixels (slots PT_MAXUPD, + 1); this forms the gradient, the Schur
+// rhs and the status from them without another observation pass (2.5 ms at C4).  The mask is
+// unchanged (every masked pixel is active at the build point), so the mask buffers do not flip.
+void Engine::ic_initial_from_build() {
+  PointArgs pa{ov_, PT_GRAD, rec_.p, gn_[0].p, Dic_.p, ic_.lambda, s_n_.p, partial_pt_.p};
+  pa.rec_g = rec_g_.p;  // per-observation records and the point-major gather (the fixed-point scales
+                        // of the later passes are set by the build itself)
+  const auto e = ev_begin(PBA_K_REDUCE);
+  launch_point(pa, stream_);
+  launch_cf(ov_, Bic_.p, s_n_.p, partial_cf_.p, stream_, nullptr);
+  ev_end(PBA_K_REDUCE, e);
+  finalize(partial_.p, partial_cf_.p, false, true, false, gf_[0].p, rhs_[0].p, nullptr, nullptr, true, PT_MAXUPD);
 }
 
 // Status of the last IC pass.  The fixed-point g_n sums hold every term whose magnitude the build's
@@ -900,6 +920,7 @@ void Engine::ic_build(const pba_config* cfg) {
   Bpm_.alloc(6 * nO);
   a.Bpm_out = Bpm_.p;  // point-major copy written by the pass itself
   a.fm2pm = fm2pm_.p;
+  a.rec_g = rec_g_.p;  // the initial pass's g_n terms (ic_initial_from_build)
   fuse_dense(a);
   trace_mark(stream_, "ic_build: setup+alloc");
   ensure_images();
@@ -927,6 +948,7 @@ void Engine::ic_build(const pba_config* cfg) {
   trace_mark(stream_, "ic_build: D, B copy, warnings");
   ic_factorize_loop(ic_.lambda);
   ic_.built = true;
+  ic_.init_from_build = !(std::getenv("PBA_IC_INIT_FROM_BUILD") && std::getenv("PBA_IC_INIT_FROM_BUILD")[0] == '0');
   trace_mark(stream_, "ic_build: factorize");
 }
 

@@ -78,6 +78,9 @@ struct SolverState {
   int builds = 0;
   int factorizations = 0;
   int mcur = 0;  // index of the sticky residual mask in mask_[] (solver.hpp:162)
+  // the build pass's tile partials and g_n records still hold IcSolver::run's initial pass (same
+  // parameters, rows, residuals and mask); cleared by every later observation pass
+  bool init_from_build = false;
   std::vector<std::string> warnings;  // frame warnings (solver.cpp:265-271)
   int64_t zero_d_count = 0;           // number of D_n == 0 points (:359-364)
   mutable std::vector<int32_t> zero_d;  // their user indices, downloaded and sorted on first request
@@ -310,7 +313,8 @@ class Engine {
   ObsArgs obs_args(double gamma) const;
   MaxUpdArgs maxupd_args(const PoseD* pose_old, const PoseD* pose_new, const double* d_old, const double* d_new) const;
   void finalize(const double* partial, const double* partial_cf, bool bs, bool pt, bool want_h, double* g_f,
-                double* rhs, const double* g_f_in, double* H, bool status);
+                double* rhs, const double* g_f_in, double* H, bool status, int e_slot = 0);
+  void ic_initial_from_build();  // the run's initial pass from the build pass's sums (no observation pass)
   // IC pieces
   void ic_eval(const PoseD* pose, const double* d, const uint32_t* mask_in, uint32_t* active_out, int buf,
                double lambda, const PoseD* pose_old, const double* d_old);

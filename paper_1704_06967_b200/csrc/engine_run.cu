@@ -139,6 +139,7 @@ void Engine::download_block_hessian(const DBuf<double>& H, const DBuf<double>& D
 
 // refresh_ic_hessian (solver.cpp:505-531): H from the frozen rows with fresh weights
 void Engine::ic_refresh() {
+  ic_.init_from_build = false;  // the pass overwrites the tile partials
   ObsArgs a = obs_args(ic_.cfg.gamma);
   a.pose_eval = pose_cur_.p;
   a.d_eval = d_cur_.p;
@@ -173,6 +174,7 @@ void Engine::alloc_fc() {
 // and the Schur rhs term with lambda_next.
 void Engine::fc_eval(double gamma, const PoseD* pose, const double* d, int buf, double lambda_next,
                      const PoseD* pose_old, const double* d_old) {
+  ic_.init_from_build = false;  // the pass overwrites the tile partials
   ObsArgs a = obs_args(gamma);
   a.pose_eval = pose;
   a.pose_old = pose_old;
@@ -375,10 +377,17 @@ void Engine::begin(bool ic, const pba_config* cfg) {
     if (F_ > 0) ck(cudaMemcpyAsync(pose_cur_.p, pose0_.p, F_ * sizeof(PoseD), cudaMemcpyDeviceToDevice, stream_), "p");
     if (N_ > 0) ck(cudaMemcpyAsync(d_cur_.p, d0_.p, N_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_), "d");
     // :487-495 initial pass, sticky mask &= active
-    ic_eval(pose_cur_.p, d_cur_.p, mask_[ic_.mcur].p, mask_[1 - ic_.mcur].p, 0, ic_.lambda, nullptr, nullptr);
-    const Status s = ic_read_status();
+    Status s{};
+    if (ic_.init_from_build) {  // the build pass already evaluated it (ic_initial_from_build)
+      ic_initial_from_build();
+      s = read_status();
+      ic_.init_from_build = false;  // gn_[0] / rhs_[0] now belong to the run
+    } else {
+      ic_eval(pose_cur_.p, d_cur_.p, mask_[ic_.mcur].p, mask_[1 - ic_.mcur].p, 0, ic_.lambda, nullptr, nullptr);
+      s = ic_read_status();
+      ic_.mcur = 1 - ic_.mcur;
+    }
     if (s.num_active == 0) throw PbaError(PBA_E_EMPTY_PROBLEM, "no in-bounds residuals");
-    ic_.mcur = 1 - ic_.mcur;
     run_.energy = s.energy;
     run_.initial_active = run_.num_active = static_cast<int64_t>(s.num_active);
     run_.rhs_lambda = ic_.lambda;

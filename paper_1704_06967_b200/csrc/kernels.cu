@@ -400,7 +400,10 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   static_assert(LPO == 1 || (PT > 0 && PT % LPO == 0), "LPO lanes split a compile-time pattern evenly");
   constexpr int OPB = NT / LPO;  // observations per block step
   constexpr bool kH = (MODE != OBS_IC);         // builds J^T W J, B, D
-  constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC);
+  // J^T W r per frame: the IC / FC passes, and the IC build, whose rows, residuals and mask are those
+  // of IcSolver::run's initial pass at the same parameters (solver.cpp:487-495): the build hands that
+  // pass's gradient, energy and active count to the run (Engine::begin), which then skips it
+  constexpr bool kG = (MODE == OBS_IC || MODE == OBS_FC || MODE == OBS_BUILD);
   const int tb = kTab ? tab.tile0 + static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
   const int t = a.ov.tile_order ? a.ov.tile_order[tb] : tb;  // launch order only: partials stay per tile
   const int f = a.ov.tile_frame[t];
@@ -443,6 +446,10 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   for (int i = 0; i < 6; ++i) gacc[i] = 0.0;
   double energy = 0.0;
   int nact = 0, noob = 0;  // integer counters: off the FP64 pipe
+  double energy_m = 0.0;   // OBS_BUILD: energy and count over the pixels that enter the sticky mask
+  int nact_m = 0;
+  (void)energy_m;
+  (void)nact_m;
   // L2 prefetch of the streamed per-observation inputs, kLanePrefetch block steps ahead
   auto prefetch_step = [&](int64_t qs) {
     if (qs >= q1) return;
@@ -480,6 +487,8 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
     const double4* tpl = a.tgrad + static_cast<int64_t>(n) * P;  // frozen {tval, gx, gy} of the point
     double b6[6] = {0, 0, 0, 0, 0, 0};
     double dc = 0.0, gnc = 0.0;
+    double gterm = 0.0;  // OBS_BUILD: the observation's g_n term of the initial pass
+    (void)gterm;
     double mw[3] = {0.0, 0.0, 0.0};  // PBA_IC_FACT: sum over the observation's pixels of wr m
     (void)mw;
     uint32_t bits = 0u;
@@ -702,6 +711,13 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             }
             dc += w * row[6] * row[6];
             gnc += fabs(row[6]);  // bound of the IC g_n terms: |w r| <= gamma (k_point PT_DONLY)
+            // the run's initial pass (fresh weights at the same residual, solver.cpp:461): w(r) r
+            const double wr = fabs(r) <= gam ? r : copysign(gam, r);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) gacc[c] = fma(row[c], wr, gacc[c]);
+            gterm = fma(row[6], wr, gterm);
+            energy_m += huber_loss(r, gam);
+            ++nact_m;
           }
         }
         if (a.Jmw) {  // store m unless the consumers rebuild it
@@ -741,6 +757,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
         else *a.gfix_bad = 1;  // non-finite or beyond the bound: the engine re-runs the pass unscaled
       } else if (MODE == OBS_IC && a.rec_g) a.rec_g[q] = gnc;  // IC needs the g_n term only (D is frozen)
       else a.rec[q] = make_double2(gnc, dc);
+      if (MODE == OBS_BUILD && a.rec_g) a.rec_g[q] = gterm;
       if constexpr (kH) {
 #pragma unroll
         for (int i2 = 0; i2 < 6; ++i2) a.B_out[q * 6 + i2] = b6[i2];
@@ -792,9 +809,14 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
   put(PT_E, energy);
   put(PT_NACT, static_cast<double>(nact));
   put(PT_NOOB, static_cast<double>(noob));
+  if constexpr (MODE == OBS_BUILD) {  // the initial pass's energy and active count (slots PT_MAXUPD, + 1)
+    put(PT_MAXUPD, energy_m);
+    put(PT_MAXUPD + 1, static_cast<double>(nact_m));
+  }
   __syncthreads();
   if (warp == 0) {
-    const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (kG && lane < 6) || (kH && lane >= PT_H && lane < PT_H + 21);
+    const bool used = (lane >= PT_E && lane < PT_MAXUPD) || (kG && lane < 6) || (kH && lane >= PT_H && lane < PT_H + 21) ||
+                      (MODE == OBS_BUILD && lane >= PT_MAXUPD);
     double v = 0.0;
     if (used)
       for (int w = 0; w < NT / 32; ++w) v += red[w][lane];
@@ -1298,7 +1320,9 @@ __global__ void __launch_bounds__(NT) k_finalize(const FinalizeArgs a) {
       } else if (c < 33) {
         if (a.want_h && a.partial) v = tile_sum(a.partial, PT_STRIDE, PT_H + (c - 12), t0, t1, lane, false);
       } else if (c < 36) {
-        if (a.partial) v = tile_sum(a.partial, PT_STRIDE, PT_E + (c - 33), t0, t1, lane, false);
+        // e_slot: the energy and active count sit in other slots (the IC build's initial-pass sums; no oob count)
+        if (a.partial && a.e_slot) v = c < 35 ? tile_sum(a.partial, PT_STRIDE, a.e_slot + (c - 33), t0, t1, lane, false) : 0.0;
+        else if (a.partial) v = tile_sum(a.partial, PT_STRIDE, PT_E + (c - 33), t0, t1, lane, false);
       } else {
         if (a.partial_cf) v = tile_sum(a.partial_cf, 8, 6, t0, t1, lane, true);
       }

@@ -212,6 +212,7 @@ struct FinalizeArgs {
   Status* status;             // or null
   double* fscal;              // F*4 scratch: per-frame {energy, #active, #oob, max update}
   unsigned int* ticket;       // grid ticket (zero between launches)
+  int e_slot;                 // 0 = energy / #active / #oob at PT_E..; else energy, #active at e_slot, e_slot + 1
 };
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 

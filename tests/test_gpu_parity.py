@@ -356,6 +356,36 @@ def test_ic_gradient_sum_variants_match(c1, env, monkeypatch):
     assert_params_close(alt.final_R, ref.final_R, 1e-8)
 
 
+def test_initial_pass_from_the_build_matches_a_separate_pass(c1, monkeypatch):
+    """IcSolver::run's initial pass (solver.cpp:487-495) taken from the build pass's sums (default)
+    against a separate IC pass at the same parameters (PBA_IC_INIT_FROM_BUILD=0): same initial
+    active count and energy, same trajectory; and a begin() after another pass has overwritten the
+    build's partials (ic_gradient) falls back to the separate pass."""
+    st = c1.state
+    cfg = c1.cfg.solver_config(max_iters=6)
+    ref = Handle(st, "gpu").ic_run(cfg)
+    h = Handle(st, "gpu")
+    h.ic_build(cfg)
+    h.ic_gradient()            # an observation pass between build and run
+    h._check(h.b.ic_begin(h.h, None))  # run on the existing build (null config): separate initial pass
+    done = False
+    while not done:
+        _, done = h.iterate()
+    mid = h.end(cfg)
+    monkeypatch.setenv("PBA_IC_INIT_FROM_BUILD", "0")
+    alt = Handle(st, "gpu").ic_run(cfg)
+    for other in (alt, mid):
+        assert other.masked_residuals == ref.masked_residuals and other.iterations == ref.iterations
+        assert [s.accepted for s in other.iters] == [s.accepted for s in ref.iters]
+        assert [s.num_active for s in other.iters] == [s.num_active for s in ref.iters]
+        assert other.hessian_factorizations == ref.hessian_factorizations
+        for x, y in zip(other.iters, ref.iters):
+            assert abs(x.energy - y.energy) <= 1e-10 * abs(y.energy)
+        assert_params_close(other.final_inv_depths, ref.final_inv_depths, 1e-8)
+        assert_params_close(other.final_t, ref.final_t, 1e-8)
+        assert_params_close(other.final_R, ref.final_R, 1e-8)
+
+
 def test_apply_update_and_gauge_substeps(tiny):
     st = tiny.state
     g, o = pair(st)

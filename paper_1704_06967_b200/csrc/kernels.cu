@@ -574,7 +574,7 @@ __device__ __forceinline__ void obs_lane_body(const ObsArgs& a, const FrameTab& 
             r = T.x - bilinear(fr.img, fr.W, u, v);
           }
           act = true;
-          energy += huber_loss(r, gam);
+          if constexpr (MODE != OBS_BUILD) energy += huber_loss(r, gam);  // the build reports the masked energy only
           ++nact;
           if (a.r_out) a.r_out[q * P + k] = r;
           if constexpr (kV2) {

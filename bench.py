@@ -533,6 +533,22 @@ def run_ours(args, rank, world):
                "what": "one ic_solve through the C ABI from pinned host buffers: upload, IC build "
                        "(J rows, H, Schur, Cholesky), LM iterations, download of final parameters"}
 
+        # the FC baseline end to end, same buffers and iteration count (fc_solve, solver.cpp:849-851)
+        if fc is not None and not sharded:
+            solver.fc_solve(st_pin, c2)  # untimed
+            f_px, f_s, f_ms = 0, 0.0, []
+            for _ in range(max(1, min(args.e2e_steps, 2))):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                rep = solver.fc_solve(st_pin, c2)
+                dt = time.perf_counter() - t0
+                f_s += dt
+                f_ms.append(round(1e3 * dt, 2))
+                f_px += sum(it.num_active for it in rep.iters)
+            fc["e2e"] = {"value": f_px / f_s, "unit": "obs_px/s", "ms_per_step": 1e3 * f_s / len(f_ms), "step_ms": f_ms,
+                         "iters_per_step": args.e2e_iters, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                         "what": "one fc_solve through the C ABI from pinned host buffers"}
+
     # ---------------- BASELINE C2: box room, joint window (affine, FC) and per-host restatement ----------------
     c2 = None
     if not args.no_c2 and not sharded:

@@ -702,7 +702,7 @@ def main():
         from tests._oracle import REF_LIB
         if REF_LIB.exists() and rank == 0:  # the unmodified reference on one core, one dense window sample
             kf = min(32, st.num_frames)
-            cpu = reference_threads(st, r["cfg"], kf, args.cpu_points or max(100, int(3.2e6 / (kf * st.pattern.shape[0]))),
+            cpu = reference_threads(st, r["cfg"], kf, args.cpu_points or max(100, int(8e6 / (kf * st.pattern.shape[0]))),
                                     1)
         else:
             cpu = cpu_baseline(st, r["cfg"], min(npts, st.num_points))

@@ -341,14 +341,18 @@ def dense_window_samples(st, frames_per_sample, npts, count, seed=0):
         contiguous = np.diff(st.obs_ptr) == last - first + 1
     out = []
     for _ in range(count):
+        best = None
         for _try in range(64):
             f0 = int(rng.integers(0, F - K + 1))
             ok = np.nonzero(contiguous & (first <= f0) & (last >= f0 + K - 1))[0]
+            if best is None or ok.size > best[1].size:
+                best = (f0, ok)
             if ok.size >= npts:
                 break
-        else:
-            raise RuntimeError("no frame window of the scene has enough fully observed points")
-        idx = np.sort(rng.choice(ok, size=npts, replace=False))
+        f0, ok = best
+        if ok.size == 0:
+            raise RuntimeError("no frame window of the scene has fully observed points")
+        idx = np.sort(rng.choice(ok, size=min(npts, ok.size), replace=False))  # fewer when the scene has fewer
         out.append(solver.ProblemState(st.ref, st.ref_K, st.targets[f0:f0 + K], st.targets_K[f0:f0 + K],
                                        st.R[f0:f0 + K].copy(), st.t[f0:f0 + K].copy(), st.anchors_px[idx].copy(),
                                        st.inv_depths[idx].copy(), st.pattern, None, None))
@@ -387,7 +391,7 @@ def reference_threads(st, cfg, frames_per_sample, npts_per_thread, threads, seed
     return {"value": v, "unit": "obs_px/s", "cores": threads, "kind": "reference",
             "ms_per_iter": ms / max(iters - 1, 1),
             "sample": f"{threads} threads x one dense window each ({subs[0].num_frames} consecutive frames x "
-                      f"{npts_per_thread} points observed in all of them, of {st.num_frames} frames / {st.num_points} "
+                      f"{subs[0].num_points} points observed in all of them, of {st.num_frames} frames / {st.num_points} "
                       f"points), {iters} IC iterations each, {sum(r[2] for r in res)} observations in total; the "
                       f"unmodified reference solver.cpp (oracle/_ref, single-threaded per handle); {wall:.1f} s"}
 
